@@ -1,0 +1,158 @@
+/*
+ * dz_b200.h — C ABI of the B200-native DeltaZip serving hot path.
+ *
+ * The reference (DeltaZip, arXiv 2312.05215; /root/reference/pkg) is a pure
+ * Python/numpy package with no FFI. Each entry point below replaces one
+ * reference function on the serving hot path; the citation names it.
+ * Plain pointers and sizes only: device pointers are CUDA global memory,
+ * `stream` is a cudaStream_t passed as void*. Every call is stream-ordered,
+ * never synchronises the host, allocates nothing and keeps no global mutable
+ * state, so a whole decode step can be captured in a CUDA graph.
+ *
+ * Status codes mirror the reference exception contract (errors.py:8-43).
+ */
+#ifndef DZ_B200_H
+#define DZ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.py) ---------------------------------------------------- */
+#define DZ_OK 0
+#define DZ_E_SHAPE 1       /* ShapeError      errors.py:8   */
+#define DZ_E_ENCODING 2    /* EncodingError   errors.py:12  */
+#define DZ_E_FORMAT 3      /* FormatError     errors.py:24  */
+#define DZ_E_PARTITION 4   /* PartitionError  errors.py:35  */
+#define DZ_E_UNKNOWN 5     /* UnknownDeltaError errors.py:43 */
+#define DZ_E_VALUE 6       /* plain ValueError (e.g. scales reshape, compress.py:484) */
+#define DZ_E_UNSUPPORTED 7 /* layout the called kernel does not take (caller routes elsewhere) */
+#define DZ_E_CUDA 8        /* CUDA runtime error */
+
+/* ---- element types --------------------------------------------------------------- */
+#define DZ_F32 0
+#define DZ_BF16 1
+#define DZ_F64 2   /* K1 only: exact f64 product, bit-identical to dequantize_layer */
+
+/* ---- fused epilogue activations (dz_sbmm) ------------------------------------------ */
+#define DZ_ACT_NONE 0
+#define DZ_ACT_TANH 1   /* forward_model's tanh between layers (inference.py:288-289) */
+
+/* ---- delta kinds held in a device delta table ------------------------------------ */
+#define DZ_KIND_SPARSE4 1  /* 2:4, codes as 4-bit fields (bits 3 or 4), native blocks */
+#define DZ_KIND_SPARSE2 2  /* 2:4, codes as 2-bit fields (bits 2), native blocks     */
+#define DZ_KIND_DENSE 3    /* dequantised bf16 ΔW in the dense native block layout   */
+
+/* One layer delta in the REFERENCE packed layout (LayerDelta, compress.py:101-143),
+ * all pointers device-resident, bytes exactly as the reference stores them. */
+typedef struct dz_ref_delta {
+  const uint32_t* packed;   /* packed_values, <u4                                  */
+  int64_t n_words;
+  const uint8_t* index;     /* index_stream (NULL / 0 bytes when sparsity="none")  */
+  int64_t index_bytes;
+  const float* scales;      /* scales <f4, (rows, n_groups) row-major; may be empty */
+  int64_t n_scales;
+  int32_t rows, cols, bits, sparse, group_size, _pad;
+} dz_ref_delta;
+
+/* One entry of a device delta table consumed by dz_sbmm. */
+typedef struct dz_native_delta {
+  const void* blocks;       /* native blocks (dz_repack_sparse / dz_pack_dense_bf16) */
+  int32_t kind;             /* DZ_KIND_*                                             */
+  int32_t qmax;             /* code offset: u - qmax = code (compress.py:265-277)     */
+  int32_t rows, cols;
+} dz_native_delta;
+
+/* One unit of SBMM work over a row tile (built by dz_plan). */
+typedef struct dz_job {
+  int32_t slot;             /* delta-table index; -1 = base GEMM over all tokens     */
+  int32_t tok_begin;        /* first position in `order` (delta) or token (base)     */
+  int32_t tok_count;        /* <= 64 (base / dense) or <= 16 (sparse)                */
+  int32_t kind;             /* 0 = base, else DZ_KIND_* of the slot                  */
+} dz_job;
+
+typedef struct dz_sbmm_args {
+  const uint16_t* X;        /* bf16 [T][ldx]; columns in..ceil128(in) must be zero  */
+  int64_t ldx;
+  void* Y;                  /* [T][ldy] of y_dtype                                   */
+  int64_t ldy;
+  int32_t y_dtype;          /* DZ_F32 or DZ_BF16                                     */
+  int32_t act;              /* DZ_ACT_*, applied to y = base + delta in the epilogue */
+  int32_t T, out, in;
+  const void* base;         /* dense native blocks of W_base [out][in] (NULL: no base) */
+  const dz_native_delta* table; /* device array [n_slots]                            */
+  int32_t n_slots;
+  const int32_t* order;     /* device [T]: token indices stably sorted by slot       */
+  const dz_job* jobs;       /* device [n_jobs]                                       */
+  int32_t n_jobs;
+  void* workspace;          /* dz_sbmm_workspace_bytes(T, out) bytes; counters must be
+                               zero the first time (they self-reset after every call) */
+  int32_t grid;             /* persistent CTAs; 0 = one per SM                       */
+} dz_sbmm_args;
+
+const char* dz_version(void);
+const char* dz_strerror(int status);
+
+/* K1 — bit-exact unpack. Replaces compress.dequantize_layer (compress.py:467-497),
+ * with unpack_codes (:265-277), decode_mask_indices (:295-314) and
+ * _float64_unpayload (:343-345). out = [rows][ld_out] of out_dtype; fp32 output is
+ * bit-identical to np.float32(dequantize_layer(ld)), bf16 to torch .to(bfloat16).
+ * A corrupt nibble (p0 >= p1) sets *err_flag (device int) to DZ_E_FORMAT. */
+int dz_unpack(const dz_ref_delta* d, int out_dtype, void* out, int64_t ld_out,
+              int* err_flag, void* stream);
+
+/* Pieces of K1 exposed for the codec API: unpack_codes (compress.py:265-277) into
+ * int32 codes, and decode_mask_indices (compress.py:295-314) into a uint8 keep mask
+ * [rows][cols]. Same error contract (host-checked lengths, *err_flag on bad nibble). */
+int dz_unpack_codes(const uint32_t* words, int64_t n_words, int32_t bits, int64_t count,
+                    int32_t* out, void* stream);
+int dz_decode_index(const uint8_t* index, int64_t index_bytes, int32_t rows, int32_t cols,
+                    uint8_t* keep, int* err_flag, void* stream);
+
+/* Upload-time re-layout of a 2:4 delta (bits 2/3/4, group_size % 128 == 0 or one
+ * group per row) into 16x128 native blocks: the same codes, index nibbles and
+ * scales, arranged as mma.sp fragments. Lossless (dz_unpack_native inverts it);
+ * validates every index nibble like decode_mask_indices (compress.py:307-309). */
+int64_t dz_native_sparse_bytes(int32_t rows, int32_t cols, int32_t bits);
+int dz_repack_sparse(const dz_ref_delta* d, void* native_out, int* err_flag, void* stream);
+/* Inverse view of a native sparse delta, for parity checks of the re-layout. */
+int dz_unpack_native(const void* native, int32_t rows, int32_t cols, int32_t bits,
+                     int32_t qmax, float* out, int64_t ld_out, void* stream);
+
+/* Dense bf16 [rows][ldw] -> dense native blocks (base weight, or a dequantised delta
+ * that the sparse kernel does not take). */
+int64_t dz_native_dense_bytes(int32_t rows, int32_t cols);
+int dz_pack_dense_bf16(const uint16_t* W, int64_t ldw, int32_t rows, int32_t cols,
+                       void* native_out, void* stream);
+
+/* Copy X [T][in] (ldx) into a zero-padded [T][ldp] buffer, ldp = ceil128(in). */
+int dz_pad_x(const uint16_t* X, int64_t ldx, int32_t T, int32_t in, uint16_t* Xp,
+             int64_t ldp, void* stream);
+
+/* Host-side plan. Replaces inference.group_by_delta (inference.py:106-123): stable
+ * sort of token rows by slot, then cut into dz_jobs. kinds[n_slots] gives each
+ * slot's DZ_KIND_*. Returns DZ_E_UNKNOWN when a slot is out of range
+ * (inference.py:135-137). max_jobs >= dz_plan_max_jobs(T). */
+int32_t dz_plan_max_jobs(int32_t T);
+int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t n_slots,
+            int32_t with_base, int32_t* order_out, dz_job* jobs_out, int32_t max_jobs,
+            int32_t* n_jobs_out);
+
+/* K2 — fused decode SBMM. Replaces inference.sbmm (inference.py:126-154):
+ * Y[t] = W_base x_t + ΔW_{slot(t)} x_t for every token in ONE persistent launch:
+ * TMA bulk copies stage native blocks and X through shared memory, warps decode
+ * codes in registers and issue mma.sp (2:4) / mma (dense) with fp32 accumulation,
+ * per-(row,128-col) scales are applied per block, and the base and delta partials
+ * are combined by the last work item of each row tile (no separate add kernel).
+ * Deterministic and batch-invariant: a token's result does not depend on the
+ * other tokens in the call. */
+size_t dz_sbmm_workspace_bytes(int32_t T, int32_t out);
+int dz_sbmm(const dz_sbmm_args* args, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DZ_B200_H */

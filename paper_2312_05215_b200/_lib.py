@@ -1,0 +1,121 @@
+"""ctypes binding of the C ABI in `include/dz_b200.h` (library `_dz_b200.so`, built in-tree).
+
+There is no CPU fallback: if the library is missing every entry point raises CudaError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import (
+    CudaError, EncodingError, FormatError, PartitionError, ShapeError, UnknownDeltaError,
+)
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_dz_b200.so")
+
+DZ_OK, DZ_E_SHAPE, DZ_E_ENCODING, DZ_E_FORMAT, DZ_E_PARTITION = 0, 1, 2, 3, 4
+DZ_E_UNKNOWN, DZ_E_VALUE, DZ_E_UNSUPPORTED, DZ_E_CUDA = 5, 6, 7, 8
+DZ_F32, DZ_BF16, DZ_F64 = 0, 1, 2
+DZ_ACT_NONE, DZ_ACT_TANH = 0, 1
+DZ_KIND_SPARSE4, DZ_KIND_SPARSE2, DZ_KIND_DENSE = 1, 2, 3
+
+
+class DzRefDelta(C.Structure):
+    _fields_ = [
+        ("packed", C.c_void_p), ("n_words", C.c_int64),
+        ("index", C.c_void_p), ("index_bytes", C.c_int64),
+        ("scales", C.c_void_p), ("n_scales", C.c_int64),
+        ("rows", C.c_int32), ("cols", C.c_int32), ("bits", C.c_int32),
+        ("sparse", C.c_int32), ("group_size", C.c_int32), ("_pad", C.c_int32),
+    ]
+
+
+class DzNativeDelta(C.Structure):
+    _fields_ = [("blocks", C.c_void_p), ("kind", C.c_int32), ("qmax", C.c_int32),
+                ("rows", C.c_int32), ("cols", C.c_int32)]
+
+
+class DzJob(C.Structure):
+    _fields_ = [("slot", C.c_int32), ("tok_begin", C.c_int32), ("tok_count", C.c_int32),
+                ("kind", C.c_int32)]
+
+
+class DzSbmmArgs(C.Structure):
+    _fields_ = [
+        ("X", C.c_void_p), ("ldx", C.c_int64),
+        ("Y", C.c_void_p), ("ldy", C.c_int64),
+        ("y_dtype", C.c_int32), ("act", C.c_int32),
+        ("T", C.c_int32), ("out", C.c_int32), ("in_", C.c_int32),
+        ("base", C.c_void_p),
+        ("table", C.c_void_p), ("n_slots", C.c_int32),
+        ("order", C.c_void_p),
+        ("jobs", C.c_void_p), ("n_jobs", C.c_int32),
+        ("workspace", C.c_void_p),
+        ("grid", C.c_int32),
+    ]
+
+
+# symbol -> (restype, argtypes); every symbol include/dz_b200.h declares
+SIGNATURES = {
+    "dz_version": (C.c_char_p, []),
+    "dz_strerror": (C.c_char_p, [C.c_int]),
+    "dz_unpack": (C.c_int, [C.POINTER(DzRefDelta), C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "dz_unpack_codes": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p]),
+    "dz_decode_index": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                  C.c_void_p]),
+    "dz_native_sparse_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
+    "dz_repack_sparse": (C.c_int, [C.POINTER(DzRefDelta), C.c_void_p, C.c_void_p, C.c_void_p]),
+    "dz_unpack_native": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                   C.c_int64, C.c_void_p]),
+    "dz_native_dense_bytes": (C.c_int64, [C.c_int32, C.c_int32]),
+    "dz_pack_dense_bf16": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
+    "dz_pad_x": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p]),
+    "dz_plan_max_jobs": (C.c_int32, [C.c_int32]),
+    "dz_plan": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                          C.c_int32, C.POINTER(C.c_int32)]),
+    "dz_sbmm_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int32]),
+    "dz_sbmm": (C.c_int, [C.POINTER(DzSbmmArgs), C.c_void_p]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load (once) and return the CDLL. Raises CudaError when the extension is absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise CudaError(f"CUDA extension not built: {LIB_PATH} missing (run __graft_entry__.build())")
+        try:
+            L = C.CDLL(LIB_PATH)
+        except OSError as e:  # pragma: no cover
+            raise CudaError(f"cannot load {LIB_PATH}: {e}") from e
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(status: int, what: str = "") -> None:
+    """Map a DZ_* status to the reference exception class."""
+    if status == DZ_OK:
+        return
+    msg = lib().dz_strerror(status).decode()
+    if what:
+        msg = f"{what}: {msg}"
+    if status == DZ_E_SHAPE:
+        raise ShapeError(msg)
+    if status == DZ_E_ENCODING:
+        raise EncodingError(msg)
+    if status == DZ_E_FORMAT:
+        raise FormatError(msg)
+    if status == DZ_E_PARTITION:
+        raise PartitionError(msg)
+    if status == DZ_E_UNKNOWN:
+        raise UnknownDeltaError(msg)
+    if status in (DZ_E_VALUE, DZ_E_UNSUPPORTED):
+        raise ValueError(msg)
+    raise CudaError(msg)

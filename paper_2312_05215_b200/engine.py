@@ -1,0 +1,217 @@
+"""Device-resident serving objects and the throughput API over the fused SBMM kernel (K2).
+
+- `NativeDelta`  one layer delta uploaded once: the reference bytes are copied to HBM, every index
+                 nibble is validated (FormatError here, at load time), and 2:4 deltas with 2/3/4-bit
+                 codes are re-laid out into mma.sp-native 16x128 blocks (same bytes per parameter).
+                 Other variants (dense, 8/16-bit, odd group sizes) are dequantised on the GPU (K1)
+                 to bf16 and stored as dense native blocks — still GPU, never a CPU path.
+- `NativeBase`   the shared base weight W [out, in] in dense native blocks.
+- `DeltaTable`   the device table of NativeDeltas one linear layer can route tokens to.
+- `Plan`         the batch plan (group_by_delta, inference.py:106-123) for one token->slot map;
+                 shared by every linear of a decode step.
+- `sbmm_forward` Y = X W^T + SBMM(X, ΔW_slot) in one persistent launch.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .compress import SPARSITY_2_4, dequantize_layer_device
+from .device import ErrFlag, RefDeltaDevice, require_cuda, stream_ptr
+from .errors import ShapeError, UnknownDeltaError
+
+BLK_ROWS, BLK_COLS = 16, 128
+
+
+def _ceil(a: int, b: int) -> int:
+    return -(-a // b)
+
+
+class NativeDelta:
+    """One LayerDelta resident on the GPU in kernel-native form."""
+
+    def __init__(self, kind: int, qmax: int, rows: int, cols: int, blocks: torch.Tensor, bits: int):
+        self.kind, self.qmax, self.rows, self.cols, self.blocks, self.bits = kind, qmax, rows, cols, blocks, bits
+
+    @property
+    def nbytes(self) -> int:
+        return self.blocks.numel()
+
+    @staticmethod
+    def sparse_native_ok(ld) -> bool:
+        ng = _ceil(int(ld.cols), int(ld.group_size))
+        return (ld.sparsity == SPARSITY_2_4 and int(ld.bits) in (2, 3, 4)
+                and (int(ld.group_size) % BLK_COLS == 0 or ng == 1))
+
+    @classmethod
+    def from_layer_delta(cls, ld, device=None) -> "NativeDelta":
+        dev = device or require_cuda()
+        ref = RefDeltaDevice(ld, dev)
+        lib = L.lib()
+        err = ErrFlag(dev)
+        if cls.sparse_native_ok(ld):
+            nbytes = lib.dz_native_sparse_bytes(ref.rows, ref.cols, ref.bits)
+            blocks = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            L.check(lib.dz_repack_sparse(ref.struct, blocks.data_ptr(), err.ptr, stream_ptr()), "upload delta")
+            err.raise_if_set("corrupt index stream: kept positions not strictly increasing")
+            kind = L.DZ_KIND_SPARSE2 if ref.bits == 2 else L.DZ_KIND_SPARSE4
+            return cls(kind, (1 << (ref.bits - 1)) - 1, ref.rows, ref.cols, blocks, ref.bits)
+        dense = dequantize_layer_device(ld, torch.bfloat16, ref=ref)  # raises FormatError / EncodingError
+        return cls.from_dense_bf16(dense, bits=ref.bits)
+
+    @classmethod
+    def from_dense_bf16(cls, W: torch.Tensor, bits: int = 16) -> "NativeDelta":
+        blocks = pack_dense(W)
+        return cls(L.DZ_KIND_DENSE, 0, W.shape[0], W.shape[1], blocks, bits)
+
+    def to_dense_f32(self) -> torch.Tensor:
+        """Inverse view (parity check of the re-layout)."""
+        out = torch.empty(self.rows, self.cols, dtype=torch.float32, device=self.blocks.device)
+        if self.kind == L.DZ_KIND_DENSE:
+            raise ValueError("dense native deltas are already bf16 matrices")
+        L.check(L.lib().dz_unpack_native(self.blocks.data_ptr(), self.rows, self.cols, self.bits, self.qmax,
+                                         out.data_ptr(), self.cols, stream_ptr()), "unpack_native")
+        return out
+
+
+def pack_dense(W: torch.Tensor) -> torch.Tensor:
+    if W.dim() != 2 or W.dtype != torch.bfloat16 or not W.is_cuda:
+        raise ShapeError("pack_dense expects a 2-D bf16 CUDA tensor")
+    W = W.contiguous()
+    rows, cols = W.shape
+    nbytes = L.lib().dz_native_dense_bytes(rows, cols)
+    blocks = torch.empty(nbytes, dtype=torch.uint8, device=W.device)
+    L.check(L.lib().dz_pack_dense_bf16(W.data_ptr(), W.stride(0), rows, cols, blocks.data_ptr(), stream_ptr()),
+            "pack base")
+    return blocks
+
+
+class NativeBase:
+    """Shared base weight W_base [out, in] (bf16) in dense native blocks."""
+
+    def __init__(self, W: torch.Tensor):
+        self.out, self.inp = int(W.shape[0]), int(W.shape[1])
+        self.blocks = pack_dense(W)
+
+    @property
+    def nbytes(self) -> int:
+        return self.out * self.inp * 2  # algorithmic bytes (the pad is not counted)
+
+
+class DeltaTable:
+    """Device table of the deltas one linear layer serves (slot i -> deltas[i])."""
+
+    def __init__(self, deltas: list[NativeDelta], out: int, inp: int):
+        for d in deltas:
+            if (d.rows, d.cols) != (out, inp):
+                raise ShapeError(f"delta shape ({d.rows}, {d.cols}) != base ({out}, {inp})")
+        self.deltas = list(deltas)
+        self.out, self.inp = out, inp
+        n = max(1, len(deltas))
+        arr = (L.DzNativeDelta * n)()
+        for i, d in enumerate(deltas):
+            arr[i] = L.DzNativeDelta(d.blocks.data_ptr(), d.kind, d.qmax, d.rows, d.cols)
+        raw = np.frombuffer(C.string_at(C.addressof(arr), C.sizeof(arr)), dtype=np.uint8).copy()
+        dev = deltas[0].blocks.device if deltas else require_cuda()
+        self.dev = torch.from_numpy(raw).to(dev)
+        self.kinds = np.array([d.kind for d in deltas] or [L.DZ_KIND_SPARSE4], dtype=np.int32)
+
+    def __len__(self) -> int:
+        return len(self.deltas)
+
+
+class Plan:
+    """Batch plan: stable sort of tokens by slot + job list (dz_plan), uploaded to the device."""
+
+    def __init__(self, slots, kinds: np.ndarray, n_slots: int, with_base: bool = True, device=None):
+        s = np.ascontiguousarray(np.asarray(slots, dtype=np.int32).ravel())
+        self.T = int(s.size)
+        lib = L.lib()
+        maxj = lib.dz_plan_max_jobs(self.T)
+        order = np.zeros(max(self.T, 1), dtype=np.int32)
+        jobs = (L.DzJob * max(maxj, 1))()
+        nj = C.c_int32(0)
+        kinds = np.ascontiguousarray(kinds, dtype=np.int32)
+        st = lib.dz_plan(s.ctypes.data, self.T, kinds.ctypes.data, n_slots, 1 if with_base else 0,
+                         order.ctypes.data, jobs, maxj, C.byref(nj))
+        if st == L.DZ_E_UNKNOWN:
+            raise UnknownDeltaError("a token references a slot outside the delta table")
+        L.check(st, "plan")
+        self.n_jobs = int(nj.value)
+        self.order_host = order[: self.T].copy()
+        self.jobs_host = np.frombuffer(C.string_at(C.addressof(jobs), C.sizeof(L.DzJob) * max(self.n_jobs, 1)),
+                                       dtype=np.int32).reshape(-1, 4)[: self.n_jobs].copy()
+        dev = device or require_cuda()
+        self.order = torch.from_numpy(order).to(dev)
+        self.jobs = torch.from_numpy(np.frombuffer(C.string_at(C.addressof(jobs), C.sizeof(L.DzJob) * max(maxj, 1)),
+                                                   dtype=np.uint8).copy()).to(dev)
+        self.with_base = with_base
+
+
+class Workspace:
+    """Per-(T, out) scratch for the fused kernel: scheduler + tile counters (zeroed once; the
+    kernel resets them itself) and the fp32 partial buffers."""
+
+    def __init__(self):
+        self._bufs: dict[tuple, torch.Tensor] = {}
+
+    def get(self, T: int, out: int, device) -> torch.Tensor:
+        need = int(L.lib().dz_sbmm_workspace_bytes(T, out))
+        key = (str(device),)
+        buf = self._bufs.get(key)
+        if buf is None or buf.numel() < need:
+            buf = torch.zeros(max(need, 256), dtype=torch.uint8, device=device)
+            self._bufs[key] = buf
+        return buf
+
+
+_default_ws = Workspace()
+
+
+def prepare_x(X: torch.Tensor) -> torch.Tensor:
+    """Kernel contract: bf16, row stride >= ceil128(in), zero columns in..ceil128(in), 16 B aligned."""
+    if X.dim() != 2 or X.dtype != torch.bfloat16 or not X.is_cuda:
+        raise ShapeError("X must be a 2-D bf16 CUDA tensor [T, in]")
+    T, inp = X.shape
+    ldp = _ceil(inp, BLK_COLS) * BLK_COLS
+    if ldp == inp and X.stride(1) == 1 and X.stride(0) % 8 == 0 and X.data_ptr() % 16 == 0:
+        return X
+    Xp = torch.empty(T, ldp, dtype=torch.bfloat16, device=X.device)
+    L.check(L.lib().dz_pad_x(X.data_ptr(), X.stride(0), T, inp, Xp.data_ptr(), ldp, stream_ptr()), "pad x")
+    return Xp
+
+
+def sbmm_forward(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: DeltaTable,
+                 y_dtype: torch.dtype = torch.bfloat16, act: int = L.DZ_ACT_NONE, Y: torch.Tensor | None = None,
+                 workspace: Workspace | None = None, grid: int = 0) -> torch.Tensor:
+    """Y[T, out] = X W_base^T + ΔW_{slot(t)} x_t for all t, one fused launch (inference.py:126-154)."""
+    T, inp = int(X.shape[0]), int(X.shape[1])
+    out = table.out if base is None else base.out
+    if base is not None and (base.out, base.inp) != (table.out, table.inp):
+        raise ShapeError("base / delta table shape mismatch")
+    if inp != table.inp:
+        raise ShapeError(f"input dim {inp} != layer in {table.inp}")
+    if T != plan.T:
+        raise ShapeError("plan built for a different batch")
+    Xp = prepare_x(X)
+    if Y is None:
+        Y = torch.empty(T, out, dtype=y_dtype, device=X.device)
+    ws = (workspace or _default_ws).get(T, out, X.device)
+    a = L.DzSbmmArgs()
+    a.X, a.ldx = Xp.data_ptr(), Xp.stride(0)
+    a.Y, a.ldy = Y.data_ptr(), Y.stride(0)
+    a.y_dtype = L.DZ_F32 if Y.dtype == torch.float32 else L.DZ_BF16
+    a.act = act
+    a.T, a.out, a.in_ = T, out, inp
+    a.base = base.blocks.data_ptr() if base is not None else None
+    a.table, a.n_slots = table.dev.data_ptr(), len(table)
+    a.order = plan.order.data_ptr()
+    a.jobs, a.n_jobs = plan.jobs.data_ptr(), plan.n_jobs
+    a.workspace = ws.data_ptr()
+    a.grid = grid
+    L.check(L.lib().dz_sbmm(C.byref(a), stream_ptr()), "sbmm")
+    return Y
