@@ -42,9 +42,11 @@ extern "C" {
 #define DZ_ACT_TANH 1   /* forward_model's tanh between layers (inference.py:288-289) */
 
 /* ---- delta kinds held in a device delta table ------------------------------------ */
-#define DZ_KIND_SPARSE4 1  /* 2:4, codes as 4-bit fields (bits 3 or 4), native blocks */
-#define DZ_KIND_SPARSE2 2  /* 2:4, codes as 2-bit fields (bits 2), native blocks     */
-#define DZ_KIND_DENSE 3    /* dequantised bf16 ΔW in the dense native block layout   */
+#define DZ_KIND_SPARSE4 1  /* 2:4, 4-bit codes (qmax 7) in native blocks                */
+#define DZ_KIND_SPARSE2 2  /* 2:4, 2-bit codes (qmax 1) in native blocks                */
+#define DZ_KIND_DENSE 3    /* bf16 matrix in the dense native block layout (base weight, or
+                              a delta variant the sparse path does not take, dequantised) */
+#define DZ_KIND_SPARSE3 4  /* 2:4, 3-bit codes (qmax 3) held in 4-bit fields           */
 
 /* One layer delta in the REFERENCE packed layout (LayerDelta, compress.py:101-143),
  * all pointers device-resident, bytes exactly as the reference stores them. */
@@ -58,12 +60,15 @@ typedef struct dz_ref_delta {
   int32_t rows, cols, bits, sparse, group_size, _pad;
 } dz_ref_delta;
 
-/* One entry of a device delta table consumed by dz_sbmm. */
+/* One entry of a device delta table consumed by dz_sbmm (192 bytes; arrays of entries must be
+ * 64-byte aligned). Fill it on the host with dz_native_delta_init, then copy it to the device. */
 typedef struct dz_native_delta {
   const void* blocks;       /* native blocks (dz_repack_sparse / dz_pack_dense_bf16) */
   int32_t kind;             /* DZ_KIND_*                                             */
   int32_t qmax;             /* code offset: u - qmax = code (compress.py:265-277)     */
   int32_t rows, cols;
+  uint8_t _reserved[40];
+  uint64_t tmap[16];        /* TMA descriptor (CUtensorMap) of `blocks` as a 2-D array */
 } dz_native_delta;
 
 /* One unit of SBMM work over a row tile (built by dz_plan). */
@@ -82,7 +87,7 @@ typedef struct dz_sbmm_args {
   int32_t y_dtype;          /* DZ_F32 or DZ_BF16                                     */
   int32_t act;              /* DZ_ACT_*, applied to y = base + delta in the epilogue */
   int32_t T, out, in;
-  const void* base;         /* dense native blocks of W_base [out][in] (NULL: no base) */
+  const dz_native_delta* base; /* device entry (dz_base_init) of W_base [out][in], or NULL */
   const dz_native_delta* table; /* device array [n_slots]                            */
   int32_t n_slots;
   const int32_t* order;     /* device [T]: token indices stably sorted by slot       */
@@ -127,6 +132,16 @@ int dz_unpack_native(const void* native, int32_t rows, int32_t cols, int32_t bit
 int64_t dz_native_dense_bytes(int32_t rows, int32_t cols);
 int dz_pack_dense_bf16(const uint16_t* W, int64_t ldw, int32_t rows, int32_t cols,
                        void* native_out, void* stream);
+
+/* Host: fill the entry of a base weight W [rows][cols] bf16 (row stride ldw elements, 16-byte
+ * aligned rows). The fused kernel streams W in its natural layout with 128B-swizzled TMA tiles
+ * straight into tcgen05 MMAs — no re-layout of the base model. */
+int dz_base_init(dz_native_delta* entry, const uint16_t* W, int64_t ldw, int32_t rows, int32_t cols);
+
+/* Host: fill a table entry, encoding the TMA descriptor the fused kernel streams `blocks`
+ * with (kind DZ_KIND_*; rows/cols of the layer). */
+int dz_native_delta_init(dz_native_delta* entry, const void* blocks, int32_t kind, int32_t rows,
+                         int32_t cols);
 
 /* Copy X [T][in] (ldx) into a zero-padded [T][ldp] buffer, ldp = ceil128(in). */
 int dz_pad_x(const uint16_t* X, int64_t ldx, int32_t T, int32_t in, uint16_t* Xp,

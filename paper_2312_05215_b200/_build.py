@@ -27,7 +27,12 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, trace: bool = False) -> str:
+    """Build `_dz_b200.so` (or the DZ_TRACE-instrumented `_dz_b200_trace.so` for tools/trace.py)."""
+    global LIB, BUILD
+    if trace:
+        LIB = os.path.join(PKG, "_dz_b200_trace.so")
+        BUILD = os.path.join(ROOT, "build", "obj_trace")
     os.makedirs(BUILD, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "dz_b200.h"))
@@ -37,7 +42,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         obj = os.path.join(BUILD, src + ".o")
         objs.append(obj)
         if force or _stale(obj, [path] + headers):
-            cmd = [NVCC, *ARCH, *NVFLAGS, "-c", path, "-o", obj]
+            cmd = [NVCC, *ARCH, *NVFLAGS, *(["-DDZ_TRACE"] if trace else []), "-c", path, "-o", obj]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:
                 sys.stderr.write(r.stdout + r.stderr)
@@ -54,4 +59,4 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(verbose=True, force="--force" in sys.argv))
+    print(build(verbose=True, force="--force" in sys.argv, trace="--trace" in sys.argv))

@@ -12,13 +12,13 @@ from .errors import (
     CudaError, EncodingError, FormatError, PartitionError, ShapeError, UnknownDeltaError,
 )
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_dz_b200.so")
+LIB_PATH = os.environ.get("DZ_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_dz_b200.so")
 
 DZ_OK, DZ_E_SHAPE, DZ_E_ENCODING, DZ_E_FORMAT, DZ_E_PARTITION = 0, 1, 2, 3, 4
 DZ_E_UNKNOWN, DZ_E_VALUE, DZ_E_UNSUPPORTED, DZ_E_CUDA = 5, 6, 7, 8
 DZ_F32, DZ_BF16, DZ_F64 = 0, 1, 2
 DZ_ACT_NONE, DZ_ACT_TANH = 0, 1
-DZ_KIND_SPARSE4, DZ_KIND_SPARSE2, DZ_KIND_DENSE = 1, 2, 3
+DZ_KIND_SPARSE4, DZ_KIND_SPARSE2, DZ_KIND_DENSE, DZ_KIND_SPARSE3 = 1, 2, 3, 4
 
 
 class DzRefDelta(C.Structure):
@@ -33,7 +33,8 @@ class DzRefDelta(C.Structure):
 
 class DzNativeDelta(C.Structure):
     _fields_ = [("blocks", C.c_void_p), ("kind", C.c_int32), ("qmax", C.c_int32),
-                ("rows", C.c_int32), ("cols", C.c_int32)]
+                ("rows", C.c_int32), ("cols", C.c_int32), ("_reserved", C.c_uint8 * 40),
+                ("tmap", C.c_uint64 * 16)]
 
 
 class DzJob(C.Structure):
@@ -70,6 +71,8 @@ SIGNATURES = {
                                    C.c_int64, C.c_void_p]),
     "dz_native_dense_bytes": (C.c_int64, [C.c_int32, C.c_int32]),
     "dz_pack_dense_bf16": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
+    "dz_base_init": (C.c_int, [C.POINTER(DzNativeDelta), C.c_void_p, C.c_int64, C.c_int32, C.c_int32]),
+    "dz_native_delta_init": (C.c_int, [C.POINTER(DzNativeDelta), C.c_void_p, C.c_int32, C.c_int32, C.c_int32]),
     "dz_pad_x": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p]),
     "dz_plan_max_jobs": (C.c_int32, [C.c_int32]),
     "dz_plan": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,

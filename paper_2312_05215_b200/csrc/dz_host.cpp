@@ -50,7 +50,8 @@ extern "C" int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, in
     const int32_t c = count[s + 1] - count[s];
     if (c == 0) continue;
     const int32_t kind = kinds[s];
-    if (kind != DZ_KIND_SPARSE4 && kind != DZ_KIND_SPARSE2 && kind != DZ_KIND_DENSE) return DZ_E_VALUE;
+    if (kind != DZ_KIND_SPARSE4 && kind != DZ_KIND_SPARSE2 && kind != DZ_KIND_SPARSE3 && kind != DZ_KIND_DENSE)
+      return DZ_E_VALUE;
     const int32_t chunk = kind == DZ_KIND_DENSE ? 64 : 16;
     for (int32_t off = 0; off < c; off += chunk)
       if (!push(s, start[s] + off, (c - off) < chunk ? (c - off) : chunk, kind)) return DZ_E_VALUE;

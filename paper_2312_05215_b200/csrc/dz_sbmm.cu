@@ -2,165 +2,283 @@
 //
 // Replaces inference.sbmm (inference.py:126-154): y_t = W_base x_t + ΔW_{slot(t)} x_t.
 //
-// Work decomposition. An item is (row tile of RT=128 output rows, job); a job is either the
-// base GEMM for up to 64 tokens or one delta group for up to 16 (sparse) / 64 (dense) of its
-// tokens (dz_plan, the group_by_delta of inference.py:106-123). Persistent CTAs pull items from
-// an atomic counter. Per CTA: warp NW is the producer — it TMA-bulk-copies the native blocks of
-// its item (one contiguous copy per 16-row group per chunk) and the X rows of the job's tokens
-// into a 4-stage shared-memory ring; warps 0..NW-1 each own 16 rows, decode codes in registers
-// (LOP3 magic-number bf16 conversion, deferred per-(row,128-col) scaling) and issue mma.sp
-// m16n8k32 (2:4 deltas, the index nibble IS the sparse metadata) or mma m16n8k16 (base, dense
-// deltas), fp32 accumulation. At the end of an item each warp writes its fp32 partial
-// (base -> Pb, delta -> Pd; tokens are disjoint across delta jobs) and the LAST item of a row
-// tile (per-tile counter) writes Y = Pb + Pd — no separate add kernel, no atomics on data,
-// deterministic and batch-invariant (a token's K order never depends on the batch).
+// Work decomposition. An item is (row tile of RT=128 output rows, job); a job is either the base
+// GEMM for up to 64 tokens or one delta group for up to 16 (sparse) / 64 (dense) of its tokens
+// (dz_plan = group_by_delta, inference.py:106-123). Items are ordered job-major (all base items
+// first, the big ones) and pulled by persistent CTAs from an atomic counter (2 CTAs per SM).
+//
+// Warp roles per CTA:
+//  * producer (1 warp): per chunk ONE 2-D TMA tensor copy of the item's A operand — the base W
+//    tile in its natural layout (128 rows x 64 cols, SWIZZLE_128B), or the delta's native blocks
+//    viewed as a 2-D uint64 array — plus the X tile: one swizzled tensor copy for the base
+//    (contiguous tokens, OOB rows zero-filled) or one 1-D bulk copy per routed token for a delta.
+//    Stages form a 4-deep shared-memory ring with full/empty mbarriers.
+//  * MMA issuer (1 warp, one elected thread): base stages become tcgen05.mma kind::f16
+//    (M=128 rows, N=64 tokens, K=16 x 4 per stage) into a double-buffered TMEM accumulator;
+//    tcgen05.commit frees the stage and, on the last chunk, signals the accumulator full.
+//  * consumers (4 warps, two 16-row groups each): 2:4 delta stages — decode codes in registers
+//    (LOP3 magic-number bf16 conversion; deferred per-(row,128-col) scaling) and mma.sp m16n8k32
+//    (the reference's index nibble IS the sparse-MMA metadata), fp32 accumulation; dense-delta
+//    stages use mma m16n8k16. They also drain the base accumulator from TMEM (tcgen05.ld).
+//
+// At the end of an item the consumers write its fp32 partial (base -> Pb, delta -> Pd; tokens
+// are disjoint across delta jobs) and the LAST item of a row tile (per-tile counter, acq_rel
+// atomic) writes Y = act(Pb + Pd) — no separate add kernel, no atomics on data, deterministic, and
+// batch-invariant (a token's K order never depends on the rest of the batch).
+#include <cuda.h>
+
+#include <cstddef>
 #include <cstdio>
+#include <cstring>
 #include <mutex>
 
 #include "dz_common.cuh"
 
+#ifdef DZ_TRACE
+__device__ unsigned long long dz_trace_buf[8192][4];
+__device__ int dz_trace_n;
+__device__ volatile int dz_trace_cta = -1;  // the CTA that took item 0
+#define TRACE(ev, a0, a1) do { if (static_cast<int>(blockIdx.x) == dz_trace_cta) { \
+  int _i = atomicAdd(&dz_trace_n, 1); \
+  if (_i < 8192) { dz_trace_buf[_i][0] = dz::globaltimer(); dz_trace_buf[_i][1] = (ev); \
+  dz_trace_buf[_i][2] = (a0); dz_trace_buf[_i][3] = (a1); } } } while (0)
+#else
+#define TRACE(ev, a0, a1) do {} while (0)
+#endif
+
 namespace dz {
 
-constexpr int NW = 8;                     // consumer warps (16 rows each)
-constexpr int NTHREADS = (NW + 1) * 32;   // + 1 producer warp
-constexpr int RT = NW * kBlkRows;         // rows per item
-constexpr int NB_SP = 4;                  // sparse chunk = 4 blocks = 512 columns
+constexpr int NW = 4;                     // consumer warps per CTA
+constexpr int MR = 2;                     // 16-row groups per consumer warp
+constexpr int WARP_PROD = NW;             // TMA producer warp
+constexpr int WARP_MMA = NW + 1;          // tcgen05 issuer / TMEM owner warp
+constexpr int NTHREADS = (NW + 2) * 32;
+constexpr int RG = NW * MR;               // row groups per item
+constexpr int RT = RG * kBlkRows;         // rows per item (128) == UMMA M
+constexpr int NB_SP = 2;                  // sparse chunk = 2 blocks = 256 columns
 constexpr int NT_SP = 2;                  // n-tiles per sparse job (16 tokens)
 constexpr int NT_DN = 8;                  // n-tiles per dense job (64 tokens)
-constexpr int XS_SP = NB_SP * kBlkCols * 2 + 16;  // smem bytes per staged token row (16 B pad:
-constexpr int XS_DN = kBlkCols * 2 + 16;          //   ldmatrix rows hit distinct bank groups)
-constexpr int A_SP = NW * NB_SP * sparse_block_bytes(4);  // 26624
-constexpr int X_SP = NT_SP * 8 * XS_SP;                   // 16640
-constexpr int A_DN = NW * kDenseBlockBytes;               // 32768
-constexpr int X_DN = NT_DN * 8 * XS_DN;                   // 17408
-constexpr int STAGE_BYTES = (A_SP + X_SP > A_DN + X_DN) ? A_SP + X_SP : A_DN + X_DN;
+constexpr int KC_DN = 64;                 // dense / base chunk = 64 columns
+constexpr int BASE_N = 64;                // tokens per base job == UMMA N
+constexpr int XS_SP = NB_SP * kBlkCols * 2 + 16;  // smem bytes per staged token row; +16 B so the
+constexpr int XS_DN = KC_DN * 2 + 16;             //   8 rows of an ldmatrix hit distinct banks
+constexpr int A_SP = RG * NB_SP * sparse_block_bytes(4);  // 13312
+constexpr int X_SP = NT_SP * 8 * XS_SP;                   // 8448
+constexpr int DN_HALF = kDenseBlockBytes / 2;             // 2048
+constexpr int A_DN = RG * DN_HALF;                        // 16384 == 128 rows x 128 B (base W tile)
+constexpr int X_DN = NT_DN * 8 * XS_DN;                   // 9216 (>= 64 x 128 B swizzled X tile)
+constexpr int STAGE_BYTES = ((A_SP + X_SP > A_DN + X_DN ? A_SP + X_SP : A_DN + X_DN) + 1023) / 1024 * 1024;
 constexpr int NSTAGE = 4;
 constexpr int JOB_DN_TOK = NT_DN * 8;
 constexpr int kMaxTiles = 4096;           // row tiles per call (out <= 524288)
+constexpr int TMEM_COLS = 2 * BASE_N;     // two fp32 accumulators (double buffer)
+constexpr uint32_t IDESC_BASE = umma_idesc_bf16(RT, BASE_N);
 
 struct StageHdr {
-  int item;   // -1: end of work
-  int chunk;
-  int nb;     // blocks (of 128 columns) in this chunk
+  int item;       // -1: end of work
+  int rt;         // row tile
+  int kind;       // 0 base, DZ_KIND_*
+  int tok_begin;
+  int tok_count;
+  int nb;         // sparse: blocks in chunk; dense: 1
+  int flags;      // bit0: first chunk, bit1: last chunk
   int pad;
 };
 
 struct Smem {
   uint64_t full[NSTAGE];
   uint64_t empty[NSTAGE];
+  uint64_t tmem_full[2];
+  uint64_t tmem_empty[2];
   StageHdr hdr[NSTAGE];
+  uint32_t tmem_base;
   int last_flag;
-  int pad[3];
+  int tok_ids[JOB_DN_TOK];
 };
-constexpr int SMEM_BYTES = STAGE_BYTES * NSTAGE + 1024;
+constexpr int SMEM_BYTES = 1024 + STAGE_BYTES * NSTAGE + static_cast<int>(sizeof(Smem));
 
-struct Geo {
-  int nkb;   // 128-column blocks along K
-  int n16;   // 16-row groups along out
-  int nrt;   // row tiles
-};
+__device__ __forceinline__ bool kind_dense(int kind) { return kind == 0 || kind == DZ_KIND_DENSE; }
 
-__device__ __forceinline__ bool job_dense(int kind) { return kind == 0 || kind == DZ_KIND_DENSE; }
-__device__ __forceinline__ int job_nchunks(int kind, const Geo& geo) {
-  return job_dense(kind) ? geo.nkb : ceil_div(geo.nkb, NB_SP);
-}
-__device__ __forceinline__ int blk_bytes(int kind) {
-  return job_dense(kind) ? kDenseBlockBytes : sparse_block_bytes(kind == DZ_KIND_SPARSE2 ? 2 : 4);
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
 }
 
 // ------------------------------------------------------------------------------------------
-// Consumer math
+// Consumer math (CUDA-core decode + legacy mma.sp / mma)
 // ------------------------------------------------------------------------------------------
 template <int FB>
-__device__ __forceinline__ void sparse_chunk(float (&acc)[NT_SP][4], uint32_t sA, uint32_t xl, int nb, int nt,
-                                             uint32_t off2, int lane) {
+__device__ __forceinline__ void conv_codes(uint32_t (&a)[4], const uint32_t (&cw)[4], int i, uint32_t off2) {
+  if (FB == 4) {
+    const uint32_t w = cw[i];
+#pragma unroll
+    for (int k = 0; k < 4; k++) a[k] = bf16x2_sub(lop3_and_or(w >> (4 * k), 0x000F000Fu, 0x43004300u), off2);
+  } else {
+    const uint32_t w = cw[i >> 1];
+    const int o = 4 * (i & 1);
+#pragma unroll
+    for (int k = 0; k < 4; k++) a[k] = bf16x2_sub(lop3_and_or(w >> (2 * (o + k)), 0x00030003u, 0x43004300u), off2);
+  }
+}
+
+// One sparse chunk (nb <= NB_SP blocks) for this warp's nrv <= MR row groups and NT token tiles.
+template <int FB, int NT>
+__device__ __forceinline__ void sparse_chunk(float (&acc)[MR][NT_DN][4], uint32_t sA, uint32_t xl, int nb,
+                                             int nrv, uint32_t off2, int lane) {
   constexpr int CODE = sparse_code_bytes(FB);
   constexpr int BLK = sparse_block_bytes(FB);
   const int g = lane >> 2;
-#pragma unroll 1
-  for (int b = 0; b < nb; b++) {
-    const uint32_t blk = sA + b * BLK;
-    uint32_t cw[4];
-    if (FB == 4) {
-      const uint4 c = lds128(blk + lane * 16);
-      cw[0] = c.x; cw[1] = c.y; cw[2] = c.z; cw[3] = c.w;
-    } else {
-      const uint2 c = lds64(blk + lane * 8);
-      cw[0] = c.x; cw[1] = c.y; cw[2] = 0; cw[3] = 0;
-    }
-    const uint2 m = lds64(blk + CODE + lane * 8);
-    const uint2 sv = lds64(blk + CODE + kMetaBytes + g * 8);
-    const float s0 = __uint_as_float(sv.x), s1 = __uint_as_float(sv.y);
-    float tmp[NT_SP][4];
+  uint32_t cw[NB_SP][MR][4];
+  uint2 meta[NB_SP][MR];
+  float2 sc[NB_SP][MR];
 #pragma unroll
-    for (int n = 0; n < NT_SP; n++) tmp[n][0] = tmp[n][1] = tmp[n][2] = tmp[n][3] = 0.f;
+  for (int b = 0; b < NB_SP; b++) {
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-      uint32_t a[4];
-      if (FB == 4) {
-        const uint32_t w = cw[i];
-#pragma unroll
-        for (int k = 0; k < 4; k++) a[k] = bf16x2_sub(lop3_and_or(w >> (4 * k), 0x000F000Fu, 0x43004300u), off2);
+    for (int r = 0; r < MR; r++) {
+      // row group r of this warp: NB_SP contiguous blocks at (r*NB_SP + b)*BLK
+      const uint32_t blk = sA + (r * NB_SP + b) * BLK;
+      if (b < nb && r < nrv) {
+        if (FB == 4) {
+          const uint4 c = lds128(blk + lane * 16);
+          cw[b][r][0] = c.x; cw[b][r][1] = c.y; cw[b][r][2] = c.z; cw[b][r][3] = c.w;
+        } else {
+          const uint2 c = lds64(blk + lane * 8);
+          cw[b][r][0] = c.x; cw[b][r][1] = c.y; cw[b][r][2] = 0; cw[b][r][3] = 0;
+        }
+        meta[b][r] = lds64(blk + CODE + lane * 8);
+        const uint2 sv = lds64(blk + CODE + kMetaBytes + g * 8);
+        sc[b][r] = make_float2(__uint_as_float(sv.x), __uint_as_float(sv.y));
       } else {
-        const uint32_t w = cw[i >> 1];
-        const int o = 4 * (i & 1);
-#pragma unroll
-        for (int k = 0; k < 4; k++)
-          a[k] = bf16x2_sub(lop3_and_or(w >> (2 * (o + k)), 0x00030003u, 0x43004300u), off2);
+        cw[b][r][0] = cw[b][r][1] = cw[b][r][2] = cw[b][r][3] = 0;
+        meta[b][r] = make_uint2(0x44444444u, 0x44444444u);
+        sc[b][r] = make_float2(0.f, 0.f);
       }
-      const uint32_t e = (i < 2) ? m.x : m.y;
+    }
+  }
+  float tmp[NB_SP][MR][NT][4];
 #pragma unroll
-      for (int n = 0; n < NT_SP; n++) {
-        if (n < nt) {
-          uint32_t bf[4];
-          ldmatrix_x4(bf, xl + n * 8 * XS_SP + (b * kBlkCols + 32 * i) * 2);
+  for (int b = 0; b < NB_SP; b++)
+#pragma unroll
+    for (int r = 0; r < MR; r++)
+#pragma unroll
+      for (int n = 0; n < NT; n++) tmp[b][r][n][0] = tmp[b][r][n][1] = tmp[b][r][n][2] = tmp[b][r][n][3] = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+#pragma unroll
+    for (int b = 0; b < NB_SP; b++) {
+      if (b >= nb) continue;  // partial last chunk
+      uint32_t bf[NT][4];
+#pragma unroll
+      for (int n = 0; n < NT; n++) ldmatrix_x4(bf[n], xl + n * 8 * XS_SP + (b * kBlkCols + 32 * i) * 2);
+#pragma unroll
+      for (int r = 0; r < MR; r++) {
+        if (r >= nrv) continue;  // padding row group (zero-filled by TMA, never stored)
+        uint32_t a[4];
+        conv_codes<FB>(a, cw[b][r], i, off2);
+        const uint32_t e = (i < 2) ? meta[b][r].x : meta[b][r].y;
+#pragma unroll
+        for (int n = 0; n < NT; n++) {
           if (i & 1)
-            mma_sp_bf16_16832<1>(tmp[n], a, bf, e);
+            mma_sp_bf16_16832<1>(tmp[b][r][n], a, bf[n], e);
           else
-            mma_sp_bf16_16832<0>(tmp[n], a, bf, e);
+            mma_sp_bf16_16832<0>(tmp[b][r][n], a, bf[n], e);
         }
       }
     }
-#pragma unroll
-    for (int n = 0; n < NT_SP; n++) {
-      acc[n][0] = fmaf(s0, tmp[n][0], acc[n][0]);
-      acc[n][1] = fmaf(s0, tmp[n][1], acc[n][1]);
-      acc[n][2] = fmaf(s1, tmp[n][2], acc[n][2]);
-      acc[n][3] = fmaf(s1, tmp[n][3], acc[n][3]);
-    }
   }
+#pragma unroll
+  for (int b = 0; b < NB_SP; b++)
+#pragma unroll
+    for (int r = 0; r < MR; r++)
+#pragma unroll
+      for (int n = 0; n < NT; n++) {
+        acc[r][n][0] = fmaf(sc[b][r].x, tmp[b][r][n][0], acc[r][n][0]);
+        acc[r][n][1] = fmaf(sc[b][r].x, tmp[b][r][n][1], acc[r][n][1]);
+        acc[r][n][2] = fmaf(sc[b][r].y, tmp[b][r][n][2], acc[r][n][2]);
+        acc[r][n][3] = fmaf(sc[b][r].y, tmp[b][r][n][3], acc[r][n][3]);
+      }
 }
 
-__device__ __forceinline__ void dense_chunk(float (&acc)[NT_DN][4], uint32_t sA, uint32_t xl, int nt, int lane) {
+// One dense-delta half-block chunk (64 columns = 4 k16 MMAs); X rows are per-token (XS_DN).
+template <int NT>
+__device__ __forceinline__ void dense_chunk(float (&acc)[MR][NT_DN][4], uint32_t sA, uint32_t sX, int nrv,
+                                            int lane) {
 #pragma unroll
-  for (int jj = 0; jj < 4; jj++) {
-    const uint4 a0v = lds128(sA + (2 * jj) * 512 + lane * 16);
-    const uint4 a1v = lds128(sA + (2 * jj + 1) * 512 + lane * 16);
-    const uint32_t a0[4] = {a0v.x, a0v.y, a0v.z, a0v.w};
-    const uint32_t a1[4] = {a1v.x, a1v.y, a1v.z, a1v.w};
+  for (int jj = 0; jj < 2; jj++) {
+    uint32_t a[MR][2][4];
 #pragma unroll
-    for (int n = 0; n < NT_DN; n++) {
-      if (n < nt) {
-        uint32_t bf[4];
-        ldmatrix_x4(bf, xl + n * 8 * XS_DN + jj * 64);
-        mma_bf16_16816(acc[n], a0, bf[0], bf[1]);
-        mma_bf16_16816(acc[n], a1, bf[2], bf[3]);
+    for (int r = 0; r < MR; r++) {
+#pragma unroll
+      for (int s = 0; s < 2; s++) {
+        const uint4 v = lds128(sA + r * DN_HALF + (2 * jj + s) * 512 + lane * 16);
+        a[r][s][0] = v.x; a[r][s][1] = v.y; a[r][s][2] = v.z; a[r][s][3] = v.w;
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < NT; n++) {
+      uint32_t bf[4];
+      ldmatrix_x4(bf, sX + (n * 8 + (lane & 7)) * XS_DN + ((jj * 4 + (lane >> 3)) << 4));
+#pragma unroll
+      for (int r = 0; r < MR; r++) {
+        if (r >= nrv) continue;
+        mma_bf16_16816(acc[r][n], a[r][0], bf[0], bf[1]);
+        mma_bf16_16816(acc[r][n], a[r][1], bf[2], bf[3]);
       }
     }
   }
 }
 
-template <int NT>
-__device__ __forceinline__ void write_partial(const float (&acc)[NT][4], float* __restrict__ P, int out, int row0,
-                                              int tcount, const int* __restrict__ tok_ids, int lane) {
+__device__ __forceinline__ void dense_dispatch(int nt, float (&acc)[MR][NT_DN][4], uint32_t sA, uint32_t sX,
+                                               int nrv, int lane) {
+  switch (nt) {
+    case 1: dense_chunk<1>(acc, sA, sX, nrv, lane); break;
+    case 2: dense_chunk<2>(acc, sA, sX, nrv, lane); break;
+    case 3: dense_chunk<3>(acc, sA, sX, nrv, lane); break;
+    case 4: dense_chunk<4>(acc, sA, sX, nrv, lane); break;
+    case 5: dense_chunk<5>(acc, sA, sX, nrv, lane); break;
+    case 6: dense_chunk<6>(acc, sA, sX, nrv, lane); break;
+    case 7: dense_chunk<7>(acc, sA, sX, nrv, lane); break;
+    default: dense_chunk<8>(acc, sA, sX, nrv, lane); break;
+  }
+}
+
+__device__ __forceinline__ void write_partial(const float (&acc)[MR][NT_DN][4], int nt, float* __restrict__ P,
+                                              int out, int rg0, int tcount, const int* tok_ids, int lane) {
   const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-  for (int n = 0; n < NT; n++) {
+  for (int r = 0; r < MR; r++) {
+    const int row0 = (rg0 + r) * kBlkRows;
 #pragma unroll
-    for (int v = 0; v < 4; v++) {
-      const int tk = n * 8 + 2 * t + (v & 1);
-      const int r = row0 + g + ((v & 2) ? 8 : 0);
-      if (tk < tcount && r < out) P[static_cast<int64_t>(tok_ids[tk]) * out + r] = acc[n][v];
+    for (int n = 0; n < NT_DN; n++) {
+      if (n < nt) {
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+          const int tk = n * 8 + 2 * t + (v & 1);
+          const int row = row0 + g + ((v & 2) ? 8 : 0);
+          if (tk < tcount && row < out) P[static_cast<int64_t>(tok_ids[tk]) * out + row] = acc[r][n][v];
+        }
+      }
+    }
+  }
+}
+
+// Base accumulator (TMEM, lane = output row, column = token) -> Pb. Warp w owns lanes 32w..32w+31.
+__device__ __forceinline__ void drain_base_accumulator(uint32_t tmem_acc, int warp, int lane, float* __restrict__ Pb,
+                                                       int out, int row0, int tok_begin, int tcount) {
+  const int row = row0 + 32 * warp + lane;
+#pragma unroll
+  for (int c = 0; c < BASE_N / 16; c++) {
+    if (c * 16 >= tcount) break;
+    uint32_t v[16];
+    tmem_ld16(tmem_acc + (static_cast<uint32_t>(32 * warp) << 16) + c * 16, v);
+    tmem_ld_wait();
+    if (row < out) {
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        const int tk = c * 16 + j;
+        if (tk < tcount) Pb[static_cast<int64_t>(tok_begin + tk) * out + row] = __uint_as_float(v[j]);
+      }
     }
   }
 }
@@ -168,17 +286,19 @@ __device__ __forceinline__ void write_partial(const float (&acc)[NT][4], float* 
 // ------------------------------------------------------------------------------------------
 // The persistent kernel
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NTHREADS, 1) k_sbmm(dz_sbmm_args a) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* stages = smem_raw;
-  Smem* sm = reinterpret_cast<Smem*>(smem_raw + STAGE_BYTES * NSTAGE);
+__global__ void __launch_bounds__(NTHREADS, 2)
+    k_sbmm(const __grid_constant__ dz_sbmm_args a, const __grid_constant__ CUtensorMap xmap) {
+  extern __shared__ uint8_t smem_dyn[];
+  // 1024-B alignment for the SWIZZLE_128B tiles
+  uint8_t* stages = smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);
+  Smem* sm = reinterpret_cast<Smem*>(stages + STAGE_BYTES * NSTAGE);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  Geo geo;
-  geo.nkb = ceil_div(a.in, kBlkCols);
-  geo.n16 = ceil_div(a.out, kBlkRows);
-  geo.nrt = ceil_div(a.out, RT);
-  const int n_items = geo.nrt * a.n_jobs;
+  const int n16 = ceil_div(a.out, kBlkRows);
+  const int nrt = ceil_div(a.out, RT);
+  const int nkb = ceil_div(a.in, kBlkCols);
+  const int nch_base = ceil_div(a.in, KC_DN);
+  const int n_items = nrt * a.n_jobs;
 
   int* ws_i = reinterpret_cast<int*>(a.workspace);
   int* sched = ws_i;              // [0] item counter, [1] finished CTAs
@@ -189,162 +309,322 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_sbmm(dz_sbmm_args a) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; s++) {
       mbar_init(&sm->full[s], 1);
-      mbar_init(&sm->empty[s], NW);
+      mbar_init(&sm->empty[s], NW + 1);  // consumer warps + the MMA warp (commit or arrive)
+    }
+    for (int b = 0; b < 2; b++) {
+      mbar_init(&sm->tmem_full[b], 1);
+      mbar_init(&sm->tmem_empty[b], NW);
     }
     fence_mbar_init();
   }
+  if (warp == WARP_MMA) {
+    tmem_alloc(&sm->tmem_base, TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
   __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = sm->tmem_base;
 
-  if (warp == NW) {
-    // ===================== producer =====================
+  if (warp == WARP_PROD) {
+    // ===================== TMA producer =====================
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_keep = policy_evict_last();
+    if (lane == 0) prefetch_tmap(&xmap);
     int stage = 0;
     uint32_t phase = 0;
-    while (true) {
-      int item = 0;
-      if (lane == 0) item = atomicAdd(&sched[0], 1);
-      item = __shfl_sync(0xffffffffu, item, 0);
-      if (item >= n_items) break;
-      const int rt = item / a.n_jobs;
-      const dz_job job = a.jobs[item - rt * a.n_jobs];
-      const bool dense = job_dense(job.kind);
-      const uint8_t* src = static_cast<const uint8_t*>(job.kind == 0 ? a.base : a.table[job.slot].blocks);
-      const int bb = blk_bytes(job.kind);
-      const int nch = job_nchunks(job.kind, geo);
-      const int nbmax = dense ? 1 : NB_SP;
-      const int xs = dense ? XS_DN : XS_SP;
-      const int aoff = dense ? A_DN : A_SP;
-      int nvalid = geo.n16 - rt * NW;
-      nvalid = nvalid > NW ? NW : nvalid;
+    int id_raw = 0;
+    if (lane == 0) id_raw = atomicAdd(&sched[0], 1);
+    int item = __shfl_sync(0xffffffffu, id_raw, 0);
+#ifdef DZ_TRACE
+    if (lane == 0 && item == 0) dz_trace_cta = blockIdx.x;
+#endif
+    while (item < n_items) {
+      const dz_job job = a.jobs[item / nrt];
+      const int rt = item - (item / nrt) * nrt;
+      int tok = 0, tok2 = 0;
+      if (job.kind != 0) {
+        if (lane < job.tok_count) tok = a.order[job.tok_begin + lane];
+        if (lane + 32 < job.tok_count) tok2 = a.order[job.tok_begin + lane + 32];
+      }
+      const bool is_base = job.kind == 0;
+      const bool dense = kind_dense(job.kind);
+      const dz_native_delta* ent = is_base ? a.base : a.table + job.slot;
+      const void* amap = ent->tmap;  // address only: the descriptor stays in global memory
+      const int bb = dense ? kDenseBlockBytes : sparse_block_bytes(kind_fbits(job.kind));
+      const int nch = is_base ? nch_base : dense ? 2 * nkb : ceil_div(nkb, NB_SP);
+      const uint32_t abytes = dense ? static_cast<uint32_t>(A_DN) : static_cast<uint32_t>(RG * NB_SP * bb);
+      int id_nxt_raw = 0;
       for (int ch = 0; ch < nch; ch++) {
-        const int kb0 = ch * nbmax;
-        const int nb = (geo.nkb - kb0) < nbmax ? (geo.nkb - kb0) : nbmax;
+        // fetch the next item id while the last chunk goes out (one item in flight per CTA, so
+        // the dynamic schedule stays balanced)
+        if (ch == nch - 1 && lane == 0) id_nxt_raw = atomicAdd(&sched[0], 1);
+        if (lane == 0) TRACE(1, item, ch);
         mbar_wait(&sm->empty[stage], phase ^ 1);
+        if (lane == 0) TRACE(2, item, ch);
         uint8_t* sbuf = stages + static_cast<size_t>(stage) * STAGE_BYTES;
+        int nb, col0, xbytes, ax, ay;
+        if (dense) {
+          nb = 1;
+          col0 = ch * KC_DN;
+          xbytes = KC_DN * 2;
+          ax = is_base ? col0 : ch * (DN_HALF / 8);
+          ay = rt * (is_base ? RT : RG);
+        } else {
+          const int kb0 = ch * NB_SP;
+          nb = (nkb - kb0) < NB_SP ? (nkb - kb0) : NB_SP;
+          col0 = kb0 * kBlkCols;
+          xbytes = nb * kBlkCols * 2;
+          ax = ch * (NB_SP * bb / 8);
+          ay = rt * RG;
+        }
         if (lane == 0) {
-          sm->hdr[stage] = StageHdr{item, ch, nb, 0};
-          const uint32_t bytes = static_cast<uint32_t>(nvalid * nb * bb + job.tok_count * nb * kBlkCols * 2);
-          mbar_arrive_expect_tx(&sm->full[stage], bytes);
+          StageHdr h;
+          h.item = item; h.rt = rt; h.kind = job.kind;
+          h.tok_begin = job.tok_begin; h.tok_count = job.tok_count; h.nb = nb;
+          h.flags = (ch == 0 ? 1 : 0) | (ch == nch - 1 ? 2 : 0);
+          h.pad = 0;
+          sm->hdr[stage] = h;
+          const uint32_t xb = is_base ? static_cast<uint32_t>(KC_DN * BASE_N * 2)
+                                      : static_cast<uint32_t>(job.tok_count * xbytes);
+          mbar_arrive_expect_tx(&sm->full[stage], abytes + xb);
+          tma_load_2d(sbuf, amap, ax, ay, &sm->full[stage], pol_stream);
+          if (is_base) tma_load_2d(sbuf + A_DN, &xmap, col0, job.tok_begin, &sm->full[stage], pol_keep);
         }
-        __syncwarp();
-        if (lane < nvalid) {
-          const int rg = rt * NW + lane;
-          const uint8_t* s = src + (static_cast<size_t>(rg) * geo.nkb + kb0) * bb;
-          tma_load_1d(sbuf + lane * nbmax * bb, s, static_cast<uint32_t>(nb * bb), &sm->full[stage], pol_stream);
-        }
-        for (int tk = lane; tk < job.tok_count; tk += 32) {
-          const int tok = job.kind == 0 ? job.tok_begin + tk : a.order[job.tok_begin + tk];
-          const uint16_t* xs_src = a.X + static_cast<int64_t>(tok) * a.ldx + kb0 * kBlkCols;
-          tma_load_1d(sbuf + aoff + tk * xs, xs_src, static_cast<uint32_t>(nb * kBlkCols * 2), &sm->full[stage],
-                      pol_keep);
+        if (!is_base) {
+          const int aoff = dense ? A_DN : A_SP;
+          const int xs = dense ? XS_DN : XS_SP;
+          if (lane < job.tok_count)
+            tma_load_1d(sbuf + aoff + lane * xs, a.X + static_cast<int64_t>(tok) * a.ldx + col0,
+                        static_cast<uint32_t>(xbytes), &sm->full[stage], pol_keep);
+          if (lane + 32 < job.tok_count)
+            tma_load_1d(sbuf + aoff + (lane + 32) * xs, a.X + static_cast<int64_t>(tok2) * a.ldx + col0,
+                        static_cast<uint32_t>(xbytes), &sm->full[stage], pol_keep);
         }
         if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
       }
+      item = __shfl_sync(0xffffffffu, id_nxt_raw, 0);
     }
     mbar_wait(&sm->empty[stage], phase ^ 1);
     if (lane == 0) {
-      sm->hdr[stage] = StageHdr{-1, 0, 0, 0};
+      sm->hdr[stage].item = -1;
       mbar_arrive(&sm->full[stage]);
-      __threadfence();
       const int done = atomicAdd(&sched[1], 1);
       if (done == static_cast<int>(gridDim.x) - 1) {  // last CTA out resets the scheduler
         sched[0] = 0;
         sched[1] = 0;
       }
     }
-    return;
-  }
-
-  // ===================== consumers =====================
-  const int g = lane >> 2;
-  float acc_d[NT_DN][4];
-  float acc_s[NT_SP][4];
-  int stage = 0;
-  uint32_t phase = 0;
-  __shared__ int tok_ids_sh[JOB_DN_TOK];
-  while (true) {
-    mbar_wait(&sm->full[stage], phase);
-    const StageHdr h = sm->hdr[stage];
-    if (h.item < 0) break;
-    const int rt = h.item / a.n_jobs;
-    const dz_job job = a.jobs[h.item - rt * a.n_jobs];
-    const bool dense = job_dense(job.kind);
-    const int rg = rt * NW + warp;
-    const bool valid = rg < geo.n16;
-    const uint32_t sbuf = smem_u32(stages + static_cast<size_t>(stage) * STAGE_BYTES);
-    if (h.chunk == 0) {
+  } else if (warp == WARP_MMA) {
+    // ===================== tcgen05 issuer =====================
+    int stage = 0;
+    uint32_t phase = 0;
+    int nbase = 0;  // base items seen (selects the TMEM accumulator buffer and its phase)
+    while (true) {
+      mbar_wait(&sm->full[stage], phase);
+      const StageHdr h = sm->hdr[stage];
+      if (h.item < 0) break;
+      if (h.kind == 0) {
+        const int buf = nbase & 1;
+        const uint32_t acc_phase = (nbase >> 1) & 1;
+        if (h.flags & 1) mbar_wait(&sm->tmem_empty[buf], acc_phase ^ 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sbuf = smem_u32(stages + static_cast<size_t>(stage) * STAGE_BYTES);
+          const uint64_t adesc = umma_desc_sw128(sbuf);
+          const uint64_t bdesc = umma_desc_sw128(sbuf + A_DN);
+          const uint32_t tmem_d = tmem_base + buf * BASE_N;
 #pragma unroll
-      for (int n = 0; n < NT_DN; n++) acc_d[n][0] = acc_d[n][1] = acc_d[n][2] = acc_d[n][3] = 0.f;
-#pragma unroll
-      for (int n = 0; n < NT_SP; n++) acc_s[n][0] = acc_s[n][1] = acc_s[n][2] = acc_s[n][3] = 0.f;
-    }
-    const int nt = ceil_div(job.tok_count, 8);
-    if (valid) {
-      if (dense) {
-        const uint32_t xl = sbuf + A_DN + (lane & 7) * XS_DN + (lane >> 3) * 16;
-        dense_chunk(acc_d, sbuf + warp * kDenseBlockBytes, xl, nt, lane);
-      } else {
-        const uint32_t xl = sbuf + A_SP + (lane & 7) * XS_SP + (lane >> 3) * 16;
-        const int qmax = a.table[job.slot].qmax;
-        const uint32_t off = 0x4300u + static_cast<uint32_t>(qmax);  // bf16(128 + qmax), exact
-        const uint32_t off2 = off | (off << 16);
-        if (job.kind == DZ_KIND_SPARSE4)
-          sparse_chunk<4>(acc_s, sbuf + warp * NB_SP * sparse_block_bytes(4), xl, h.nb, nt, off2, lane);
-        else
-          sparse_chunk<2>(acc_s, sbuf + warp * NB_SP * sparse_block_bytes(2), xl, h.nb, nt, off2, lane);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm->empty[stage]);
-    if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
-
-    if (h.chunk == job_nchunks(job.kind, geo) - 1) {
-      // ---- item epilogue: partial -> workspace, then row-tile completion ----
-      const int ctid = threadIdx.x;  // 0 .. NW*32-1
-      named_bar_sync(1, NW * 32);    // tok_ids_sh reuse guard
-      for (int tk = ctid; tk < job.tok_count; tk += NW * 32)
-        tok_ids_sh[tk] = job.kind == 0 ? job.tok_begin + tk : a.order[job.tok_begin + tk];
-      named_bar_sync(1, NW * 32);
-      if (valid) {
-        if (dense)
-          write_partial<NT_DN>(acc_d, job.kind == 0 ? Pb : Pd, a.out, rg * kBlkRows, job.tok_count, tok_ids_sh, lane);
-        else
-          write_partial<NT_SP>(acc_s, Pd, a.out, rg * kBlkRows, job.tok_count, tok_ids_sh, lane);
-      }
-      __threadfence();
-      named_bar_sync(1, NW * 32);
-      if (ctid == 0) {
-        const int old = atomicAdd(&tile_cnt[rt], 1);
-        sm->last_flag = (old == a.n_jobs - 1);
-      }
-      named_bar_sync(1, NW * 32);
-      if (sm->last_flag) {
-        __threadfence();
-        const int r0 = rt * RT;
-        const int nr = (a.out - r0) < RT ? (a.out - r0) : RT;
-        const bool has_base = a.base != nullptr;
-        for (int idx = ctid; idx < a.T * nr; idx += NW * 32) {
-          const int tk = idx / nr, r = r0 + idx % nr;
-          const int64_t o = static_cast<int64_t>(tk) * a.out + r;
-          float y = __ldcg(Pd + o);
-          if (has_base) y = __ldcg(Pb + o) + y;
-          if (a.act == DZ_ACT_TANH) y = tanhf(y);
-          if (a.y_dtype == DZ_F32)
-            reinterpret_cast<float*>(a.Y)[static_cast<int64_t>(tk) * a.ldy + r] = y;
-          else
-            reinterpret_cast<__nv_bfloat16*>(a.Y)[static_cast<int64_t>(tk) * a.ldy + r] = __float2bfloat16_rn(y);
+          for (int k = 0; k < KC_DN / 16; k++)  // K=16 per MMA: +32 B inside the 128-B swizzle atom
+            umma_bf16(tmem_d, adesc + 2 * k, bdesc + 2 * k, IDESC_BASE, (h.flags & 1) && k == 0 ? 0u : 1u);
+          umma_commit(&sm->empty[stage]);
+          if (h.flags & 2) umma_commit(&sm->tmem_full[buf]);
         }
-        if (ctid == 0) tile_cnt[rt] = 0;  // self-reset for the next launch
+        __syncwarp();
+        if (h.flags & 2) nbase++;
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm->empty[stage]);
+      }
+      if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
+    }
+  } else {
+    // ===================== consumers =====================
+    float acc[MR][NT_DN][4];  // dense deltas use all NT_DN tiles, sparse deltas the first NT_SP
+    int stage = 0;
+    uint32_t phase = 0;
+    int nbase = 0;
+    const int ctid = threadIdx.x;  // 0 .. NW*32-1
+    while (true) {
+      mbar_wait(&sm->full[stage], phase);
+      const StageHdr h = sm->hdr[stage];
+      if (lane == 0 && warp == 0) TRACE(3, h.item, stage);
+      if (h.item < 0) break;
+      const bool is_base = h.kind == 0;
+      const int rg0 = h.rt * RG + warp * MR;
+      const int nrv = (n16 - rg0) < MR ? (n16 - rg0) : MR;  // row groups of this warp inside `out`
+      const uint32_t sbuf = smem_u32(stages + static_cast<size_t>(stage) * STAGE_BYTES);
+      const int nt = ceil_div(h.tok_count, 8);
+      if (!is_base) {
+        if (h.flags & 1) {
+#pragma unroll
+          for (int r = 0; r < MR; r++)
+#pragma unroll
+            for (int n = 0; n < NT_DN; n++) acc[r][n][0] = acc[r][n][1] = acc[r][n][2] = acc[r][n][3] = 0.f;
+        }
+        if (nrv > 0) {
+          if (h.kind == DZ_KIND_DENSE) {
+            dense_dispatch(nt, acc, sbuf + warp * MR * DN_HALF, sbuf + A_DN, nrv, lane);
+          } else {
+            const uint32_t xl = sbuf + A_SP + (lane & 7) * XS_SP + (lane >> 3) * 16;
+            const uint32_t off = 0x4300u + static_cast<uint32_t>(kind_qmax(h.kind));  // bf16(128 + qmax)
+            const uint32_t off2 = off | (off << 16);
+            if (h.kind != DZ_KIND_SPARSE2) {
+              const uint32_t sA = sbuf + warp * MR * NB_SP * sparse_block_bytes(4);
+              if (nt == 1) sparse_chunk<4, 1>(acc, sA, xl, h.nb, nrv, off2, lane);
+              else sparse_chunk<4, 2>(acc, sA, xl, h.nb, nrv, off2, lane);
+            } else {
+              const uint32_t sA = sbuf + warp * MR * NB_SP * sparse_block_bytes(2);
+              if (nt == 1) sparse_chunk<2, 1>(acc, sA, xl, h.nb, nrv, off2, lane);
+              else sparse_chunk<2, 2>(acc, sA, xl, h.nb, nrv, off2, lane);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm->empty[stage]);
+      if (lane == 0 && warp == 0) TRACE(4, h.item, stage);
+      if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
+
+      if (h.flags & 2) {
+        // ---- item epilogue: partial -> workspace, then row-tile completion ----
+        if (is_base) {
+          const int buf = nbase & 1;
+          mbar_wait(&sm->tmem_full[buf], (nbase >> 1) & 1);
+          tc_fence_after();
+          drain_base_accumulator(tmem_base + buf * BASE_N, warp, lane, Pb, a.out, h.rt * RT, h.tok_begin,
+                                 h.tok_count);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm->tmem_empty[buf]);
+          nbase++;
+        } else {
+          named_bar_sync(1, NW * 32);  // tok_ids reuse guard
+          for (int tk = ctid; tk < h.tok_count; tk += NW * 32) sm->tok_ids[tk] = a.order[h.tok_begin + tk];
+          named_bar_sync(1, NW * 32);
+          if (nrv > 0) write_partial(acc, nt, Pd, a.out, rg0, h.tok_count, sm->tok_ids, lane);
+        }
+        named_bar_sync(1, NW * 32);
+        if (ctid == 0) {
+          // acq_rel at gpu scope: releases this CTA's partial stores (ordered before it by bar.sync;
+          // fence cumulativity) and acquires every earlier item's partials for the combine.
+          const int old = atom_add_acq_rel_gpu(&tile_cnt[h.rt], 1);
+          sm->last_flag = (old == a.n_jobs - 1);
+        }
+        named_bar_sync(1, NW * 32);
+        if (sm->last_flag) {
+          const int r0 = h.rt * RT;
+          const int nr = (a.out - r0) < RT ? (a.out - r0) : RT;
+          const bool has_base = a.base != nullptr;
+          for (int idx = ctid; idx < a.T * nr; idx += NW * 32) {
+            const int tk = idx / nr, r = r0 + idx % nr;
+            const int64_t o = static_cast<int64_t>(tk) * a.out + r;
+            float y = __ldcg(Pd + o);
+            if (has_base) y = __ldcg(Pb + o) + y;
+            if (a.act == DZ_ACT_TANH) y = tanhf(y);
+            if (a.y_dtype == DZ_F32)
+              reinterpret_cast<float*>(a.Y)[static_cast<int64_t>(tk) * a.ldy + r] = y;
+            else
+              reinterpret_cast<__nv_bfloat16*>(a.Y)[static_cast<int64_t>(tk) * a.ldy + r] = __float2bfloat16_rn(y);
+          }
+          if (ctid == 0) tile_cnt[h.rt] = 0;  // self-reset for the next launch
+        }
+        if (lane == 0 && warp == 0) TRACE(5, h.item, 0);
       }
     }
   }
-  (void)g;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == WARP_MMA) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Host: TMA descriptors (driver entry point fetched through the runtime; no -lcuda)
+// ------------------------------------------------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static std::once_flag once;
+  static EncodeTiledFn fn = nullptr;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+static int encode_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t dim0, uint64_t dim1,
+                     uint64_t stride1_bytes, uint32_t box0, uint32_t box1, CUtensorMapSwizzle swz) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return DZ_E_CUDA;
+  const cuuint64_t dims[2] = {dim0, dim1};
+  const cuuint64_t strides[1] = {stride1_bytes};
+  const cuuint32_t box[2] = {box0, box1};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? DZ_OK : DZ_E_CUDA;
 }
 
 }  // namespace dz
 
 using namespace dz;
+
+static_assert(sizeof(dz_native_delta) == 192, "dz_native_delta must be 192 bytes");
+static_assert(offsetof(dz_native_delta, tmap) == 64, "tensor map must be 64-byte aligned in the entry");
+static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
+
+extern "C" int dz_native_delta_init(dz_native_delta* e, const void* blocks, int32_t kind, int32_t rows, int32_t cols) {
+  if (!e || !blocks) return DZ_E_VALUE;
+  if (rows < 1 || cols < 1) return DZ_E_SHAPE;
+  if (kind != DZ_KIND_SPARSE4 && kind != DZ_KIND_SPARSE2 && kind != DZ_KIND_SPARSE3 && kind != DZ_KIND_DENSE)
+    return DZ_E_VALUE;
+  if (reinterpret_cast<uintptr_t>(blocks) & 15) return DZ_E_VALUE;
+  std::memset(e, 0, sizeof(*e));
+  e->blocks = blocks;
+  e->kind = kind;
+  e->qmax = kind == DZ_KIND_DENSE ? 0 : kind_qmax(kind);
+  e->rows = rows;
+  e->cols = cols;
+  const int nkb = ceil_div(cols, kBlkCols), n16 = ceil_div(rows, kBlkRows);
+  const int bb = kind == DZ_KIND_DENSE ? kDenseBlockBytes : sparse_block_bytes(kind_fbits(kind));
+  const uint32_t box0 = kind == DZ_KIND_DENSE ? DN_HALF / 8 : NB_SP * bb / 8;
+  return encode_2d(reinterpret_cast<CUtensorMap*>(e->tmap), CU_TENSOR_MAP_DATA_TYPE_UINT64, blocks,
+                   static_cast<uint64_t>(nkb) * bb / 8, static_cast<uint64_t>(n16), static_cast<uint64_t>(nkb) * bb,
+                   box0, RG, CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+extern "C" int dz_base_init(dz_native_delta* e, const uint16_t* W, int64_t ldw, int32_t rows, int32_t cols) {
+  if (!e || !W) return DZ_E_VALUE;
+  if (rows < 1 || cols < 1 || ldw < cols) return DZ_E_SHAPE;
+  if ((reinterpret_cast<uintptr_t>(W) & 15) || (ldw % 8)) return DZ_E_SHAPE;  // TMA: 16-B rows
+  std::memset(e, 0, sizeof(*e));
+  e->blocks = W;
+  e->kind = 0;
+  e->rows = rows;
+  e->cols = cols;
+  return encode_2d(reinterpret_cast<CUtensorMap*>(e->tmap), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, W,
+                   static_cast<uint64_t>(cols), static_cast<uint64_t>(rows), static_cast<uint64_t>(ldw) * 2, KC_DN, RT,
+                   CU_TENSOR_MAP_SWIZZLE_128B);
+}
 
 extern "C" size_t dz_sbmm_workspace_bytes(int32_t T, int32_t out) {
   if (T < 0 || out < 1) return 0;
@@ -363,19 +643,43 @@ extern "C" int dz_sbmm(const dz_sbmm_args* a, void* stream) {
   if (a->y_dtype != DZ_F32 && a->y_dtype != DZ_BF16) return DZ_E_VALUE;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
+  static int ctas_per_sm = 1;
   std::call_once(once, [] {
     attr_err = cudaFuncSetAttribute(k_sbmm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, k_sbmm, NTHREADS, SMEM_BYTES);
+    if (ctas_per_sm < 1) ctas_per_sm = 1;
   });
   if (attr_err != cudaSuccess) return DZ_E_CUDA;
+  CUtensorMap xmap;  // X [T][in] bf16, 64-column x 64-token SWIZZLE_128B tiles (base UMMA B operand)
+  int st = encode_2d(&xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a->X, static_cast<uint64_t>(a->in),
+                     static_cast<uint64_t>(a->T), static_cast<uint64_t>(a->ldx) * 2, KC_DN, BASE_N,
+                     CU_TENSOR_MAP_SWIZZLE_128B);
+  if (st) return st;
   int grid = a->grid;
   if (grid <= 0) {
     int dev = 0, sms = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return DZ_E_CUDA;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return DZ_E_CUDA;
-    grid = sms;
+    grid = sms * ctas_per_sm;
   }
   const int n_items = ceil_div(a->out, RT) * a->n_jobs;
   if (grid > n_items) grid = n_items;
-  k_sbmm<<<grid, NTHREADS, SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(*a);
+  k_sbmm<<<grid, NTHREADS, SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(*a, xmap);
   return cudaGetLastError() == cudaSuccess ? DZ_OK : DZ_E_CUDA;
 }
+
+#ifdef DZ_TRACE
+extern "C" int dz_trace_read(unsigned long long* host, int max_events) {
+  int n = 0;
+  cudaMemcpyFromSymbol(&n, dz_trace_n, sizeof(int));
+  if (n > max_events) n = max_events;
+  if (n > 8192) n = 8192;
+  cudaMemcpyFromSymbol(host, dz_trace_buf, sizeof(unsigned long long) * 4 * n);
+  int zero = 0;
+  cudaMemcpyToSymbol(dz_trace_n, &zero, sizeof(int));
+  int neg = -1;
+  cudaMemcpyToSymbol(dz_trace_cta, &neg, sizeof(int));
+  return n;
+}
+#endif

@@ -58,7 +58,7 @@ class NativeDelta:
             blocks = torch.empty(nbytes, dtype=torch.uint8, device=dev)
             L.check(lib.dz_repack_sparse(ref.struct, blocks.data_ptr(), err.ptr, stream_ptr()), "upload delta")
             err.raise_if_set("corrupt index stream: kept positions not strictly increasing")
-            kind = L.DZ_KIND_SPARSE2 if ref.bits == 2 else L.DZ_KIND_SPARSE4
+            kind = {2: L.DZ_KIND_SPARSE2, 3: L.DZ_KIND_SPARSE3, 4: L.DZ_KIND_SPARSE4}[ref.bits]
             return cls(kind, (1 << (ref.bits - 1)) - 1, ref.rows, ref.cols, blocks, ref.bits)
         dense = dequantize_layer_device(ld, torch.bfloat16, ref=ref)  # raises FormatError / EncodingError
         return cls.from_dense_bf16(dense, bits=ref.bits)
@@ -90,16 +90,39 @@ def pack_dense(W: torch.Tensor) -> torch.Tensor:
     return blocks
 
 
+def table_bytes(deltas: list[NativeDelta]) -> np.ndarray:
+    """Host-encoded dz_native_delta entries (192 B each, with their TMA descriptors)."""
+    n = max(1, len(deltas))
+    arr = (L.DzNativeDelta * n)()
+    for i, d in enumerate(deltas):
+        L.check(L.lib().dz_native_delta_init(C.byref(arr[i]), d.blocks.data_ptr(), d.kind, d.rows, d.cols),
+                "table entry")
+    return np.frombuffer(C.string_at(C.addressof(arr), C.sizeof(arr)), dtype=np.uint8).copy()
+
+
 class NativeBase:
-    """Shared base weight W_base [out, in] (bf16) in dense native blocks."""
+    """Shared base weight W_base [out, in] (bf16), kept in its natural row-major layout: the fused
+    kernel streams it with 128B-swizzled TMA tiles straight into tcgen05 MMAs. Rows are padded to
+    a 16-byte multiple only when `in` is not a multiple of 8 (TMA row-stride rule)."""
 
     def __init__(self, W: torch.Tensor):
+        if W.dim() != 2 or W.dtype != torch.bfloat16 or not W.is_cuda:
+            raise ShapeError("base weight must be a 2-D bf16 CUDA tensor")
         self.out, self.inp = int(W.shape[0]), int(W.shape[1])
-        self.blocks = pack_dense(W)
+        if W.stride(1) != 1 or W.stride(0) % 8 or W.data_ptr() % 16:
+            ld = _ceil(self.inp, 8) * 8
+            Wp = torch.zeros(self.out, ld, dtype=torch.bfloat16, device=W.device)
+            Wp[:, : self.inp] = W
+            W = Wp
+        self.W = W
+        e = L.DzNativeDelta()
+        L.check(L.lib().dz_base_init(C.byref(e), W.data_ptr(), W.stride(0), self.out, self.inp), "base entry")
+        raw = np.frombuffer(C.string_at(C.addressof(e), C.sizeof(e)), dtype=np.uint8).copy()
+        self.entry = torch.from_numpy(raw).to(W.device)
 
     @property
     def nbytes(self) -> int:
-        return self.out * self.inp * 2  # algorithmic bytes (the pad is not counted)
+        return self.out * self.inp * 2
 
 
 class DeltaTable:
@@ -111,13 +134,8 @@ class DeltaTable:
                 raise ShapeError(f"delta shape ({d.rows}, {d.cols}) != base ({out}, {inp})")
         self.deltas = list(deltas)
         self.out, self.inp = out, inp
-        n = max(1, len(deltas))
-        arr = (L.DzNativeDelta * n)()
-        for i, d in enumerate(deltas):
-            arr[i] = L.DzNativeDelta(d.blocks.data_ptr(), d.kind, d.qmax, d.rows, d.cols)
-        raw = np.frombuffer(C.string_at(C.addressof(arr), C.sizeof(arr)), dtype=np.uint8).copy()
         dev = deltas[0].blocks.device if deltas else require_cuda()
-        self.dev = torch.from_numpy(raw).to(dev)
+        self.dev = torch.from_numpy(table_bytes(deltas)).to(dev)
         self.kinds = np.array([d.kind for d in deltas] or [L.DZ_KIND_SPARSE4], dtype=np.int32)
 
     def __len__(self) -> int:
@@ -127,7 +145,8 @@ class DeltaTable:
 class Plan:
     """Batch plan: stable sort of tokens by slot + job list (dz_plan), uploaded to the device."""
 
-    def __init__(self, slots, kinds: np.ndarray, n_slots: int, with_base: bool = True, device=None):
+    def __init__(self, slots, kinds: np.ndarray, n_slots: int, with_base: bool = True, device=None,
+                 upload: bool = True):
         s = np.ascontiguousarray(np.asarray(slots, dtype=np.int32).ravel())
         self.T = int(s.size)
         lib = L.lib()
@@ -145,11 +164,14 @@ class Plan:
         self.order_host = order[: self.T].copy()
         self.jobs_host = np.frombuffer(C.string_at(C.addressof(jobs), C.sizeof(L.DzJob) * max(self.n_jobs, 1)),
                                        dtype=np.int32).reshape(-1, 4)[: self.n_jobs].copy()
-        dev = device or require_cuda()
-        self.order = torch.from_numpy(order).to(dev)
-        self.jobs = torch.from_numpy(np.frombuffer(C.string_at(C.addressof(jobs), C.sizeof(L.DzJob) * max(maxj, 1)),
-                                                   dtype=np.uint8).copy()).to(dev)
+        self.jobs_bytes = np.frombuffer(C.string_at(C.addressof(jobs), C.sizeof(L.DzJob) * max(maxj, 1)),
+                                        dtype=np.uint8).copy()
         self.with_base = with_base
+        self.order = self.jobs = None
+        if upload:
+            dev = device or require_cuda()
+            self.order = torch.from_numpy(order).to(dev)
+            self.jobs = torch.from_numpy(self.jobs_bytes).to(dev)
 
 
 class Workspace:
@@ -207,7 +229,7 @@ def sbmm_forward(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: De
     a.y_dtype = L.DZ_F32 if Y.dtype == torch.float32 else L.DZ_BF16
     a.act = act
     a.T, a.out, a.in_ = T, out, inp
-    a.base = base.blocks.data_ptr() if base is not None else None
+    a.base = base.entry.data_ptr() if base is not None else None
     a.table, a.n_slots = table.dev.data_ptr(), len(table)
     a.order = plan.order.data_ptr()
     a.jobs, a.n_jobs = plan.jobs.data_ptr(), plan.n_jobs
