@@ -75,7 +75,7 @@ typedef struct dz_native_delta {
 typedef struct dz_job {
   int32_t slot;             /* delta-table index; -1 = base GEMM over all tokens     */
   int32_t tok_begin;        /* first position in `order` (delta) or token (base)     */
-  int32_t tok_count;        /* <= 64 (base / dense) or <= 16 (sparse)                */
+  int32_t tok_count;        /* <= 64 (base), <= 32 (dense delta), <= 8 (sparse)      */
   int32_t kind;             /* 0 = base, else DZ_KIND_* of the slot                  */
 } dz_job;
 
@@ -96,6 +96,7 @@ typedef struct dz_sbmm_args {
   void* workspace;          /* dz_sbmm_workspace_bytes(T, out) bytes; counters must be
                                zero the first time (they self-reset after every call) */
   int32_t grid;             /* persistent CTAs; 0 = one per SM                       */
+  int32_t debug;            /* 0; bit 0 = skip consumer math (pipeline bandwidth probe) */
 } dz_sbmm_args;
 
 const char* dz_version(void);

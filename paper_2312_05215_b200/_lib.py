@@ -53,7 +53,7 @@ class DzSbmmArgs(C.Structure):
         ("order", C.c_void_p),
         ("jobs", C.c_void_p), ("n_jobs", C.c_int32),
         ("workspace", C.c_void_p),
-        ("grid", C.c_int32),
+        ("grid", C.c_int32), ("debug", C.c_int32),
     ]
 
 

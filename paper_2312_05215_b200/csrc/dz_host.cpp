@@ -24,7 +24,7 @@ extern "C" const char* dz_strerror(int status) {
 extern "C" int32_t dz_plan_max_jobs(int32_t T) { return T < 0 ? 0 : 2 * T + 2; }
 
 // Stable sort of token rows by slot (inference.py:106-123: `sorted` is stable), then cut into
-// jobs: base token chunks of 64, sparse delta chunks of 16, dense delta chunks of 64.
+// jobs: base token chunks of 64, sparse delta chunks of 8, dense delta chunks of 32.
 extern "C" int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t n_slots,
                        int32_t with_base, int32_t* order_out, dz_job* jobs_out, int32_t max_jobs,
                        int32_t* n_jobs_out) {
@@ -52,7 +52,7 @@ extern "C" int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, in
     const int32_t kind = kinds[s];
     if (kind != DZ_KIND_SPARSE4 && kind != DZ_KIND_SPARSE2 && kind != DZ_KIND_SPARSE3 && kind != DZ_KIND_DENSE)
       return DZ_E_VALUE;
-    const int32_t chunk = kind == DZ_KIND_DENSE ? 64 : 16;
+    const int32_t chunk = kind == DZ_KIND_DENSE ? 32 : 8;
     for (int32_t off = 0; off < c; off += chunk)
       if (!push(s, start[s] + off, (c - off) < chunk ? (c - off) : chunk, kind)) return DZ_E_VALUE;
   }

@@ -35,13 +35,16 @@
 #include "dz_common.cuh"
 
 #ifdef DZ_TRACE
-__device__ unsigned long long dz_trace_buf[8192][4];
-__device__ int dz_trace_n;
-__device__ volatile int dz_trace_cta = -1;  // the CTA that took item 0
-#define TRACE(ev, a0, a1) do { if (static_cast<int>(blockIdx.x) == dz_trace_cta) { \
-  int _i = atomicAdd(&dz_trace_n, 1); \
-  if (_i < 8192) { dz_trace_buf[_i][0] = dz::globaltimer(); dz_trace_buf[_i][1] = (ev); \
-  dz_trace_buf[_i][2] = (a0); dz_trace_buf[_i][3] = (a1); } } } while (0)
+// Per-warp private event slots of the traced CTA (the one that took item 0): plain stores, no
+// atomics, so tracing does not perturb the pipeline. Slot [warp][i] = {globaltimer, ev|a0|a1}.
+__device__ unsigned long long dz_trace_buf[8][1024][2];
+__device__ int dz_trace_cnt[8];
+__device__ volatile int dz_trace_cta = -1;
+#define TRACE(ev, a0, a1) do { if (blockIdx.x == 0 && trace_i < 1024) { \
+  dz_trace_buf[threadIdx.x >> 5][trace_i][0] = clock64(); \
+  dz_trace_buf[threadIdx.x >> 5][trace_i][1] = (static_cast<unsigned long long>(ev) << 56) | \
+      (static_cast<unsigned long long>(static_cast<uint32_t>(a0)) << 16) | static_cast<uint16_t>(a1); \
+  trace_i++; dz_trace_cnt[threadIdx.x >> 5] = trace_i; } } while (0)
 #else
 #define TRACE(ev, a0, a1) do {} while (0)
 #endif
@@ -55,21 +58,21 @@ constexpr int WARP_MMA = NW + 1;          // tcgen05 issuer / TMEM owner warp
 constexpr int NTHREADS = (NW + 2) * 32;
 constexpr int RG = NW * MR;               // row groups per item
 constexpr int RT = RG * kBlkRows;         // rows per item (128) == UMMA M
-constexpr int NB_SP = 2;                  // sparse chunk = 2 blocks = 256 columns
-constexpr int NT_SP = 2;                  // n-tiles per sparse job (16 tokens)
-constexpr int NT_DN = 8;                  // n-tiles per dense job (64 tokens)
+constexpr int NB_SP = 4;                  // sparse chunk = 4 blocks = 512 columns (one 3-D TMA box)
+constexpr int NT_SP = 1;                  // n-tiles per sparse job (8 tokens, dz_plan)
+constexpr int NT_DN = 4;                  // n-tiles per dense-delta job (32 tokens, dz_plan)
 constexpr int KC_DN = 64;                 // dense / base chunk = 64 columns
 constexpr int BASE_N = 64;                // tokens per base job == UMMA N
 constexpr int XS_SP = NB_SP * kBlkCols * 2 + 16;  // smem bytes per staged token row; +16 B so the
 constexpr int XS_DN = KC_DN * 2 + 16;             //   8 rows of an ldmatrix hit distinct banks
-constexpr int A_SP = RG * NB_SP * sparse_block_bytes(4);  // 13312
-constexpr int X_SP = NT_SP * 8 * XS_SP;                   // 8448
+constexpr int A_SP = RG * NB_SP * sparse_block_bytes(4);  // 26624
+constexpr int X_SP = NT_SP * 8 * XS_SP;                   // 8320
 constexpr int DN_HALF = kDenseBlockBytes / 2;             // 2048
 constexpr int A_DN = RG * DN_HALF;                        // 16384 == 128 rows x 128 B (base W tile)
-constexpr int X_DN = NT_DN * 8 * XS_DN;                   // 9216 (>= 64 x 128 B swizzled X tile)
+constexpr int X_DN = 64 * XS_DN;                          // 9216 (>= 64 x 128 B swizzled X tile)
 constexpr int STAGE_BYTES = ((A_SP + X_SP > A_DN + X_DN ? A_SP + X_SP : A_DN + X_DN) + 1023) / 1024 * 1024;
-constexpr int NSTAGE = 4;
-constexpr int JOB_DN_TOK = NT_DN * 8;
+constexpr int NSTAGE = 3;
+constexpr int JOB_DN_TOK = BASE_N;        // largest token count of a job
 constexpr int kMaxTiles = 4096;           // row tiles per call (out <= 524288)
 constexpr int TMEM_COLS = 2 * BASE_N;     // two fp32 accumulators (double buffer)
 constexpr uint32_t IDESC_BASE = umma_idesc_bf16(RT, BASE_N);
@@ -92,8 +95,8 @@ struct Smem {
   uint64_t tmem_empty[2];
   StageHdr hdr[NSTAGE];
   uint32_t tmem_base;
-  int last_flag;
-  int tok_ids[JOB_DN_TOK];
+  int combine_rt;                    // row tile whose Y the consumers write next (-1: none)
+  int tok_ids[NSTAGE][JOB_DN_TOK];  // token ids of the item, staged with its last chunk
 };
 constexpr int SMEM_BYTES = 1024 + STAGE_BYTES * NSTAGE + static_cast<int>(sizeof(Smem));
 
@@ -122,82 +125,98 @@ __device__ __forceinline__ void conv_codes(uint32_t (&a)[4], const uint32_t (&cw
   }
 }
 
-// One sparse chunk (nb <= NB_SP blocks) for this warp's nrv <= MR row groups and NT token tiles.
-template <int FB, int NT>
-__device__ __forceinline__ void sparse_chunk(float (&acc)[MR][NT_DN][4], uint32_t sA, uint32_t xl, int nb,
-                                             int nrv, uint32_t off2, int lane) {
+// Two consecutive blocks (b0, b0+1 < nb) of a sparse chunk for this warp's nrv <= MR row groups
+// and NT token tiles: loads, decodes and issues 4 independent mma.sp chains.
+constexpr int PAIR = 2;
+// FULL: both blocks and all MR row groups valid -> no guards, straight-line code the compiler can
+// interleave (the common case); otherwise guarded (tail chunk / tail row tile).
+template <int FB, int NT, bool FULL>
+__device__ __forceinline__ void sparse_pair(float (&acc)[MR][NT_DN][4], uint32_t sA, uint32_t xl, int b0, int nb,
+                                            int nrv, uint32_t off2, int lane) {
   constexpr int CODE = sparse_code_bytes(FB);
   constexpr int BLK = sparse_block_bytes(FB);
   const int g = lane >> 2;
-  uint32_t cw[NB_SP][MR][4];
-  uint2 meta[NB_SP][MR];
-  float2 sc[NB_SP][MR];
+  uint32_t cw[PAIR][MR][4];
+  uint2 meta[PAIR][MR];
+  float2 sc[PAIR][MR];
 #pragma unroll
-  for (int b = 0; b < NB_SP; b++) {
+  for (int p = 0; p < PAIR; p++) {
 #pragma unroll
     for (int r = 0; r < MR; r++) {
-      // row group r of this warp: NB_SP contiguous blocks at (r*NB_SP + b)*BLK
-      const uint32_t blk = sA + (r * NB_SP + b) * BLK;
-      if (b < nb && r < nrv) {
+      // the TMA box lands row group by row group: rg r of this warp holds NB_SP contiguous blocks
+      const uint32_t blk = sA + (r * NB_SP + b0 + p) * BLK;
+      if (FULL || (b0 + p < nb && r < nrv)) {
         if (FB == 4) {
           const uint4 c = lds128(blk + lane * 16);
-          cw[b][r][0] = c.x; cw[b][r][1] = c.y; cw[b][r][2] = c.z; cw[b][r][3] = c.w;
+          cw[p][r][0] = c.x; cw[p][r][1] = c.y; cw[p][r][2] = c.z; cw[p][r][3] = c.w;
         } else {
           const uint2 c = lds64(blk + lane * 8);
-          cw[b][r][0] = c.x; cw[b][r][1] = c.y; cw[b][r][2] = 0; cw[b][r][3] = 0;
+          cw[p][r][0] = c.x; cw[p][r][1] = c.y; cw[p][r][2] = 0; cw[p][r][3] = 0;
         }
-        meta[b][r] = lds64(blk + CODE + lane * 8);
+        meta[p][r] = lds64(blk + CODE + lane * 8);
         const uint2 sv = lds64(blk + CODE + kMetaBytes + g * 8);
-        sc[b][r] = make_float2(__uint_as_float(sv.x), __uint_as_float(sv.y));
+        sc[p][r] = make_float2(__uint_as_float(sv.x), __uint_as_float(sv.y));
       } else {
-        cw[b][r][0] = cw[b][r][1] = cw[b][r][2] = cw[b][r][3] = 0;
-        meta[b][r] = make_uint2(0x44444444u, 0x44444444u);
-        sc[b][r] = make_float2(0.f, 0.f);
+        cw[p][r][0] = cw[p][r][1] = cw[p][r][2] = cw[p][r][3] = 0;
+        meta[p][r] = make_uint2(0x44444444u, 0x44444444u);
+        sc[p][r] = make_float2(0.f, 0.f);
       }
     }
   }
-  float tmp[NB_SP][MR][NT][4];
+  float tmp[PAIR][MR][NT][4];
 #pragma unroll
-  for (int b = 0; b < NB_SP; b++)
+  for (int p = 0; p < PAIR; p++)
 #pragma unroll
     for (int r = 0; r < MR; r++)
 #pragma unroll
-      for (int n = 0; n < NT; n++) tmp[b][r][n][0] = tmp[b][r][n][1] = tmp[b][r][n][2] = tmp[b][r][n][3] = 0.f;
+      for (int n = 0; n < NT; n++) tmp[p][r][n][0] = tmp[p][r][n][1] = tmp[p][r][n][2] = tmp[p][r][n][3] = 0.f;
 #pragma unroll
   for (int i = 0; i < 4; i++) {
 #pragma unroll
-    for (int b = 0; b < NB_SP; b++) {
-      if (b >= nb) continue;  // partial last chunk
+    for (int p = 0; p < PAIR; p++) {
+      if (!FULL && b0 + p >= nb) continue;  // partial last chunk
       uint32_t bf[NT][4];
 #pragma unroll
-      for (int n = 0; n < NT; n++) ldmatrix_x4(bf[n], xl + n * 8 * XS_SP + (b * kBlkCols + 32 * i) * 2);
+      for (int n = 0; n < NT; n++) ldmatrix_x4(bf[n], xl + n * 8 * XS_SP + ((b0 + p) * kBlkCols + 32 * i) * 2);
 #pragma unroll
       for (int r = 0; r < MR; r++) {
-        if (r >= nrv) continue;  // padding row group (zero-filled by TMA, never stored)
+        if (!FULL && r >= nrv) continue;  // padding row group (zero-filled by TMA, never stored)
         uint32_t a[4];
-        conv_codes<FB>(a, cw[b][r], i, off2);
-        const uint32_t e = (i < 2) ? meta[b][r].x : meta[b][r].y;
+        conv_codes<FB>(a, cw[p][r], i, off2);
+        const uint32_t e = (i < 2) ? meta[p][r].x : meta[p][r].y;
 #pragma unroll
         for (int n = 0; n < NT; n++) {
           if (i & 1)
-            mma_sp_bf16_16832<1>(tmp[b][r][n], a, bf[n], e);
+            mma_sp_bf16_16832<1>(tmp[p][r][n], a, bf[n], e);
           else
-            mma_sp_bf16_16832<0>(tmp[b][r][n], a, bf[n], e);
+            mma_sp_bf16_16832<0>(tmp[p][r][n], a, bf[n], e);
         }
       }
     }
   }
 #pragma unroll
-  for (int b = 0; b < NB_SP; b++)
+  for (int p = 0; p < PAIR; p++)
 #pragma unroll
     for (int r = 0; r < MR; r++)
 #pragma unroll
       for (int n = 0; n < NT; n++) {
-        acc[r][n][0] = fmaf(sc[b][r].x, tmp[b][r][n][0], acc[r][n][0]);
-        acc[r][n][1] = fmaf(sc[b][r].x, tmp[b][r][n][1], acc[r][n][1]);
-        acc[r][n][2] = fmaf(sc[b][r].y, tmp[b][r][n][2], acc[r][n][2]);
-        acc[r][n][3] = fmaf(sc[b][r].y, tmp[b][r][n][3], acc[r][n][3]);
+        acc[r][n][0] = fmaf(sc[p][r].x, tmp[p][r][n][0], acc[r][n][0]);
+        acc[r][n][1] = fmaf(sc[p][r].x, tmp[p][r][n][1], acc[r][n][1]);
+        acc[r][n][2] = fmaf(sc[p][r].y, tmp[p][r][n][2], acc[r][n][2]);
+        acc[r][n][3] = fmaf(sc[p][r].y, tmp[p][r][n][3], acc[r][n][3]);
       }
+}
+
+template <int FB, int NT>
+__device__ __forceinline__ void sparse_chunk(float (&acc)[MR][NT_DN][4], uint32_t sA, uint32_t xl, int nb,
+                                             int nrv, uint32_t off2, int lane) {
+  if (nb == NB_SP && nrv == MR) {
+#pragma unroll 1
+    for (int b0 = 0; b0 < NB_SP; b0 += PAIR) sparse_pair<FB, NT, true>(acc, sA, xl, b0, nb, nrv, off2, lane);
+  } else {
+#pragma unroll 1
+    for (int b0 = 0; b0 < nb; b0 += PAIR) sparse_pair<FB, NT, false>(acc, sA, xl, b0, nb, nrv, off2, lane);
+  }
 }
 
 // One dense-delta half-block chunk (64 columns = 4 k16 MMAs); X rows are per-token (XS_DN).
@@ -236,10 +255,7 @@ __device__ __forceinline__ void dense_dispatch(int nt, float (&acc)[MR][NT_DN][4
     case 2: dense_chunk<2>(acc, sA, sX, nrv, lane); break;
     case 3: dense_chunk<3>(acc, sA, sX, nrv, lane); break;
     case 4: dense_chunk<4>(acc, sA, sX, nrv, lane); break;
-    case 5: dense_chunk<5>(acc, sA, sX, nrv, lane); break;
-    case 6: dense_chunk<6>(acc, sA, sX, nrv, lane); break;
-    case 7: dense_chunk<7>(acc, sA, sX, nrv, lane); break;
-    default: dense_chunk<8>(acc, sA, sX, nrv, lane); break;
+    default: dense_chunk<4>(acc, sA, sX, nrv, lane); break;
   }
 }
 
@@ -328,6 +344,8 @@ __global__ void __launch_bounds__(NTHREADS, 2)
 
   if (warp == WARP_PROD) {
     // ===================== TMA producer =====================
+    int trace_i = 0;
+    (void)trace_i;
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_keep = policy_evict_last();
     if (lane == 0) prefetch_tmap(&xmap);
@@ -336,17 +354,15 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     int id_raw = 0;
     if (lane == 0) id_raw = atomicAdd(&sched[0], 1);
     int item = __shfl_sync(0xffffffffu, id_raw, 0);
-#ifdef DZ_TRACE
-    if (lane == 0 && item == 0) dz_trace_cta = blockIdx.x;
-#endif
+    dz_job job = item < n_items ? a.jobs[item / nrt] : dz_job{0, 0, 0, 0};
+    int tok = 0, tok2 = 0;
+    if (item < n_items) {
+      if (lane < job.tok_count) tok = job.kind == 0 ? job.tok_begin + lane : a.order[job.tok_begin + lane];
+      if (lane + 32 < job.tok_count)
+        tok2 = job.kind == 0 ? job.tok_begin + lane + 32 : a.order[job.tok_begin + lane + 32];
+    }
     while (item < n_items) {
-      const dz_job job = a.jobs[item / nrt];
       const int rt = item - (item / nrt) * nrt;
-      int tok = 0, tok2 = 0;
-      if (job.kind != 0) {
-        if (lane < job.tok_count) tok = a.order[job.tok_begin + lane];
-        if (lane + 32 < job.tok_count) tok2 = a.order[job.tok_begin + lane + 32];
-      }
       const bool is_base = job.kind == 0;
       const bool dense = kind_dense(job.kind);
       const dz_native_delta* ent = is_base ? a.base : a.table + job.slot;
@@ -354,11 +370,12 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       const int bb = dense ? kDenseBlockBytes : sparse_block_bytes(kind_fbits(job.kind));
       const int nch = is_base ? nch_base : dense ? 2 * nkb : ceil_div(nkb, NB_SP);
       const uint32_t abytes = dense ? static_cast<uint32_t>(A_DN) : static_cast<uint32_t>(RG * NB_SP * bb);
-      int id_nxt_raw = 0;
+      // Next item: its id is fetched after chunk 0 goes out (one item of lookahead per CTA keeps
+      // the dynamic schedule balanced), its descriptor and token ids after chunks 1 and 2, so the
+      // dependent global loads overlap this item's stream instead of stalling the ring.
+      int id_nxt_raw = 0, item_nxt = n_items, tok_n = 0, tok2_n = 0;
+      dz_job job_n{0, 0, 0, 0};
       for (int ch = 0; ch < nch; ch++) {
-        // fetch the next item id while the last chunk goes out (one item in flight per CTA, so
-        // the dynamic schedule stays balanced)
-        if (ch == nch - 1 && lane == 0) id_nxt_raw = atomicAdd(&sched[0], 1);
         if (lane == 0) TRACE(1, item, ch);
         mbar_wait(&sm->empty[stage], phase ^ 1);
         if (lane == 0) TRACE(2, item, ch);
@@ -375,21 +392,33 @@ __global__ void __launch_bounds__(NTHREADS, 2)
           nb = (nkb - kb0) < NB_SP ? (nkb - kb0) : NB_SP;
           col0 = kb0 * kBlkCols;
           xbytes = nb * kBlkCols * 2;
-          ax = ch * (NB_SP * bb / 8);
+          ax = kb0;  // 3-D box {block bytes, NB_SP blocks, RG row groups}: coords (0, kb0, rg0)
           ay = rt * RG;
+        }
+        const bool last = ch == nch - 1;
+        if (last) {  // token ids ride with the last chunk (the consumers' epilogue needs them)
+          if (lane < job.tok_count) sm->tok_ids[stage][lane] = tok;
+          if (lane + 32 < job.tok_count) sm->tok_ids[stage][lane + 32] = tok2;
+          __syncwarp();
         }
         if (lane == 0) {
           StageHdr h;
           h.item = item; h.rt = rt; h.kind = job.kind;
           h.tok_begin = job.tok_begin; h.tok_count = job.tok_count; h.nb = nb;
-          h.flags = (ch == 0 ? 1 : 0) | (ch == nch - 1 ? 2 : 0);
+          h.flags = (ch == 0 ? 1 : 0) | (last ? 2 : 0);
           h.pad = 0;
           sm->hdr[stage] = h;
           const uint32_t xb = is_base ? static_cast<uint32_t>(KC_DN * BASE_N * 2)
                                       : static_cast<uint32_t>(job.tok_count * xbytes);
-          mbar_arrive_expect_tx(&sm->full[stage], abytes + xb);
-          tma_load_2d(sbuf, amap, ax, ay, &sm->full[stage], pol_stream);
+          TRACE(6, item, ch);
+          mbar_arrive_expect_tx(&sm->full[stage], abytes + xb);  // release: orders the smem writes above
+          TRACE(7, item, ch);
+          if (dense)
+            tma_load_2d(sbuf, amap, ax, ay, &sm->full[stage], pol_stream);
+          else
+            tma_load_3d(sbuf, amap, 0, ax, ay, &sm->full[stage], pol_stream);
           if (is_base) tma_load_2d(sbuf + A_DN, &xmap, col0, job.tok_begin, &sm->full[stage], pol_keep);
+          TRACE(8, item, ch);
         }
         if (!is_base) {
           const int aoff = dense ? A_DN : A_SP;
@@ -401,9 +430,25 @@ __global__ void __launch_bounds__(NTHREADS, 2)
             tma_load_1d(sbuf + aoff + (lane + 32) * xs, a.X + static_cast<int64_t>(tok2) * a.ldx + col0,
                         static_cast<uint32_t>(xbytes), &sm->full[stage], pol_keep);
         }
+        if (lane == 0) TRACE(9, item, ch);
         if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
+        // ---- next-item prefetch, spread over the first chunks ----
+        if (ch == 0 && lane == 0) id_nxt_raw = atomicAdd(&sched[0], 1);
+        if (ch == (nch > 1 ? 1 : 0)) {
+          item_nxt = __shfl_sync(0xffffffffu, id_nxt_raw, 0);
+          if (item_nxt < n_items) job_n = a.jobs[item_nxt / nrt];
+        }
+        if (ch == (nch > 2 ? 2 : nch - 1) && item_nxt < n_items) {
+          if (lane < job_n.tok_count)
+            tok_n = job_n.kind == 0 ? job_n.tok_begin + lane : a.order[job_n.tok_begin + lane];
+          if (lane + 32 < job_n.tok_count)
+            tok2_n = job_n.kind == 0 ? job_n.tok_begin + lane + 32 : a.order[job_n.tok_begin + lane + 32];
+        }
       }
-      item = __shfl_sync(0xffffffffu, id_nxt_raw, 0);
+      item = item_nxt;
+      job = job_n;
+      tok = tok_n;
+      tok2 = tok2_n;
     }
     mbar_wait(&sm->empty[stage], phase ^ 1);
     if (lane == 0) {
@@ -450,11 +495,82 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     }
   } else {
     // ===================== consumers =====================
+    int trace_i = 0;
+    (void)trace_i;
     float acc[MR][NT_DN][4];  // dense deltas use all NT_DN tiles, sparse deltas the first NT_SP
     int stage = 0;
     uint32_t phase = 0;
     int nbase = 0;
+    // Row-tile completion: after an item's partial stores (named barrier over the consumer warps)
+    // thread 0 bumps tile_cnt with an acq_rel atomic; its result is only examined at the NEXT
+    // epilogue (or at exit), so the round trip never stalls the stream. The consumers of the CTA
+    // that completed a tile then write its Y = act(Pb + Pd) with batched 16-B loads.
     const int ctid = threadIdx.x;  // 0 .. NW*32-1
+    int pend_rt = -1, pend_old = 0;  // meaningful in thread 0 only
+    auto combine = [&](int crt) {
+      const int r0 = crt * RT;
+      const int nr = (a.out - r0) < RT ? (a.out - r0) : RT;
+      const bool has_base = a.base != nullptr;
+      const bool vec = (nr % 4 == 0) && (a.out % 4 == 0) && (a.ldy % 4 == 0);
+      if (vec) {
+        const int nq = nr / 4;  // float4 per token row
+        const int total = a.T * nq;
+        for (int base_i = 0; base_i < total; base_i += NW * 32 * 2) {
+          float4 d[2], b[2];
+#pragma unroll
+          for (int u = 0; u < 2; u++) {
+            const int i = base_i + u * NW * 32 + ctid;
+            if (i < total) {
+              const int64_t o = static_cast<int64_t>(i / nq) * a.out + r0 + (i % nq) * 4;
+              d[u] = __ldcg(reinterpret_cast<const float4*>(Pd + o));
+              b[u] = has_base ? __ldcg(reinterpret_cast<const float4*>(Pb + o)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 2; u++) {
+            const int i = base_i + u * NW * 32 + ctid;
+            if (i < total) {
+              float y[4] = {b[u].x + d[u].x, b[u].y + d[u].y, b[u].z + d[u].z, b[u].w + d[u].w};
+              if (a.act == DZ_ACT_TANH)
+                for (int q = 0; q < 4; q++) y[q] = tanhf(y[q]);
+              const int64_t yo = static_cast<int64_t>(i / nq) * a.ldy + r0 + (i % nq) * 4;
+              if (a.y_dtype == DZ_F32) {
+                *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.Y) + yo) = make_float4(y[0], y[1], y[2], y[3]);
+              } else {
+                __nv_bfloat162 lo = __floats2bfloat162_rn(y[0], y[1]), hi = __floats2bfloat162_rn(y[2], y[3]);
+                uint2 pk = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+                *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.Y) + yo) = pk;
+              }
+            }
+          }
+        }
+      } else {
+        for (int idx = ctid; idx < a.T * nr; idx += NW * 32) {
+          const int tk = idx / nr, r = r0 + idx % nr;
+          const int64_t o = static_cast<int64_t>(tk) * a.out + r;
+          float y = __ldcg(Pd + o);
+          if (has_base) y = __ldcg(Pb + o) + y;
+          if (a.act == DZ_ACT_TANH) y = tanhf(y);
+          if (a.y_dtype == DZ_F32)
+            reinterpret_cast<float*>(a.Y)[static_cast<int64_t>(tk) * a.ldy + r] = y;
+          else
+            reinterpret_cast<__nv_bfloat16*>(a.Y)[static_cast<int64_t>(tk) * a.ldy + r] = __float2bfloat16_rn(y);
+        }
+      }
+      if (ctid == 0) tile_cnt[crt] = 0;  // self-reset for the next launch
+    };
+    // resolve the pending completion (if any) and register `new_rt` (-1: none) as the next one
+    auto rotate_pending = [&](int new_rt) {
+      named_bar_sync(1, NW * 32);  // this item's partial stores (all consumer warps) precede ...
+      if (ctid == 0) {
+        sm->combine_rt = (pend_rt >= 0 && pend_old == a.n_jobs - 1) ? pend_rt : -1;
+        if (new_rt >= 0) pend_old = atom_add_acq_rel_gpu(&tile_cnt[new_rt], 1);  // ... this release
+        pend_rt = new_rt;
+      }
+      named_bar_sync(1, NW * 32);
+      const int crt = sm->combine_rt;
+      if (crt >= 0) combine(crt);
+    };
     while (true) {
       mbar_wait(&sm->full[stage], phase);
       const StageHdr h = sm->hdr[stage];
@@ -465,7 +581,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       const int nrv = (n16 - rg0) < MR ? (n16 - rg0) : MR;  // row groups of this warp inside `out`
       const uint32_t sbuf = smem_u32(stages + static_cast<size_t>(stage) * STAGE_BYTES);
       const int nt = ceil_div(h.tok_count, 8);
-      if (!is_base) {
+      if (!is_base && !(a.debug & 1)) {
         if (h.flags & 1) {
 #pragma unroll
           for (int r = 0; r < MR; r++)
@@ -481,23 +597,16 @@ __global__ void __launch_bounds__(NTHREADS, 2)
             const uint32_t off2 = off | (off << 16);
             if (h.kind != DZ_KIND_SPARSE2) {
               const uint32_t sA = sbuf + warp * MR * NB_SP * sparse_block_bytes(4);
-              if (nt == 1) sparse_chunk<4, 1>(acc, sA, xl, h.nb, nrv, off2, lane);
-              else sparse_chunk<4, 2>(acc, sA, xl, h.nb, nrv, off2, lane);
+              sparse_chunk<4, NT_SP>(acc, sA, xl, h.nb, nrv, off2, lane);
             } else {
               const uint32_t sA = sbuf + warp * MR * NB_SP * sparse_block_bytes(2);
-              if (nt == 1) sparse_chunk<2, 1>(acc, sA, xl, h.nb, nrv, off2, lane);
-              else sparse_chunk<2, 2>(acc, sA, xl, h.nb, nrv, off2, lane);
+              sparse_chunk<2, NT_SP>(acc, sA, xl, h.nb, nrv, off2, lane);
             }
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm->empty[stage]);
-      if (lane == 0 && warp == 0) TRACE(4, h.item, stage);
-      if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
-
       if (h.flags & 2) {
-        // ---- item epilogue: partial -> workspace, then row-tile completion ----
+        // ---- item epilogue: partial -> workspace ----
         if (is_base) {
           const int buf = nbase & 1;
           mbar_wait(&sm->tmem_full[buf], (nbase >> 1) & 1);
@@ -508,40 +617,17 @@ __global__ void __launch_bounds__(NTHREADS, 2)
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm->tmem_empty[buf]);
           nbase++;
-        } else {
-          named_bar_sync(1, NW * 32);  // tok_ids reuse guard
-          for (int tk = ctid; tk < h.tok_count; tk += NW * 32) sm->tok_ids[tk] = a.order[h.tok_begin + tk];
-          named_bar_sync(1, NW * 32);
-          if (nrv > 0) write_partial(acc, nt, Pd, a.out, rg0, h.tok_count, sm->tok_ids, lane);
+        } else if (nrv > 0) {
+          write_partial(acc, nt, Pd, a.out, rg0, h.tok_count, sm->tok_ids[stage], lane);
         }
-        named_bar_sync(1, NW * 32);
-        if (ctid == 0) {
-          // acq_rel at gpu scope: releases this CTA's partial stores (ordered before it by bar.sync;
-          // fence cumulativity) and acquires every earlier item's partials for the combine.
-          const int old = atom_add_acq_rel_gpu(&tile_cnt[h.rt], 1);
-          sm->last_flag = (old == a.n_jobs - 1);
-        }
-        named_bar_sync(1, NW * 32);
-        if (sm->last_flag) {
-          const int r0 = h.rt * RT;
-          const int nr = (a.out - r0) < RT ? (a.out - r0) : RT;
-          const bool has_base = a.base != nullptr;
-          for (int idx = ctid; idx < a.T * nr; idx += NW * 32) {
-            const int tk = idx / nr, r = r0 + idx % nr;
-            const int64_t o = static_cast<int64_t>(tk) * a.out + r;
-            float y = __ldcg(Pd + o);
-            if (has_base) y = __ldcg(Pb + o) + y;
-            if (a.act == DZ_ACT_TANH) y = tanhf(y);
-            if (a.y_dtype == DZ_F32)
-              reinterpret_cast<float*>(a.Y)[static_cast<int64_t>(tk) * a.ldy + r] = y;
-            else
-              reinterpret_cast<__nv_bfloat16*>(a.Y)[static_cast<int64_t>(tk) * a.ldy + r] = __float2bfloat16_rn(y);
-          }
-          if (ctid == 0) tile_cnt[h.rt] = 0;  // self-reset for the next launch
-        }
-        if (lane == 0 && warp == 0) TRACE(5, h.item, 0);
+        rotate_pending(h.rt);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm->empty[stage]);
+      if (lane == 0 && warp == 0) TRACE(4, h.item, stage);
+      if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
     }
+    rotate_pending(-1);  // resolve the last pending completion
   }
   tc_fence_before();
   __syncthreads();
@@ -605,11 +691,23 @@ extern "C" int dz_native_delta_init(dz_native_delta* e, const void* blocks, int3
   e->rows = rows;
   e->cols = cols;
   const int nkb = ceil_div(cols, kBlkCols), n16 = ceil_div(rows, kBlkRows);
-  const int bb = kind == DZ_KIND_DENSE ? kDenseBlockBytes : sparse_block_bytes(kind_fbits(kind));
-  const uint32_t box0 = kind == DZ_KIND_DENSE ? DN_HALF / 8 : NB_SP * bb / 8;
-  return encode_2d(reinterpret_cast<CUtensorMap*>(e->tmap), CU_TENSOR_MAP_DATA_TYPE_UINT64, blocks,
-                   static_cast<uint64_t>(nkb) * bb / 8, static_cast<uint64_t>(n16), static_cast<uint64_t>(nkb) * bb,
-                   box0, RG, CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (kind == DZ_KIND_DENSE)
+    return encode_2d(reinterpret_cast<CUtensorMap*>(e->tmap), CU_TENSOR_MAP_DATA_TYPE_UINT64, blocks,
+                     static_cast<uint64_t>(nkb) * kDenseBlockBytes / 8, static_cast<uint64_t>(n16),
+                     static_cast<uint64_t>(nkb) * kDenseBlockBytes, DN_HALF / 8, RG, CU_TENSOR_MAP_SWIZZLE_NONE);
+  // sparse: 3-D view {block bytes / 8, blocks along K, row groups}; one box = NB_SP blocks x RG groups
+  const int bb = sparse_block_bytes(kind_fbits(kind));
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return DZ_E_CUDA;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(bb / 8), static_cast<cuuint64_t>(nkb),
+                              static_cast<cuuint64_t>(n16)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(bb), static_cast<cuuint64_t>(nkb) * bb};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(bb / 8), NB_SP, RG};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = fn(reinterpret_cast<CUtensorMap*>(e->tmap), CU_TENSOR_MAP_DATA_TYPE_UINT64, 3,
+                        const_cast<void*>(blocks), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? DZ_OK : DZ_E_CUDA;
 }
 
 extern "C" int dz_base_init(dz_native_delta* e, const uint16_t* W, int64_t ldw, int32_t rows, int32_t cols) {
@@ -670,14 +768,22 @@ extern "C" int dz_sbmm(const dz_sbmm_args* a, void* stream) {
 }
 
 #ifdef DZ_TRACE
+// host: copy out {warp, t, ev, a0, a1} tuples of the traced CTA, then reset
 extern "C" int dz_trace_read(unsigned long long* host, int max_events) {
+  static unsigned long long buf[8][1024][2];
+  int cnt[8];
+  cudaMemcpyFromSymbol(cnt, dz_trace_cnt, sizeof(cnt));
+  cudaMemcpyFromSymbol(buf, dz_trace_buf, sizeof(buf));
   int n = 0;
-  cudaMemcpyFromSymbol(&n, dz_trace_n, sizeof(int));
-  if (n > max_events) n = max_events;
-  if (n > 8192) n = 8192;
-  cudaMemcpyFromSymbol(host, dz_trace_buf, sizeof(unsigned long long) * 4 * n);
-  int zero = 0;
-  cudaMemcpyToSymbol(dz_trace_n, &zero, sizeof(int));
+  for (int w = 0; w < 8; w++)
+    for (int i = 0; i < cnt[w] && i < 1024 && n < max_events; i++, n++) {
+      host[4 * n + 0] = buf[w][i][0];
+      host[4 * n + 1] = (buf[w][i][1] >> 56) | (static_cast<unsigned long long>(w) << 8);
+      host[4 * n + 2] = (buf[w][i][1] >> 16) & 0xFFFFFFFFull;
+      host[4 * n + 3] = buf[w][i][1] & 0xFFFFull;
+    }
+  int zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpyToSymbol(dz_trace_cnt, zero, sizeof(zero));
   int neg = -1;
   cudaMemcpyToSymbol(dz_trace_cta, &neg, sizeof(int));
   return n;

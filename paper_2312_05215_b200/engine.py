@@ -209,7 +209,7 @@ def prepare_x(X: torch.Tensor) -> torch.Tensor:
 
 def sbmm_forward(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: DeltaTable,
                  y_dtype: torch.dtype = torch.bfloat16, act: int = L.DZ_ACT_NONE, Y: torch.Tensor | None = None,
-                 workspace: Workspace | None = None, grid: int = 0) -> torch.Tensor:
+                 workspace: Workspace | None = None, grid: int = 0, debug: int = 0) -> torch.Tensor:
     """Y[T, out] = X W_base^T + ΔW_{slot(t)} x_t for all t, one fused launch (inference.py:126-154)."""
     T, inp = int(X.shape[0]), int(X.shape[1])
     out = table.out if base is None else base.out
@@ -235,5 +235,6 @@ def sbmm_forward(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: De
     a.jobs, a.n_jobs = plan.jobs.data_ptr(), plan.n_jobs
     a.workspace = ws.data_ptr()
     a.grid = grid
+    a.debug = debug
     L.check(L.lib().dz_sbmm(C.byref(a), stream_ptr()), "sbmm")
     return Y

@@ -89,7 +89,7 @@ def test_plan_is_stable_group_by_delta(lib, kat):
         assert covered == list(range(len(ids)))
         for j in jobs:
             if j[0] >= 0:
-                assert j[2] <= (64 if j[3] == 3 else 16)
+                assert j[2] <= (32 if j[3] == 3 else 8)
                 assert all(ids[t] == j[0] for t in order[j[1]:j[1] + j[2]])
 
 

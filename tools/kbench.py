@@ -40,6 +40,7 @@ def main():
     p.add_argument("--bits", type=int, default=4)
     p.add_argument("--grid", type=int, default=0)
     p.add_argument("--case", default="")
+    p.add_argument("--debug", type=int, default=0)
     args = p.parse_args()
     dev = torch.device("cuda")
     gen = torch.Generator(device=dev)
@@ -63,7 +64,7 @@ def main():
         if args.case and name != args.case:
             continue
         plan = Plan(sl, table.kinds, D, with_base=wb)
-        us = timeit(lambda: sbmm_forward(X, plan, base if wb else None, table, workspace=ws, grid=args.grid))
+        us = timeit(lambda: sbmm_forward(X, plan, base if wb else None, table, workspace=ws, grid=args.grid, debug=args.debug))
         res[name] = {"us": round(us, 1), "GBps": round(nbytes / us / 1e3, 1), "n_jobs": plan.n_jobs}
     print(json.dumps({"shape": [out, inp], "D": D, "T": T, **res}))
 

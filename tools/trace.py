@@ -33,16 +33,17 @@ lib = L.lib()
 lib.dz_trace_read.restype = C.c_int
 lib.dz_trace_read.argtypes = [C.c_void_p, C.c_int]
 buf = np.zeros((8192, 4), dtype=np.uint64)
+DBG = int(os.environ.get("DEBUG", "0"))
 for _ in range(3):
-    sbmm_forward(X, plan, base if case != "deltas_only" else None, table, workspace=ws)
+    sbmm_forward(X, plan, base if case != "deltas_only" else None, table, workspace=ws, debug=DBG)
 torch.cuda.synchronize()
 lib.dz_trace_read(buf.ctypes.data, 8192)
-sbmm_forward(X, plan, base if case != "deltas_only" else None, table, workspace=ws)
+sbmm_forward(X, plan, base if case != "deltas_only" else None, table, workspace=ws, debug=DBG)
 torch.cuda.synchronize()
 n = lib.dz_trace_read(buf.ctypes.data, 8192)
 ev = buf[:n]
 ev = ev[np.argsort(ev[:, 0], kind="stable")]
 t0 = ev[0, 0]
 print(f"events {n}")
-for row in ev[:400]:
-    print(f"{(int(row[0]) - int(t0)) / 1000:9.2f} us  ev{int(row[1])} item={int(row[2])} x={int(row[3])}")
+for row in ev[:1500]:
+    print(f"{(int(row[0]) - int(t0)):9d} cyc  w{int(row[1]) >> 8} ev{int(row[1]) & 255} item={int(row[2])} x={int(row[3])}")
