@@ -188,30 +188,43 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+FUSED = {"qkv": ("q", "k", "v"), "o": ("o",), "gate_up": ("gate", "up"), "down": ("down",)}
+
+
 def build_stack(layers, rank, world, device):
-    """Per layer: 7 linears, each = (base native blocks, delta table of 32 natives)."""
+    """Per layer 4 fused linears (QKV and gate/up row-concatenated: they read the same input),
+    each = (base W, delta table of 32 natives). Deltas are generated per original linear and
+    concatenated, so bytes and math are exactly those of the 7 separate linears."""
     import torch
-    from paper_2312_05215_b200 import _lib as L
     from paper_2312_05215_b200.device import ErrFlag
-    from paper_2312_05215_b200.engine import DeltaTable, NativeBase
+    from paper_2312_05215_b200.engine import DeltaTable, NativeBase, concat_rows
     from paper_2312_05215_b200.synth import llama_linears, random_base, random_native_delta
     from paper_2312_05215_b200.tp import TpLinear
 
     gen = torch.Generator(device=device)
     err = ErrFlag(device)
+    shapes = {n: (o, i) for n, o, i in llama_linears(MODEL)}
+    names = [n for n, _, _ in llama_linears(MODEL)]
     stack = []
     for l in range(layers):
         lin = {}
-        for j, (name, out, inp) in enumerate(llama_linears(MODEL)):
-            gen.manual_seed(10_000 + 7 * l + j)
-            W = random_base(out, inp, gen, device)
-            nats = [random_native_delta(out, inp, BITS, gen, device, err) for _ in range(D_DELTAS)]
+        for fname, members in FUSED.items():
+            Ws, per_delta = [], [[] for _ in range(D_DELTAS)]
+            for m in members:
+                out, inp = shapes[m]
+                gen.manual_seed(10_000 + 7 * l + names.index(m))
+                Ws.append(random_base(out, inp, gen, device))
+                for d in range(D_DELTAS):
+                    per_delta[d].append(random_native_delta(out, inp, BITS, gen, device, err))
+            W = torch.cat(Ws) if len(Ws) > 1 else Ws[0]
+            nats = [concat_rows(p) if len(p) > 1 else p[0] for p in per_delta]
+            out, inp = int(W.shape[0]), int(W.shape[1])
             if world == 1:
-                lin[name] = (NativeBase(W), DeltaTable(nats, out, inp), out, inp)
+                lin[fname] = (NativeBase(W), DeltaTable(nats, out, inp), out, inp)
             else:
-                axis = "row" if name in ("o", "down") else "column"
-                lin[name] = TpLinear(W, nats, axis, rank, world)
-            del W
+                axis = "row" if fname in ("o", "down") else "column"
+                lin[fname] = TpLinear(W, nats, axis, rank, world)
+            del W, Ws, per_delta
         stack.append(lin)
         torch.cuda.synchronize()
     err.raise_if_set("synthetic delta upload")
@@ -249,19 +262,21 @@ def main():
     shapes = dict((n, (o, i)) for n, o, i in llama_linears(MODEL))
     hid, inter = shapes["q"][1], shapes["gate"][0]
 
-    # activation buffers (static addresses for graph capture)
+    # activation buffers (static addresses for graph capture). Attention is out of scope: o reads
+    # the v slice of the fused QKV output, down reads the up slice of the fused gate/up output.
     def buf(cols):
         return torch.zeros(T_TOKENS, cols, dtype=torch.bfloat16, device=device)
 
+    fshape = {f: (sum(shapes[m][0] for m in ms), shapes[ms[0]][1]) for f, ms in FUSED.items()}
+    x_in = buf(hid)
     if world == 1:
-        x_in = buf(hid)
-        outs = {n: buf(shapes[n][0]) for n in shapes}
+        outs = {f: buf(fshape[f][0]) for f in FUSED}
+        v_in = outs["qkv"][:, shapes["q"][0] + shapes["k"][0]:]
+        up_in = outs["gate_up"][:, shapes["gate"][0]:]
     else:
-        x_in = buf(hid)
-        outs = {}
-        for n, lin in stack[0].items():
-            cols = lin.table.out if n not in ("o", "down") else hid
-            outs[n] = buf(cols)
+        outs = {f: buf(stack[0][f].table.out if f in ("qkv", "gate_up") else hid) for f in FUSED}
+        v_in = outs["qkv"][:, 2 * outs["qkv"].shape[1] // 3:]
+        up_in = outs["gate_up"][:, outs["gate_up"].shape[1] // 2:]
 
     def linear(lin, name, X, Y):
         if world == 1:
@@ -271,13 +286,15 @@ def main():
             Yl = lin.forward(X, plan)
             Y.copy_(Yl) if Yl.data_ptr() != Y.data_ptr() else None
 
+    step_order = [("qkv", "h"), ("o", "v"), ("gate_up", "h"), ("down", "up")]
+
     def step():
         h = x_in
         for lin in stack:
-            for n in ("q", "k", "v", "gate", "up"):
-                linear(lin[n], n, h, outs[n])
-            linear(lin["o"], "o", outs["v"], outs["o"])
-            linear(lin["down"], "down", outs["up"], outs["down"])
+            src = {"h": h, "v": v_in, "up": up_in}
+            for f, s_ in step_order:
+                linear(lin[f], f, src[s_], outs[f])
+                src = {"h": h, "v": v_in, "up": up_in}
             h = outs["down"]
         return h
 
@@ -334,27 +351,30 @@ def main():
 
     # ---- per-launch kernel durations (eager, events between consecutive launches on the stream)
     lin_bytes = {n: linear_algorithmic_bytes(o, i, BITS, D_DELTAS, T_TOKENS) for n, (o, i) in shapes.items()}
+    f_bytes = {f: sum(lin_bytes[m] for m in ms) - (len(ms) - 1) * (2 * T_TOKENS * fshape[f][1] + 4 * T_TOKENS)
+               for f, ms in FUSED.items()}  # the shared input x is read once per fused launch
     if world > 1:
-        lin_bytes = {n: b // world for n, b in lin_bytes.items()}
+        f_bytes = {n: b // world for n, b in f_bytes.items()}
     evs = []
     torch.cuda.synchronize()
     h = x_in
     order = []
     for lin in stack:
-        for n, X, Y in (("q", h, outs["q"]), ("k", h, outs["k"]), ("v", h, outs["v"]), ("gate", h, outs["gate"]),
-                        ("up", h, outs["up"]), ("o", outs["v"], outs["o"]), ("down", outs["up"], outs["down"])):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            linear(lin[n], n, X, Y)
-            b.record(stream)
-            evs.append((a, b))
-            order.append(n)
+        src = {"h": h, "v": v_in, "up": up_in}
+        for f, s_ in step_order:
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            linear(lin[f], f, src[s_], outs[f])
+            b_.record(stream)
+            evs.append((a_, b_))
+            order.append(f)
         h = outs["down"]
     torch.cuda.synchronize()
-    durs = np.array([a.elapsed_time(b) for a, b in evs])  # ms
+    durs = np.array([a_.elapsed_time(b_) for a_, b_ in evs])  # ms
     per_name = {}
     for n, d in zip(order, durs):
         per_name.setdefault(n, []).append(d)
+    lin_bytes = f_bytes
     kern_bytes = sum(lin_bytes[n] for n in order)
     kern_ms = float(durs.sum())
     achieved = kern_bytes / (kern_ms * 1e-3) / 1e9
@@ -408,7 +428,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random bf16 base, random reference-layout 4-bit 2:4 deltas uploaded via dz_repack_sparse)",
-            "config": {"workload": f"llama2-7b decoder stack, {args.layers} layers x 7 linears (q,k,v,o,gate,up,down), "
+            "config": {"workload": f"llama2-7b decoder stack, {args.layers} layers x 7 linears (q,k,v,o,gate,up,down; "
+                                   f"QKV and gate/up row-fused into one launch each), "
                                    f"D={D_DELTAS} 4-bit 2:4 deltas (gs=128), T={T_TOKENS} decode tokens, ids=perm(i%32)",
                        "global_batch": T_TOKENS, "parallelism": f"tp{world}" if world > 1 else "single",
                        "l2": "inputs > L2 (97.5 GB streamed per step)", "cuda_graph": graph is not None,
@@ -416,7 +437,7 @@ def main():
             "gpu_launches": len(order) * args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "k_sbmm (fused base GEMM + SBMM), all 224 launches of one step",
+                         "kernel": "k_sbmm (fused base GEMM + SBMM), all 4 x layers launches of one step (QKV, o, gate/up, down)",
                          "per_launch_us": {n: float(np.mean(v) * 1e3) for n, v in per_name.items()},
                          "step_GBps": step_bytes / (ms * 1e-3) / 1e9},
             "clocks": clocks,

@@ -93,8 +93,8 @@ typedef struct dz_sbmm_args {
   const int32_t* order;     /* device [T]: token indices stably sorted by slot       */
   const dz_job* jobs;       /* device [n_jobs]                                       */
   int32_t n_jobs;
-  void* workspace;          /* dz_sbmm_workspace_bytes(T, out) bytes; counters must be
-                               zero the first time (they self-reset after every call) */
+  void* workspace;          /* dz_sbmm_workspace_bytes(T, out) bytes, zeroed once at
+                               allocation; the kernel leaves it zero after every call */
   int32_t grid;             /* persistent CTAs; 0 = one per SM                       */
   int32_t debug;            /* 0; bit 0 = skip consumer math (pipeline bandwidth probe) */
 } dz_sbmm_args;
@@ -166,6 +166,8 @@ int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t n_slo
  * Deterministic and batch-invariant: a token's result does not depend on the
  * other tokens in the call. */
 size_t dz_sbmm_workspace_bytes(int32_t T, int32_t out);
+/* Resident CTAs per SM of the fused kernel (diagnostics; < 0 on error). */
+int dz_sbmm_ctas_per_sm(void);
 int dz_sbmm(const dz_sbmm_args* args, void* stream);
 
 #ifdef __cplusplus

@@ -79,6 +79,7 @@ SIGNATURES = {
                           C.c_int32, C.POINTER(C.c_int32)]),
     "dz_sbmm_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int32]),
     "dz_sbmm": (C.c_int, [C.POINTER(DzSbmmArgs), C.c_void_p]),
+    "dz_sbmm_ctas_per_sm": (C.c_int, []),
 }
 
 _lib = None

@@ -21,10 +21,12 @@
 //    (the reference's index nibble IS the sparse-MMA metadata), fp32 accumulation; dense-delta
 //    stages use mma m16n8k16. They also drain the base accumulator from TMEM (tcgen05.ld).
 //
-// At the end of an item the consumers write its fp32 partial (base -> Pb, delta -> Pd; tokens
-// are disjoint across delta jobs) and the LAST item of a row tile (per-tile counter, acq_rel
-// atomic) writes Y = act(Pb + Pd) — no separate add kernel, no atomics on data, deterministic, and
-// batch-invariant (a token's K order never depends on the rest of the batch).
+// Merge: every output element y[t][r] receives exactly two fp32 contributions — the base job of
+// token t and the single delta job of t's group. Each contributor publishes its value with a 64-bit
+// CAS on a {value, count} workspace word; the second arriver computes fl(base + delta) (two-term
+// fp32 addition is commutative, so the result does not depend on arrival order), applies the
+// activation, writes Y and resets the word. No partial buffers, no combine pass, no separate add
+// kernel; deterministic and batch-invariant (a token's K order never depends on the batch).
 #include <cuda.h>
 
 #include <cstddef>
@@ -40,6 +42,8 @@
 __device__ unsigned long long dz_trace_buf[8][1024][2];
 __device__ int dz_trace_cnt[8];
 __device__ volatile int dz_trace_cta = -1;
+__device__ unsigned long long dz_item_trace[65536][3];  // per item: start, end, (cta << 32 | kind)
+#define ITEM_TRACE(slot, item, val) do { if ((item) < 65536) dz_item_trace[(item)][(slot)] = (val); } while (0)
 #define TRACE(ev, a0, a1) do { if (blockIdx.x == 0 && trace_i < 1024) { \
   dz_trace_buf[threadIdx.x >> 5][trace_i][0] = clock64(); \
   dz_trace_buf[threadIdx.x >> 5][trace_i][1] = (static_cast<unsigned long long>(ev) << 56) | \
@@ -47,17 +51,19 @@ __device__ volatile int dz_trace_cta = -1;
   trace_i++; dz_trace_cnt[threadIdx.x >> 5] = trace_i; } } while (0)
 #else
 #define TRACE(ev, a0, a1) do {} while (0)
+#define ITEM_TRACE(slot, item, val) do {} while (0)
 #endif
 
 namespace dz {
 
-constexpr int NW = 4;                     // consumer warps per CTA
+constexpr int NW = 8;                     // consumer warps per CTA (one CTA per SM)
 constexpr int MR = 2;                     // 16-row groups per consumer warp
 constexpr int WARP_PROD = NW;             // TMA producer warp
 constexpr int WARP_MMA = NW + 1;          // tcgen05 issuer / TMEM owner warp
 constexpr int NTHREADS = (NW + 2) * 32;
 constexpr int RG = NW * MR;               // row groups per item
-constexpr int RT = RG * kBlkRows;         // rows per item (128) == UMMA M
+constexpr int RT = RG * kBlkRows;         // rows per item (256) == 2 x UMMA M
+constexpr int UMMA_M = 128;
 constexpr int NB_SP = 4;                  // sparse chunk = 4 blocks = 512 columns (one 3-D TMA box)
 constexpr int NT_SP = 1;                  // n-tiles per sparse job (8 tokens, dz_plan)
 constexpr int NT_DN = 4;                  // n-tiles per dense-delta job (32 tokens, dz_plan)
@@ -65,17 +71,16 @@ constexpr int KC_DN = 64;                 // dense / base chunk = 64 columns
 constexpr int BASE_N = 64;                // tokens per base job == UMMA N
 constexpr int XS_SP = NB_SP * kBlkCols * 2 + 16;  // smem bytes per staged token row; +16 B so the
 constexpr int XS_DN = KC_DN * 2 + 16;             //   8 rows of an ldmatrix hit distinct banks
-constexpr int A_SP = RG * NB_SP * sparse_block_bytes(4);  // 26624
+constexpr int A_SP = RG * NB_SP * sparse_block_bytes(4);  // 53248
 constexpr int X_SP = NT_SP * 8 * XS_SP;                   // 8320
 constexpr int DN_HALF = kDenseBlockBytes / 2;             // 2048
-constexpr int A_DN = RG * DN_HALF;                        // 16384 == 128 rows x 128 B (base W tile)
+constexpr int A_DN = RG * DN_HALF;                        // 32768 == 256 rows x 128 B (base W tile)
 constexpr int X_DN = 64 * XS_DN;                          // 9216 (>= 64 x 128 B swizzled X tile)
 constexpr int STAGE_BYTES = ((A_SP + X_SP > A_DN + X_DN ? A_SP + X_SP : A_DN + X_DN) + 1023) / 1024 * 1024;
 constexpr int NSTAGE = 3;
 constexpr int JOB_DN_TOK = BASE_N;        // largest token count of a job
-constexpr int kMaxTiles = 4096;           // row tiles per call (out <= 524288)
-constexpr int TMEM_COLS = 2 * BASE_N;     // two fp32 accumulators (double buffer)
-constexpr uint32_t IDESC_BASE = umma_idesc_bf16(RT, BASE_N);
+constexpr int TMEM_COLS = 2 * 2 * BASE_N; // (double buffer) x (two M=128 halves) fp32 accumulators
+constexpr uint32_t IDESC_BASE = umma_idesc_bf16(UMMA_M, BASE_N);
 
 struct StageHdr {
   int item;       // -1: end of work
@@ -95,12 +100,26 @@ struct Smem {
   uint64_t tmem_empty[2];
   StageHdr hdr[NSTAGE];
   uint32_t tmem_base;
-  int combine_rt;                    // row tile whose Y the consumers write next (-1: none)
   int tok_ids[NSTAGE][JOB_DN_TOK];  // token ids of the item, staged with its last chunk
 };
 constexpr int SMEM_BYTES = 1024 + STAGE_BYTES * NSTAGE + static_cast<int>(sizeof(Smem));
 
 __device__ __forceinline__ bool kind_dense(int kind) { return kind == 0 || kind == DZ_KIND_DENSE; }
+
+// Item order: all base items first (row tile order; the big ones start early), then the delta
+// items row-tile-major, so row tiles complete (and are combined) progressively through the launch
+// instead of all at the end. dz_plan puts the n_base base jobs first in the job list.
+__device__ __forceinline__ void item_coords(int item, int nrt, int n_jobs, int n_base, int& rt, int& j) {
+  const int nb_items = nrt * n_base;
+  if (item < nb_items) {
+    j = item / nrt;
+    rt = item - j * nrt;
+  } else {
+    const int k = item - nb_items, nd = n_jobs - n_base;
+    rt = k / nd;
+    j = n_base + (k - rt * nd);
+  }
+}
 
 __device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
   int old;
@@ -259,8 +278,90 @@ __device__ __forceinline__ void dense_dispatch(int nt, float (&acc)[MR][NT_DN][4
   }
 }
 
-__device__ __forceinline__ void write_partial(const float (&acc)[MR][NT_DN][4], int nt, float* __restrict__ P,
-                                              int out, int rg0, int tcount, const int* tok_ids, int lane) {
+struct MergeCtx {
+  unsigned long long* slots;  // [T][out] {fp32 value bits, count} words, zero between launches
+  void* Y;
+  int64_t ldy;
+  int out, y_dtype, act;
+  bool has_base;
+};
+
+__device__ __forceinline__ void store_y(const MergeCtx& m, int tok, int row, float v) {
+  if (m.act == DZ_ACT_TANH) v = tanhf(v);
+  const int64_t yo = static_cast<int64_t>(tok) * m.ldy + row;
+  if (m.y_dtype == DZ_F32)
+    reinterpret_cast<float*>(m.Y)[yo] = v;
+  else
+    reinterpret_cast<__nv_bfloat16*>(m.Y)[yo] = __float2bfloat16_rn(v);
+}
+
+// Publish N fp32 contributions v[i] to y[tok[i]][row[i]] (valid[i]). First arriver parks {v, 1};
+// the second computes fl(other + v), writes Y and clears the slot. All N CASes are issued before
+// any result is inspected, so an epilogue costs one atomic round trip, not N. Without a base there
+// is a single contributor and Y is written directly.
+template <int N>
+__device__ __forceinline__ void merge_batch(const MergeCtx& m, const int (&tok)[N], const int (&row)[N],
+                                            const float (&v)[N], const bool (&valid)[N]) {
+  if (!m.has_base) {
+#pragma unroll
+    for (int i = 0; i < N; i++)
+      if (valid[i]) store_y(m, tok[i], row[i], v[i]);
+    return;
+  }
+  unsigned long long old[N];
+#pragma unroll
+  for (int i = 0; i < N; i++) {
+    old[i] = 0ull;
+    if (valid[i])
+      old[i] = atomicCAS(m.slots + static_cast<int64_t>(tok[i]) * m.out + row[i], 0ull,
+                         (1ull << 32) | __float_as_uint(v[i]));
+  }
+#pragma unroll
+  for (int i = 0; i < N; i++) {
+    if (valid[i] && old[i] != 0ull) {  // the other contribution was parked: complete the element
+      store_y(m, tok[i], row[i], __uint_as_float(static_cast<uint32_t>(old[i])) + v[i]);
+      m.slots[static_cast<int64_t>(tok[i]) * m.out + row[i]] = 0ull;  // self-reset for the next launch
+    }
+  }
+}
+
+__device__ __forceinline__ void merge_contribution(const MergeCtx& m, int tok, int row, float v) {
+  const int t[1] = {tok}, r[1] = {row};
+  const float x[1] = {v};
+  const bool ok[1] = {true};
+  merge_batch<1>(m, t, r, x, ok);
+}
+
+// Base accumulators (TMEM, lane = output row, column = token) -> merge. Warp w drains half w/4
+// (rows 128*(w/4)..) of the tile, TMEM lanes 32*(w%4)..+31 (the lanes warp w may access).
+__device__ __forceinline__ void drain_base_accumulator(uint32_t tmem_acc, int warp, int lane, const MergeCtx& m,
+                                                       int row0, int tok_begin, int tcount) {
+  const int q = warp & 3, hm = warp >> 2;
+  const int row = row0 + hm * UMMA_M + 32 * q + lane;
+  const uint32_t taddr = tmem_acc + hm * BASE_N + (static_cast<uint32_t>(32 * q) << 16);
+#pragma unroll 1
+  for (int c = 0; c < BASE_N / 16; c++) {
+    if (c * 16 >= tcount) break;
+    uint32_t v[16];
+    tmem_ld16(taddr + c * 16, v);
+    tmem_ld_wait();
+    int tk[16], rw[16];
+    float x[16];
+    bool ok[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      tk[j] = tok_begin + c * 16 + j;
+      rw[j] = row;
+      x[j] = __uint_as_float(v[j]);
+      ok[j] = row < m.out && c * 16 + j < tcount;
+    }
+    merge_batch<16>(m, tk, rw, x, ok);
+  }
+}
+
+// Dense-delta job partial (mma.sync fragments) -> merge.
+__device__ __forceinline__ void merge_fragments(const float (&acc)[MR][NT_DN][4], int nt, const MergeCtx& m,
+                                                int rg0, int tcount, const int* tok_ids, int lane) {
   const int g = lane >> 2, t = lane & 3;
 #pragma unroll
   for (int r = 0; r < MR; r++) {
@@ -272,28 +373,8 @@ __device__ __forceinline__ void write_partial(const float (&acc)[MR][NT_DN][4], 
         for (int v = 0; v < 4; v++) {
           const int tk = n * 8 + 2 * t + (v & 1);
           const int row = row0 + g + ((v & 2) ? 8 : 0);
-          if (tk < tcount && row < out) P[static_cast<int64_t>(tok_ids[tk]) * out + row] = acc[r][n][v];
+          if (tk < tcount && row < m.out) merge_contribution(m, tok_ids[tk], row, acc[r][n][v]);
         }
-      }
-    }
-  }
-}
-
-// Base accumulator (TMEM, lane = output row, column = token) -> Pb. Warp w owns lanes 32w..32w+31.
-__device__ __forceinline__ void drain_base_accumulator(uint32_t tmem_acc, int warp, int lane, float* __restrict__ Pb,
-                                                       int out, int row0, int tok_begin, int tcount) {
-  const int row = row0 + 32 * warp + lane;
-#pragma unroll
-  for (int c = 0; c < BASE_N / 16; c++) {
-    if (c * 16 >= tcount) break;
-    uint32_t v[16];
-    tmem_ld16(tmem_acc + (static_cast<uint32_t>(32 * warp) << 16) + c * 16, v);
-    tmem_ld_wait();
-    if (row < out) {
-#pragma unroll
-      for (int j = 0; j < 16; j++) {
-        const int tk = c * 16 + j;
-        if (tk < tcount) Pb[static_cast<int64_t>(tok_begin + tk) * out + row] = __uint_as_float(v[j]);
       }
     }
   }
@@ -302,7 +383,7 @@ __device__ __forceinline__ void drain_base_accumulator(uint32_t tmem_acc, int wa
 // ------------------------------------------------------------------------------------------
 // The persistent kernel
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NTHREADS, 2)
+__global__ void __launch_bounds__(NTHREADS, 1)
     k_sbmm(const __grid_constant__ dz_sbmm_args a, const __grid_constant__ CUtensorMap xmap) {
   extern __shared__ uint8_t smem_dyn[];
   // 1024-B alignment for the SWIZZLE_128B tiles
@@ -315,12 +396,17 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   const int nkb = ceil_div(a.in, kBlkCols);
   const int nch_base = ceil_div(a.in, KC_DN);
   const int n_items = nrt * a.n_jobs;
+  const int n_base = a.base != nullptr ? ceil_div(a.T, BASE_N) : 0;  // dz_plan: base jobs first
 
-  int* ws_i = reinterpret_cast<int*>(a.workspace);
-  int* sched = ws_i;              // [0] item counter, [1] finished CTAs
-  int* tile_cnt = ws_i + 64;      // [nrt] (fixed-size region: layout independent of out)
-  float* Pb = reinterpret_cast<float*>(ws_i + 64 + kMaxTiles);
-  float* Pd = Pb + static_cast<int64_t>(a.T) * a.out;
+  int* sched = reinterpret_cast<int*>(a.workspace);  // [0] item counter, [1] finished CTAs
+  MergeCtx mctx;
+  mctx.slots = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(a.workspace) + 256);
+  mctx.Y = a.Y;
+  mctx.ldy = a.ldy;
+  mctx.out = a.out;
+  mctx.y_dtype = a.y_dtype;
+  mctx.act = a.act;
+  mctx.has_base = a.base != nullptr;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; s++) {
@@ -354,7 +440,9 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     int id_raw = 0;
     if (lane == 0) id_raw = atomicAdd(&sched[0], 1);
     int item = __shfl_sync(0xffffffffu, id_raw, 0);
-    dz_job job = item < n_items ? a.jobs[item / nrt] : dz_job{0, 0, 0, 0};
+    int rt = 0, jj = 0;
+    if (item < n_items) item_coords(item, nrt, a.n_jobs, n_base, rt, jj);
+    dz_job job = item < n_items ? a.jobs[jj] : dz_job{0, 0, 0, 0};
     int tok = 0, tok2 = 0;
     if (item < n_items) {
       if (lane < job.tok_count) tok = job.kind == 0 ? job.tok_begin + lane : a.order[job.tok_begin + lane];
@@ -362,7 +450,6 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         tok2 = job.kind == 0 ? job.tok_begin + lane + 32 : a.order[job.tok_begin + lane + 32];
     }
     while (item < n_items) {
-      const int rt = item - (item / nrt) * nrt;
       const bool is_base = job.kind == 0;
       const bool dense = kind_dense(job.kind);
       const dz_native_delta* ent = is_base ? a.base : a.table + job.slot;
@@ -373,11 +460,14 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       // Next item: its id is fetched after chunk 0 goes out (one item of lookahead per CTA keeps
       // the dynamic schedule balanced), its descriptor and token ids after chunks 1 and 2, so the
       // dependent global loads overlap this item's stream instead of stalling the ring.
-      int id_nxt_raw = 0, item_nxt = n_items, tok_n = 0, tok2_n = 0;
+      int id_nxt_raw = 0, item_nxt = n_items, tok_n = 0, tok2_n = 0, rt_n = 0;
       dz_job job_n{0, 0, 0, 0};
       for (int ch = 0; ch < nch; ch++) {
         if (lane == 0) TRACE(1, item, ch);
+        if (lane == 0 && ch == 0)
+          ITEM_TRACE(2, item, (static_cast<unsigned long long>(blockIdx.x) << 32) | static_cast<uint32_t>(job.kind));
         mbar_wait(&sm->empty[stage], phase ^ 1);
+        if (lane == 0 && ch == 0) ITEM_TRACE(0, item, globaltimer());
         if (lane == 0) TRACE(2, item, ch);
         uint8_t* sbuf = stages + static_cast<size_t>(stage) * STAGE_BYTES;
         int nb, col0, xbytes, ax, ay;
@@ -436,7 +526,11 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         if (ch == 0 && lane == 0) id_nxt_raw = atomicAdd(&sched[0], 1);
         if (ch == (nch > 1 ? 1 : 0)) {
           item_nxt = __shfl_sync(0xffffffffu, id_nxt_raw, 0);
-          if (item_nxt < n_items) job_n = a.jobs[item_nxt / nrt];
+          if (item_nxt < n_items) {
+            int j_n = 0;
+            item_coords(item_nxt, nrt, a.n_jobs, n_base, rt_n, j_n);
+            job_n = a.jobs[j_n];
+          }
         }
         if (ch == (nch > 2 ? 2 : nch - 1) && item_nxt < n_items) {
           if (lane < job_n.tok_count)
@@ -446,6 +540,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         }
       }
       item = item_nxt;
+      rt = rt_n;
       job = job_n;
       tok = tok_n;
       tok2 = tok2_n;
@@ -476,12 +571,15 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         tc_fence_after();
         if (lane == 0) {
           const uint32_t sbuf = smem_u32(stages + static_cast<size_t>(stage) * STAGE_BYTES);
-          const uint64_t adesc = umma_desc_sw128(sbuf);
           const uint64_t bdesc = umma_desc_sw128(sbuf + A_DN);
-          const uint32_t tmem_d = tmem_base + buf * BASE_N;
 #pragma unroll
-          for (int k = 0; k < KC_DN / 16; k++)  // K=16 per MMA: +32 B inside the 128-B swizzle atom
-            umma_bf16(tmem_d, adesc + 2 * k, bdesc + 2 * k, IDESC_BASE, (h.flags & 1) && k == 0 ? 0u : 1u);
+          for (int hm = 0; hm < RT / UMMA_M; hm++) {  // rows 128*hm.. of the tile: own accumulator
+            const uint64_t adesc = umma_desc_sw128(sbuf + hm * (UMMA_M * KC_DN * 2));
+            const uint32_t tmem_d = tmem_base + (buf * (RT / UMMA_M) + hm) * BASE_N;
+#pragma unroll
+            for (int k = 0; k < KC_DN / 16; k++)  // K=16 per MMA: +32 B inside the 128-B swizzle atom
+              umma_bf16(tmem_d, adesc + 2 * k, bdesc + 2 * k, IDESC_BASE, (h.flags & 1) && k == 0 ? 0u : 1u);
+          }
           umma_commit(&sm->empty[stage]);
           if (h.flags & 2) umma_commit(&sm->tmem_full[buf]);
         }
@@ -501,76 +599,6 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     int stage = 0;
     uint32_t phase = 0;
     int nbase = 0;
-    // Row-tile completion: after an item's partial stores (named barrier over the consumer warps)
-    // thread 0 bumps tile_cnt with an acq_rel atomic; its result is only examined at the NEXT
-    // epilogue (or at exit), so the round trip never stalls the stream. The consumers of the CTA
-    // that completed a tile then write its Y = act(Pb + Pd) with batched 16-B loads.
-    const int ctid = threadIdx.x;  // 0 .. NW*32-1
-    int pend_rt = -1, pend_old = 0;  // meaningful in thread 0 only
-    auto combine = [&](int crt) {
-      const int r0 = crt * RT;
-      const int nr = (a.out - r0) < RT ? (a.out - r0) : RT;
-      const bool has_base = a.base != nullptr;
-      const bool vec = (nr % 4 == 0) && (a.out % 4 == 0) && (a.ldy % 4 == 0);
-      if (vec) {
-        const int nq = nr / 4;  // float4 per token row
-        const int total = a.T * nq;
-        for (int base_i = 0; base_i < total; base_i += NW * 32 * 2) {
-          float4 d[2], b[2];
-#pragma unroll
-          for (int u = 0; u < 2; u++) {
-            const int i = base_i + u * NW * 32 + ctid;
-            if (i < total) {
-              const int64_t o = static_cast<int64_t>(i / nq) * a.out + r0 + (i % nq) * 4;
-              d[u] = __ldcg(reinterpret_cast<const float4*>(Pd + o));
-              b[u] = has_base ? __ldcg(reinterpret_cast<const float4*>(Pb + o)) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 2; u++) {
-            const int i = base_i + u * NW * 32 + ctid;
-            if (i < total) {
-              float y[4] = {b[u].x + d[u].x, b[u].y + d[u].y, b[u].z + d[u].z, b[u].w + d[u].w};
-              if (a.act == DZ_ACT_TANH)
-                for (int q = 0; q < 4; q++) y[q] = tanhf(y[q]);
-              const int64_t yo = static_cast<int64_t>(i / nq) * a.ldy + r0 + (i % nq) * 4;
-              if (a.y_dtype == DZ_F32) {
-                *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.Y) + yo) = make_float4(y[0], y[1], y[2], y[3]);
-              } else {
-                __nv_bfloat162 lo = __floats2bfloat162_rn(y[0], y[1]), hi = __floats2bfloat162_rn(y[2], y[3]);
-                uint2 pk = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
-                *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.Y) + yo) = pk;
-              }
-            }
-          }
-        }
-      } else {
-        for (int idx = ctid; idx < a.T * nr; idx += NW * 32) {
-          const int tk = idx / nr, r = r0 + idx % nr;
-          const int64_t o = static_cast<int64_t>(tk) * a.out + r;
-          float y = __ldcg(Pd + o);
-          if (has_base) y = __ldcg(Pb + o) + y;
-          if (a.act == DZ_ACT_TANH) y = tanhf(y);
-          if (a.y_dtype == DZ_F32)
-            reinterpret_cast<float*>(a.Y)[static_cast<int64_t>(tk) * a.ldy + r] = y;
-          else
-            reinterpret_cast<__nv_bfloat16*>(a.Y)[static_cast<int64_t>(tk) * a.ldy + r] = __float2bfloat16_rn(y);
-        }
-      }
-      if (ctid == 0) tile_cnt[crt] = 0;  // self-reset for the next launch
-    };
-    // resolve the pending completion (if any) and register `new_rt` (-1: none) as the next one
-    auto rotate_pending = [&](int new_rt) {
-      named_bar_sync(1, NW * 32);  // this item's partial stores (all consumer warps) precede ...
-      if (ctid == 0) {
-        sm->combine_rt = (pend_rt >= 0 && pend_old == a.n_jobs - 1) ? pend_rt : -1;
-        if (new_rt >= 0) pend_old = atom_add_acq_rel_gpu(&tile_cnt[new_rt], 1);  // ... this release
-        pend_rt = new_rt;
-      }
-      named_bar_sync(1, NW * 32);
-      const int crt = sm->combine_rt;
-      if (crt >= 0) combine(crt);
-    };
     while (true) {
       mbar_wait(&sm->full[stage], phase);
       const StageHdr h = sm->hdr[stage];
@@ -605,29 +633,54 @@ __global__ void __launch_bounds__(NTHREADS, 2)
           }
         }
       }
+      int tk0 = 0, tk1 = 0;  // this lane's token ids (sparse/dense-delta epilogue), read before release
+      if ((h.flags & 2) && !is_base) {
+        const int t2 = 2 * (lane & 3);
+        if (t2 < h.tok_count) tk0 = sm->tok_ids[stage][t2];
+        if (t2 + 1 < h.tok_count) tk1 = sm->tok_ids[stage][t2 + 1];
+      }
+      if ((h.flags & 2) && h.kind == DZ_KIND_DENSE && nrv > 0)  // rare path: needs the stage's token list
+        merge_fragments(acc, nt, mctx, rg0, h.tok_count, sm->tok_ids[stage], lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm->empty[stage]);  // the stage is free before the epilogue
+      if (lane == 0 && warp == 0) TRACE(4, h.item, stage);
+      if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
+
       if (h.flags & 2) {
-        // ---- item epilogue: partial -> workspace ----
+        // ---- item epilogue: this warp's contributions -> merged into Y ----
         if (is_base) {
           const int buf = nbase & 1;
           mbar_wait(&sm->tmem_full[buf], (nbase >> 1) & 1);
           tc_fence_after();
-          drain_base_accumulator(tmem_base + buf * BASE_N, warp, lane, Pb, a.out, h.rt * RT, h.tok_begin,
+          drain_base_accumulator(tmem_base + buf * (RT / UMMA_M) * BASE_N, warp, lane, mctx, h.rt * RT, h.tok_begin,
                                  h.tok_count);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm->tmem_empty[buf]);
           nbase++;
-        } else if (nrv > 0) {
-          write_partial(acc, nt, Pd, a.out, rg0, h.tok_count, sm->tok_ids[stage], lane);
+        } else if (nrv > 0 && h.kind != DZ_KIND_DENSE) {
+          const int g = lane >> 2, t2 = 2 * (lane & 3);
+          int tk[4 * MR], rw[4 * MR];
+          float x[4 * MR];
+          bool ok[4 * MR];
+#pragma unroll
+          for (int r = 0; r < MR; r++) {
+            const int row = (rg0 + r) * kBlkRows + g;
+#pragma unroll
+            for (int v = 0; v < 4; v++) {  // fragment: v&1 -> token t2 / t2+1, v&2 -> row +8
+              const int i = 4 * r + v;
+              tk[i] = (v & 1) ? tk1 : tk0;
+              rw[i] = row + ((v & 2) ? 8 : 0);
+              x[i] = acc[r][0][v];
+              ok[i] = r < nrv && t2 + (v & 1) < h.tok_count && rw[i] < a.out;
+            }
+          }
+          merge_batch<4 * MR>(mctx, tk, rw, x, ok);
         }
-        rotate_pending(h.rt);
+        if (lane == 0 && warp == 0) TRACE(5, h.item, 0);
+        if (lane == 0 && warp == 0) ITEM_TRACE(1, h.item, globaltimer());
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm->empty[stage]);
-      if (lane == 0 && warp == 0) TRACE(4, h.item, stage);
-      if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
     }
-    rotate_pending(-1);  // resolve the last pending completion
   }
   tc_fence_before();
   __syncthreads();
@@ -720,14 +773,38 @@ extern "C" int dz_base_init(dz_native_delta* e, const uint16_t* W, int64_t ldw, 
   e->rows = rows;
   e->cols = cols;
   return encode_2d(reinterpret_cast<CUtensorMap*>(e->tmap), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, W,
-                   static_cast<uint64_t>(cols), static_cast<uint64_t>(rows), static_cast<uint64_t>(ldw) * 2, KC_DN, RT,
-                   CU_TENSOR_MAP_SWIZZLE_128B);
+                   static_cast<uint64_t>(cols), static_cast<uint64_t>(rows), static_cast<uint64_t>(ldw) * 2, KC_DN,
+                   RT, CU_TENSOR_MAP_SWIZZLE_128B);  // one box = 64 columns x 256 rows (two UMMA M tiles)
 }
 
 extern "C" size_t dz_sbmm_workspace_bytes(int32_t T, int32_t out) {
   if (T < 0 || out < 1) return 0;
-  if (ceil_div(out, RT) > kMaxTiles) return 0;
-  return (64 + static_cast<size_t>(kMaxTiles)) * sizeof(int) + 2 * static_cast<size_t>(T) * out * sizeof(float);
+  return 256 + static_cast<size_t>(T) * out * sizeof(unsigned long long);
+}
+
+static int g_ctas_per_sm = 0;
+
+extern "C" int dz_sbmm_diag(int* v) {  // numRegs, static smem, dynamic smem, max threads, localBytes
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, k_sbmm) != cudaSuccess) return -1;
+  v[0] = fa.numRegs; v[1] = static_cast<int>(fa.sharedSizeBytes); v[2] = SMEM_BYTES;
+  v[3] = fa.maxThreadsPerBlock; v[4] = static_cast<int>(fa.localSizeBytes);
+  size_t avail = 0;
+  cudaFuncSetAttribute(k_sbmm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaOccupancyAvailableDynamicSMemPerBlock(&avail, k_sbmm, 2, NTHREADS);
+  v[5] = static_cast<int>(avail);
+  cudaFuncSetAttribute(k_sbmm, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_sbmm, NTHREADS, SMEM_BYTES);
+  v[6] = n;
+  return 0;
+}
+
+extern "C" int dz_sbmm_ctas_per_sm(void) {
+  int n = 0;
+  if (cudaFuncSetAttribute(k_sbmm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess) return -1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_sbmm, NTHREADS, SMEM_BYTES) != cudaSuccess) return -1;
+  return n;
 }
 
 extern "C" int dz_sbmm(const dz_sbmm_args* a, void* stream) {
@@ -737,7 +814,6 @@ extern "C" int dz_sbmm(const dz_sbmm_args* a, void* stream) {
   const int in_pad = ceil_div(a->in, kBlkCols) * kBlkCols;
   if (a->ldx < in_pad || (a->ldx % 8) != 0 || (reinterpret_cast<uintptr_t>(a->X) & 15) != 0) return DZ_E_SHAPE;
   if (a->ldy < a->out) return DZ_E_SHAPE;
-  if (ceil_div(a->out, RT) > kMaxTiles) return DZ_E_SHAPE;
   if (a->y_dtype != DZ_F32 && a->y_dtype != DZ_BF16) return DZ_E_VALUE;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -768,6 +844,11 @@ extern "C" int dz_sbmm(const dz_sbmm_args* a, void* stream) {
 }
 
 #ifdef DZ_TRACE
+extern "C" int dz_item_trace_read(unsigned long long* host, int n_items) {
+  if (n_items > 65536) n_items = 65536;
+  cudaMemcpyFromSymbol(host, dz_item_trace, sizeof(unsigned long long) * 3 * n_items);
+  return n_items;
+}
 // host: copy out {warp, t, ev, a0, a1} tuples of the traced CTA, then reset
 extern "C" int dz_trace_read(unsigned long long* host, int max_events) {
   static unsigned long long buf[8][1024][2];

@@ -238,3 +238,22 @@ def sbmm_forward(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: De
     a.debug = debug
     L.check(L.lib().dz_sbmm(C.byref(a), stream_ptr()), "sbmm")
     return Y
+
+
+def concat_rows(parts: list[NativeDelta]) -> NativeDelta:
+    """Row-concatenate resident deltas of linears that share an input (QKV, gate/up fusion).
+
+    Exact and copy-only: native blocks are row-group-major ([16-row group][K block]), so the
+    concatenation of [ΔW_q; ΔW_k; ΔW_v] is the concatenation of their block buffers, provided every
+    part but the last has rows % 16 == 0 and all parts share cols and kind."""
+    if not parts:
+        raise ShapeError("nothing to concatenate")
+    kind, cols = parts[0].kind, parts[0].cols
+    for p in parts:
+        if p.kind != kind or p.cols != cols or p.qmax != parts[0].qmax:
+            raise ShapeError("concat_rows needs deltas of one kind and one input width")
+    for p in parts[:-1]:
+        if p.rows % BLK_ROWS:
+            raise ShapeError("concat_rows needs rows % 16 == 0 for all but the last part")
+    blocks = torch.cat([p.blocks for p in parts])
+    return NativeDelta(kind, parts[0].qmax, sum(p.rows for p in parts), cols, blocks, parts[0].bits)
