@@ -27,12 +27,17 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False, trace: bool = False) -> str:
-    """Build `_dz_b200.so` (or the DZ_TRACE-instrumented `_dz_b200_trace.so` for tools/trace.py)."""
+def build(verbose: bool = False, force: bool = False, trace: bool = False, variant: str = "",
+          defines: list[str] | None = None) -> str:
+    """Build `_dz_b200.so`, the DZ_TRACE-instrumented `_dz_b200_trace.so` (tools/trace.py), or an
+    experiment variant `_dz_b200_<variant>.so` with extra -D defines (loaded via DZ_B200_LIB)."""
     global LIB, BUILD
+    defines = list(defines or [])
     if trace:
-        LIB = os.path.join(PKG, "_dz_b200_trace.so")
-        BUILD = os.path.join(ROOT, "build", "obj_trace")
+        variant, defines = "trace", defines + ["-DDZ_TRACE"]
+    if variant:
+        LIB = os.path.join(PKG, f"_dz_b200_{variant}.so")
+        BUILD = os.path.join(ROOT, "build", f"obj_{variant}")
     os.makedirs(BUILD, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "dz_b200.h"))
@@ -42,7 +47,7 @@ def build(verbose: bool = False, force: bool = False, trace: bool = False) -> st
         obj = os.path.join(BUILD, src + ".o")
         objs.append(obj)
         if force or _stale(obj, [path] + headers):
-            cmd = [NVCC, *ARCH, *NVFLAGS, *(["-DDZ_TRACE"] if trace else []), "-c", path, "-o", obj]
+            cmd = [NVCC, *ARCH, *NVFLAGS, *defines, "-c", path, "-o", obj]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:
                 sys.stderr.write(r.stdout + r.stderr)
@@ -59,4 +64,6 @@ def build(verbose: bool = False, force: bool = False, trace: bool = False) -> st
 
 
 if __name__ == "__main__":
-    print(build(verbose=True, force="--force" in sys.argv, trace="--trace" in sys.argv))
+    var = sys.argv[sys.argv.index("--variant") + 1] if "--variant" in sys.argv else ""
+    print(build(verbose=True, force="--force" in sys.argv, trace="--trace" in sys.argv, variant=var,
+                defines=[a for a in sys.argv[1:] if a.startswith("-D")]))

@@ -180,6 +180,14 @@ __device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t mask, uint3
   return r;
 }
 
+// x >> K computed on the FMA pipe (IMAD.HI): hi32(x * 2^(32-K)).
+template <int K>
+__device__ __forceinline__ uint32_t mulhi_shr(uint32_t x) {
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "n"(1u << (32 - K)));
+  return r;
+}
+
 // bf16x2 subtract (exact here: small integers).
 __device__ __forceinline__ uint32_t bf16x2_sub(uint32_t a, uint32_t b) {
   __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&a);

@@ -39,8 +39,8 @@
 #ifdef DZ_TRACE
 // Per-warp private event slots of the traced CTA (the one that took item 0): plain stores, no
 // atomics, so tracing does not perturb the pipeline. Slot [warp][i] = {globaltimer, ev|a0|a1}.
-__device__ unsigned long long dz_trace_buf[8][1024][2];
-__device__ int dz_trace_cnt[8];
+__device__ unsigned long long dz_trace_buf[12][1024][2];
+__device__ int dz_trace_cnt[12];
 __device__ volatile int dz_trace_cta = -1;
 __device__ unsigned long long dz_item_trace[65536][3];  // per item: start, end, (cta << 32 | kind)
 #define ITEM_TRACE(slot, item, val) do { if ((item) < 65536) dz_item_trace[(item)][(slot)] = (val); } while (0)
@@ -60,7 +60,8 @@ constexpr int NW = 8;                     // consumer warps per CTA (one CTA per
 constexpr int MR = 2;                     // 16-row groups per consumer warp
 constexpr int WARP_PROD = NW;             // TMA producer warp
 constexpr int WARP_MMA = NW + 1;          // tcgen05 issuer / TMEM owner warp
-constexpr int NTHREADS = (NW + 2) * 32;
+constexpr int WARP_XPROD = NW + 2;        // per-token X copies of delta stages
+constexpr int NTHREADS = (NW + 3) * 32;
 constexpr int RG = NW * MR;               // row groups per item
 constexpr int RT = RG * kBlkRows;         // rows per item (256) == 2 x UMMA M
 constexpr int UMMA_M = 128;
@@ -79,7 +80,9 @@ constexpr int X_DN = 64 * XS_DN;                          // 9216 (>= 64 x 128 B
 constexpr int STAGE_BYTES = ((A_SP + X_SP > A_DN + X_DN ? A_SP + X_SP : A_DN + X_DN) + 1023) / 1024 * 1024;
 constexpr int NSTAGE = 3;
 constexpr int JOB_DN_TOK = BASE_N;        // largest token count of a job
-constexpr int TMEM_COLS = 2 * 2 * BASE_N; // (double buffer) x (two M=128 halves) fp32 accumulators
+constexpr int BASE_RT = UMMA_M;           // rows per base item: one UMMA M tile (half a delta row tile)
+constexpr int BASE_CH = 2;                // 64-column K-chunks per base stage (32 KB of W in flight per stage)
+constexpr int TMEM_COLS = 2 * BASE_N;     // double-buffered fp32 accumulator, 128 lanes x 64 tokens
 constexpr uint32_t IDESC_BASE = umma_idesc_bf16(UMMA_M, BASE_N);
 
 struct StageHdr {
@@ -96,6 +99,7 @@ struct StageHdr {
 struct Smem {
   uint64_t full[NSTAGE];
   uint64_t empty[NSTAGE];
+  uint64_t xreq[NSTAGE];   // producer -> X producer: header + token ids of the stage are written
   uint64_t tmem_full[2];
   uint64_t tmem_empty[2];
   StageHdr hdr[NSTAGE];
@@ -108,12 +112,15 @@ __device__ __forceinline__ bool kind_dense(int kind) { return kind == 0 || kind 
 
 // Item order: all base items first (row tile order; the big ones start early), then the delta
 // items row-tile-major, so row tiles complete (and are combined) progressively through the launch
-// instead of all at the end. dz_plan puts the n_base base jobs first in the job list.
-__device__ __forceinline__ void item_coords(int item, int nrt, int n_jobs, int n_base, int& rt, int& j) {
-  const int nb_items = nrt * n_base;
+// instead of all at the end. dz_plan puts the n_base base jobs first in the job list. Base items
+// cover BASE_RT = 128 rows (nbt tiles), delta items RT = 256 rows (nrt tiles): a base item streams
+// 2 bytes per weight against a 4-bit delta's ~0.8, so halving it keeps the long base items off the
+// launch's critical path. Each output element still gets exactly one base and one delta partial.
+__device__ __forceinline__ void item_coords(int item, int nrt, int nbt, int n_jobs, int n_base, int& rt, int& j) {
+  const int nb_items = nbt * n_base;
   if (item < nb_items) {
-    j = item / nrt;
-    rt = item - j * nrt;
+    j = item / nbt;
+    rt = item - j * nbt;
   } else {
     const int k = item - nb_items, nd = n_jobs - n_base;
     rt = k / nd;
@@ -130,19 +137,36 @@ __device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
 // ------------------------------------------------------------------------------------------
 // Consumer math (CUDA-core decode + legacy mma.sp / mma)
 // ------------------------------------------------------------------------------------------
-template <int FB>
+// Codes -> bf16 A fragments. RAW: leave the value as 128 + u (the offset 128 + qmax is removed
+// later with a ones-MMA, see sparse_pair); else subtract it here (one HADD2 per register).
+template <int FB, bool RAW>
 __device__ __forceinline__ void conv_codes(uint32_t (&a)[4], const uint32_t (&cw)[4], int i, uint32_t off2) {
   if (FB == 4) {
     const uint32_t w = cw[i];
 #pragma unroll
-    for (int k = 0; k < 4; k++) a[k] = bf16x2_sub(lop3_and_or(w >> (4 * k), 0x000F000Fu, 0x43004300u), off2);
+    for (int k = 0; k < 4; k++) {
+      a[k] = lop3_and_or(w >> (4 * k), 0x000F000Fu, 0x43004300u);
+      if (!RAW) a[k] = bf16x2_sub(a[k], off2);
+    }
   } else {
     const uint32_t w = cw[i >> 1];
     const int o = 4 * (i & 1);
 #pragma unroll
-    for (int k = 0; k < 4; k++) a[k] = bf16x2_sub(lop3_and_or(w >> (2 * (o + k)), 0x00030003u, 0x43004300u), off2);
+    for (int k = 0; k < 4; k++) {
+      a[k] = lop3_and_or(w >> (2 * (o + k)), 0x00030003u, 0x43004300u);
+      if (!RAW) a[k] = bf16x2_sub(a[k], off2);
+    }
   }
 }
+
+// The offset trick (kOnesMma): the tensor core computes S1 = sum (128+u) x and, with an all-ones A
+// and the same metadata, S0 = sum_kept x; then sum code*x = S1 - (128+qmax) S0 in fp32. It moves
+// 16 HADD2 per 16x128 block-row from the FMA pipe to the tensor pipe. Off by default: it measured
+// ~8% slower on B200 (kept for the record; build a variant with -DDZ_ONES_MMA=1 to retry).
+#ifndef DZ_ONES_MMA
+#define DZ_ONES_MMA 0
+#endif
+constexpr bool kOnesMma = DZ_ONES_MMA != 0;
 
 // Two consecutive blocks (b0, b0+1 < nb) of a sparse chunk for this warp's nrv <= MR row groups
 // and NT token tiles: loads, decodes and issues 4 independent mma.sp chains.
@@ -152,6 +176,7 @@ constexpr int PAIR = 2;
 template <int FB, int NT, bool FULL>
 __device__ __forceinline__ void sparse_pair(float (&acc)[MR][NT_DN][4], uint32_t sA, uint32_t xl, int b0, int nb,
                                             int nrv, uint32_t off2, int lane) {
+  const float offf = __uint_as_float((off2 & 0xFFFFu) << 16);  // 128 + qmax
   constexpr int CODE = sparse_code_bytes(FB);
   constexpr int BLK = sparse_block_bytes(FB);
   const int g = lane >> 2;
@@ -183,12 +208,17 @@ __device__ __forceinline__ void sparse_pair(float (&acc)[MR][NT_DN][4], uint32_t
     }
   }
   float tmp[PAIR][MR][NT][4];
+  float sx[PAIR][MR][NT][4];  // S0 = sum of the kept x (kOnesMma)
 #pragma unroll
   for (int p = 0; p < PAIR; p++)
 #pragma unroll
     for (int r = 0; r < MR; r++)
 #pragma unroll
-      for (int n = 0; n < NT; n++) tmp[p][r][n][0] = tmp[p][r][n][1] = tmp[p][r][n][2] = tmp[p][r][n][3] = 0.f;
+      for (int n = 0; n < NT; n++) {
+        tmp[p][r][n][0] = tmp[p][r][n][1] = tmp[p][r][n][2] = tmp[p][r][n][3] = 0.f;
+        sx[p][r][n][0] = sx[p][r][n][1] = sx[p][r][n][2] = sx[p][r][n][3] = 0.f;
+      }
+  const uint32_t ones[4] = {0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u};
 #pragma unroll
   for (int i = 0; i < 4; i++) {
 #pragma unroll
@@ -201,14 +231,17 @@ __device__ __forceinline__ void sparse_pair(float (&acc)[MR][NT_DN][4], uint32_t
       for (int r = 0; r < MR; r++) {
         if (!FULL && r >= nrv) continue;  // padding row group (zero-filled by TMA, never stored)
         uint32_t a[4];
-        conv_codes<FB>(a, cw[p][r], i, off2);
+        conv_codes<FB, kOnesMma>(a, cw[p][r], i, off2);
         const uint32_t e = (i < 2) ? meta[p][r].x : meta[p][r].y;
 #pragma unroll
         for (int n = 0; n < NT; n++) {
-          if (i & 1)
+          if (i & 1) {
             mma_sp_bf16_16832<1>(tmp[p][r][n], a, bf[n], e);
-          else
+            if (kOnesMma) mma_sp_bf16_16832<1>(sx[p][r][n], ones, bf[n], e);
+          } else {
             mma_sp_bf16_16832<0>(tmp[p][r][n], a, bf[n], e);
+            if (kOnesMma) mma_sp_bf16_16832<0>(sx[p][r][n], ones, bf[n], e);
+          }
         }
       }
     }
@@ -219,10 +252,11 @@ __device__ __forceinline__ void sparse_pair(float (&acc)[MR][NT_DN][4], uint32_t
     for (int r = 0; r < MR; r++)
 #pragma unroll
       for (int n = 0; n < NT; n++) {
-        acc[r][n][0] = fmaf(sc[p][r].x, tmp[p][r][n][0], acc[r][n][0]);
-        acc[r][n][1] = fmaf(sc[p][r].x, tmp[p][r][n][1], acc[r][n][1]);
-        acc[r][n][2] = fmaf(sc[p][r].y, tmp[p][r][n][2], acc[r][n][2]);
-        acc[r][n][3] = fmaf(sc[p][r].y, tmp[p][r][n][3], acc[r][n][3]);
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+          const float t = kOnesMma ? fmaf(-offf, sx[p][r][n][v], tmp[p][r][n][v]) : tmp[p][r][n][v];
+          acc[r][n][v] = fmaf((v & 2) ? sc[p][r].y : sc[p][r].x, t, acc[r][n][v]);
+        }
       }
 }
 
@@ -336,11 +370,13 @@ __device__ __forceinline__ void merge_contribution(const MergeCtx& m, int tok, i
 // (rows 128*(w/4)..) of the tile, TMEM lanes 32*(w%4)..+31 (the lanes warp w may access).
 __device__ __forceinline__ void drain_base_accumulator(uint32_t tmem_acc, int warp, int lane, const MergeCtx& m,
                                                        int row0, int tok_begin, int tcount) {
-  const int q = warp & 3, hm = warp >> 2;
-  const int row = row0 + hm * UMMA_M + 32 * q + lane;
-  const uint32_t taddr = tmem_acc + hm * BASE_N + (static_cast<uint32_t>(32 * q) << 16);
+  // TMEM lane quarter q = warp % 4 (the hardware's warp -> lane restriction); the two warps of a
+  // quarter split the 64 token columns.
+  const int q = warp & 3, half = warp >> 2;
+  const int row = row0 + 32 * q + lane;
+  const uint32_t taddr = tmem_acc + (static_cast<uint32_t>(32 * q) << 16);
 #pragma unroll 1
-  for (int c = 0; c < BASE_N / 16; c++) {
+  for (int c = half * (BASE_N / 32); c < (half + 1) * (BASE_N / 32); c++) {
     if (c * 16 >= tcount) break;
     uint32_t v[16];
     tmem_ld16(taddr + c * 16, v);
@@ -394,9 +430,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int n16 = ceil_div(a.out, kBlkRows);
   const int nrt = ceil_div(a.out, RT);
   const int nkb = ceil_div(a.in, kBlkCols);
-  const int nch_base = ceil_div(a.in, KC_DN);
-  const int n_items = nrt * a.n_jobs;
+  const int nch_base = ceil_div(a.in, BASE_CH * KC_DN);
+  const int nbt = ceil_div(a.out, BASE_RT);
   const int n_base = a.base != nullptr ? ceil_div(a.T, BASE_N) : 0;  // dz_plan: base jobs first
+  const int n_items = nbt * n_base + nrt * (a.n_jobs - n_base);
 
   int* sched = reinterpret_cast<int*>(a.workspace);  // [0] item counter, [1] finished CTAs
   MergeCtx mctx;
@@ -412,6 +449,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int s = 0; s < NSTAGE; s++) {
       mbar_init(&sm->full[s], 1);
       mbar_init(&sm->empty[s], NW + 1);  // consumer warps + the MMA warp (commit or arrive)
+      mbar_init(&sm->xreq[s], 1);
     }
     for (int b = 0; b < 2; b++) {
       mbar_init(&sm->tmem_full[b], 1);
@@ -441,7 +479,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (lane == 0) id_raw = atomicAdd(&sched[0], 1);
     int item = __shfl_sync(0xffffffffu, id_raw, 0);
     int rt = 0, jj = 0;
-    if (item < n_items) item_coords(item, nrt, a.n_jobs, n_base, rt, jj);
+    if (item < n_items) item_coords(item, nrt, nbt, a.n_jobs, n_base, rt, jj);
     dz_job job = item < n_items ? a.jobs[jj] : dz_job{0, 0, 0, 0};
     int tok = 0, tok2 = 0;
     if (item < n_items) {
@@ -456,7 +494,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const void* amap = ent->tmap;  // address only: the descriptor stays in global memory
       const int bb = dense ? kDenseBlockBytes : sparse_block_bytes(kind_fbits(job.kind));
       const int nch = is_base ? nch_base : dense ? 2 * nkb : ceil_div(nkb, NB_SP);
-      const uint32_t abytes = dense ? static_cast<uint32_t>(A_DN) : static_cast<uint32_t>(RG * NB_SP * bb);
+      const uint32_t abytes = is_base ? static_cast<uint32_t>(BASE_RT * KC_DN * 2)
+                              : dense ? static_cast<uint32_t>(A_DN) : static_cast<uint32_t>(RG * NB_SP * bb);
       // Next item: its id is fetched after chunk 0 goes out (one item of lookahead per CTA keeps
       // the dynamic schedule balanced), its descriptor and token ids after chunks 1 and 2, so the
       // dependent global loads overlap this item's stream instead of stalling the ring.
@@ -471,12 +510,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (lane == 0) TRACE(2, item, ch);
         uint8_t* sbuf = stages + static_cast<size_t>(stage) * STAGE_BYTES;
         int nb, col0, xbytes, ax, ay;
-        if (dense) {
+        if (is_base) {
+          col0 = ch * BASE_CH * KC_DN;
+          nb = (a.in - col0) < KC_DN ? 1 : BASE_CH;  // K-chunks in this stage (no fully-OOB boxes)
+          xbytes = 0;
+          ax = col0;
+          ay = rt * BASE_RT;
+        } else if (dense) {
           nb = 1;
           col0 = ch * KC_DN;
           xbytes = KC_DN * 2;
-          ax = is_base ? col0 : ch * (DN_HALF / 8);
-          ay = rt * (is_base ? RT : RG);
+          ax = ch * (DN_HALF / 8);
+          ay = rt * RG;
         } else {
           const int kb0 = ch * NB_SP;
           nb = (nkb - kb0) < NB_SP ? (nkb - kb0) : NB_SP;
@@ -486,7 +531,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           ay = rt * RG;
         }
         const bool last = ch == nch - 1;
-        if (last) {  // token ids ride with the last chunk (the consumers' epilogue needs them)
+        if (!is_base || last) {  // token ids: the X producer's gather list / the epilogue's scatter list
           if (lane < job.tok_count) sm->tok_ids[stage][lane] = tok;
           if (lane + 32 < job.tok_count) sm->tok_ids[stage][lane + 32] = tok2;
           __syncwarp();
@@ -495,30 +540,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           StageHdr h;
           h.item = item; h.rt = rt; h.kind = job.kind;
           h.tok_begin = job.tok_begin; h.tok_count = job.tok_count; h.nb = nb;
-          h.flags = (ch == 0 ? 1 : 0) | (last ? 2 : 0);
+          h.flags = (ch == 0 ? 1 : 0) | (last ? 2 : 0) | (ch << 8);  // chunk index for the X producer
           h.pad = 0;
           sm->hdr[stage] = h;
-          const uint32_t xb = is_base ? static_cast<uint32_t>(KC_DN * BASE_N * 2)
+          const uint32_t xb = is_base ? static_cast<uint32_t>(nb * KC_DN * BASE_N * 2)
                                       : static_cast<uint32_t>(job.tok_count * xbytes);
           TRACE(6, item, ch);
-          mbar_arrive_expect_tx(&sm->full[stage], abytes + xb);  // release: orders the smem writes above
+          mbar_arrive_expect_tx(&sm->full[stage], (is_base ? nb : 1) * abytes + xb);  // release: orders the smem writes above
           TRACE(7, item, ch);
-          if (dense)
+          if (is_base) {
+            for (int c = 0; c < nb; c++) {
+              tma_load_2d(sbuf + c * (BASE_RT * KC_DN * 2), amap, ax + c * KC_DN, ay, &sm->full[stage], pol_stream);
+              tma_load_2d(sbuf + A_DN + c * (KC_DN * BASE_N * 2), &xmap, col0 + c * KC_DN, job.tok_begin,
+                          &sm->full[stage], pol_keep);
+            }
+          } else if (dense) {
             tma_load_2d(sbuf, amap, ax, ay, &sm->full[stage], pol_stream);
-          else
+          } else {
             tma_load_3d(sbuf, amap, 0, ax, ay, &sm->full[stage], pol_stream);
-          if (is_base) tma_load_2d(sbuf + A_DN, &xmap, col0, job.tok_begin, &sm->full[stage], pol_keep);
+          }
           TRACE(8, item, ch);
-        }
-        if (!is_base) {
-          const int aoff = dense ? A_DN : A_SP;
-          const int xs = dense ? XS_DN : XS_SP;
-          if (lane < job.tok_count)
-            tma_load_1d(sbuf + aoff + lane * xs, a.X + static_cast<int64_t>(tok) * a.ldx + col0,
-                        static_cast<uint32_t>(xbytes), &sm->full[stage], pol_keep);
-          if (lane + 32 < job.tok_count)
-            tma_load_1d(sbuf + aoff + (lane + 32) * xs, a.X + static_cast<int64_t>(tok2) * a.ldx + col0,
-                        static_cast<uint32_t>(xbytes), &sm->full[stage], pol_keep);
+          mbar_arrive(&sm->xreq[stage]);  // release: header + token ids are visible to the X producer
         }
         if (lane == 0) TRACE(9, item, ch);
         if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
@@ -528,8 +570,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           item_nxt = __shfl_sync(0xffffffffu, id_nxt_raw, 0);
           if (item_nxt < n_items) {
             int j_n = 0;
-            item_coords(item_nxt, nrt, a.n_jobs, n_base, rt_n, j_n);
+            item_coords(item_nxt, nrt, nbt, a.n_jobs, n_base, rt_n, j_n);
             job_n = a.jobs[j_n];
+            if (lane == 0) prefetch_tmap((job_n.kind == 0 ? a.base : a.table + job_n.slot)->tmap);
           }
         }
         if (ch == (nch > 2 ? 2 : nch - 1) && item_nxt < n_items) {
@@ -548,12 +591,37 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     mbar_wait(&sm->empty[stage], phase ^ 1);
     if (lane == 0) {
       sm->hdr[stage].item = -1;
+      mbar_arrive(&sm->xreq[stage]);
       mbar_arrive(&sm->full[stage]);
       const int done = atomicAdd(&sched[1], 1);
       if (done == static_cast<int>(gridDim.x) - 1) {  // last CTA out resets the scheduler
         sched[0] = 0;
         sched[1] = 0;
       }
+    }
+  } else if (warp == WARP_XPROD) {
+    // ===================== X producer (delta stages) =====================
+    // One 1-D bulk copy per routed token row of the chunk, completing on the stage's full barrier
+    // (whose expect_tx the producer already armed with these bytes).
+    const uint64_t pol_keep = policy_evict_last();
+    int stage = 0;
+    uint32_t phase = 0;
+    while (true) {
+      mbar_wait(&sm->xreq[stage], phase);
+      const StageHdr h = sm->hdr[stage];
+      if (h.item < 0) break;
+      if (h.kind != 0) {
+        const bool dense = h.kind == DZ_KIND_DENSE;
+        const int col0 = dense ? (h.flags >> 8) * KC_DN : (h.flags >> 8) * NB_SP * kBlkCols;
+        const int xbytes = dense ? KC_DN * 2 : h.nb * kBlkCols * 2;
+        const int aoff = dense ? A_DN : A_SP;
+        const int xs = dense ? XS_DN : XS_SP;
+        uint8_t* sbuf = stages + static_cast<size_t>(stage) * STAGE_BYTES;
+        for (int tk = lane; tk < h.tok_count; tk += 32)
+          tma_load_1d(sbuf + aoff + tk * xs, a.X + static_cast<int64_t>(sm->tok_ids[stage][tk]) * a.ldx + col0,
+                      static_cast<uint32_t>(xbytes), &sm->full[stage], pol_keep);
+      }
+      if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
     }
   } else if (warp == WARP_MMA) {
     // ===================== tcgen05 issuer =====================
@@ -571,14 +639,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc_fence_after();
         if (lane == 0) {
           const uint32_t sbuf = smem_u32(stages + static_cast<size_t>(stage) * STAGE_BYTES);
-          const uint64_t bdesc = umma_desc_sw128(sbuf + A_DN);
-#pragma unroll
-          for (int hm = 0; hm < RT / UMMA_M; hm++) {  // rows 128*hm.. of the tile: own accumulator
-            const uint64_t adesc = umma_desc_sw128(sbuf + hm * (UMMA_M * KC_DN * 2));
-            const uint32_t tmem_d = tmem_base + (buf * (RT / UMMA_M) + hm) * BASE_N;
+          const uint32_t tmem_d = tmem_base + buf * BASE_N;
+          for (int c = 0; c < h.nb; c++) {
+            const uint64_t adesc = umma_desc_sw128(sbuf + c * (BASE_RT * KC_DN * 2));
+            const uint64_t bdesc = umma_desc_sw128(sbuf + A_DN + c * (KC_DN * BASE_N * 2));
 #pragma unroll
             for (int k = 0; k < KC_DN / 16; k++)  // K=16 per MMA: +32 B inside the 128-B swizzle atom
-              umma_bf16(tmem_d, adesc + 2 * k, bdesc + 2 * k, IDESC_BASE, (h.flags & 1) && k == 0 ? 0u : 1u);
+              umma_bf16(tmem_d, adesc + 2 * k, bdesc + 2 * k, IDESC_BASE, (h.flags & 1) && c == 0 && k == 0 ? 0u : 1u);
           }
           umma_commit(&sm->empty[stage]);
           if (h.flags & 2) umma_commit(&sm->tmem_full[buf]);
@@ -652,7 +719,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const int buf = nbase & 1;
           mbar_wait(&sm->tmem_full[buf], (nbase >> 1) & 1);
           tc_fence_after();
-          drain_base_accumulator(tmem_base + buf * (RT / UMMA_M) * BASE_N, warp, lane, mctx, h.rt * RT, h.tok_begin,
+          drain_base_accumulator(tmem_base + buf * BASE_N, warp, lane, mctx, h.rt * BASE_RT, h.tok_begin,
                                  h.tok_count);
           tc_fence_before();
           __syncwarp();
@@ -727,6 +794,9 @@ static int encode_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, u
 
 using namespace dz;
 
+static_assert(A_DN + BASE_CH * KC_DN * BASE_N * 2 <= STAGE_BYTES && BASE_CH * BASE_RT * KC_DN * 2 <= A_DN,
+              "base stage layout");
+static_assert(NW == 8, "drain_base_accumulator: two consumer warps per TMEM lane quarter");
 static_assert(sizeof(dz_native_delta) == 192, "dz_native_delta must be 192 bytes");
 static_assert(offsetof(dz_native_delta, tmap) == 64, "tensor map must be 64-byte aligned in the entry");
 static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
@@ -774,7 +844,7 @@ extern "C" int dz_base_init(dz_native_delta* e, const uint16_t* W, int64_t ldw, 
   e->cols = cols;
   return encode_2d(reinterpret_cast<CUtensorMap*>(e->tmap), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, W,
                    static_cast<uint64_t>(cols), static_cast<uint64_t>(rows), static_cast<uint64_t>(ldw) * 2, KC_DN,
-                   RT, CU_TENSOR_MAP_SWIZZLE_128B);  // one box = 64 columns x 256 rows (two UMMA M tiles)
+                   BASE_RT, CU_TENSOR_MAP_SWIZZLE_128B);  // one box = 64 columns x 128 rows (one UMMA M tile)
 }
 
 extern "C" size_t dz_sbmm_workspace_bytes(int32_t T, int32_t out) {
@@ -851,19 +921,19 @@ extern "C" int dz_item_trace_read(unsigned long long* host, int n_items) {
 }
 // host: copy out {warp, t, ev, a0, a1} tuples of the traced CTA, then reset
 extern "C" int dz_trace_read(unsigned long long* host, int max_events) {
-  static unsigned long long buf[8][1024][2];
-  int cnt[8];
+  static unsigned long long buf[12][1024][2];
+  int cnt[12];
   cudaMemcpyFromSymbol(cnt, dz_trace_cnt, sizeof(cnt));
   cudaMemcpyFromSymbol(buf, dz_trace_buf, sizeof(buf));
   int n = 0;
-  for (int w = 0; w < 8; w++)
+  for (int w = 0; w < 12; w++)
     for (int i = 0; i < cnt[w] && i < 1024 && n < max_events; i++, n++) {
       host[4 * n + 0] = buf[w][i][0];
       host[4 * n + 1] = (buf[w][i][1] >> 56) | (static_cast<unsigned long long>(w) << 8);
       host[4 * n + 2] = (buf[w][i][1] >> 16) & 0xFFFFFFFFull;
       host[4 * n + 3] = buf[w][i][1] & 0xFFFFull;
     }
-  int zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int zero[12] = {0};
   cudaMemcpyToSymbol(dz_trace_cnt, zero, sizeof(zero));
   int neg = -1;
   cudaMemcpyToSymbol(dz_trace_cta, &neg, sizeof(int));
