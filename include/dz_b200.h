@@ -75,7 +75,7 @@ typedef struct dz_native_delta {
 typedef struct dz_job {
   int32_t slot;             /* delta-table index; -1 = base GEMM over all tokens     */
   int32_t tok_begin;        /* first position in `order` (delta) or token (base)     */
-  int32_t tok_count;        /* <= 64 (base), <= 32 (dense delta), <= 8 (sparse)      */
+  int32_t tok_count;        /* <= 64 (base), <= 32 (dense delta), <= 8 (sparse), <= 256 (prefill) */
   int32_t kind;             /* 0 = base, else DZ_KIND_* of the slot                  */
 } dz_job;
 
@@ -97,6 +97,15 @@ typedef struct dz_sbmm_args {
                                allocation; the kernel leaves it zero after every call */
   int32_t grid;             /* persistent CTAs; 0 = one per SM                       */
   int32_t debug;            /* 0; bit 0 = skip consumer math (pipeline bandwidth probe) */
+  /* Mixed prefill + decode batches (dz_plan_mixed). perm == NULL: pure decode plan, X is used
+   * as is. Otherwise X is first staged into xs with xs[i] = X[perm[i]]; jobs[0:n_pf_jobs] are
+   * prefill jobs over staged rows [0, t_pf) (K3: tcgen05 base + dequantised-delta MMAs in one
+   * TMEM accumulator), the remaining jobs cover staged rows [t_pf, T) (K2), and staged row i
+   * is written to Y row perm[i]. */
+  const int32_t* perm;      /* device [T] or NULL                                     */
+  void* xs;                 /* device bf16 [T][ldx] staging buffer (perm != NULL)      */
+  int32_t n_pf_jobs;
+  int32_t t_pf;
 } dz_sbmm_args;
 
 const char* dz_version(void);
@@ -156,6 +165,15 @@ int32_t dz_plan_max_jobs(int32_t T);
 int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t n_slots,
             int32_t with_base, int32_t* order_out, dz_job* jobs_out, int32_t max_jobs,
             int32_t* n_jobs_out);
+/* Mixed plan: delta groups of >= pf_min tokens (2:4 sparse kinds) become prefill jobs of
+ * <= 256 tokens for K3, staged first in perm (grouped by slot, stable); the remaining tokens
+ * keep their original order after them and are planned for K2 exactly as dz_plan does, with
+ * order_out indexing staged rows. *t_pf_out = staged prefill rows; when it is 0 the plan is
+ * the pure decode plan and perm is the identity (pass perm = NULL to dz_sbmm). */
+int dz_plan_mixed(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t n_slots,
+                  int32_t with_base, int32_t pf_min, int32_t* perm_out, int32_t* order_out,
+                  dz_job* jobs_out, int32_t max_jobs, int32_t* n_jobs_out, int32_t* n_pf_jobs_out,
+                  int32_t* t_pf_out);
 
 /* K2 — fused decode SBMM. Replaces inference.sbmm (inference.py:126-154):
  * Y[t] = W_base x_t + ΔW_{slot(t)} x_t for every token in ONE persistent launch:
@@ -166,6 +184,14 @@ int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t n_slo
  * Deterministic and batch-invariant: a token's result does not depend on the
  * other tokens in the call. */
 size_t dz_sbmm_workspace_bytes(int32_t T, int32_t out);
+/* K3 — prefill SBMM (dz_prefill.cu), launched by dz_sbmm for the prefill jobs of a mixed plan:
+ * per (128-row tile, <= 256-token group) one TMEM accumulator receives tcgen05 MMAs of the base
+ * W tile and of the group's delta tile, dequantised (code * scale -> bf16) from native blocks
+ * into shared memory by CUDA-core warps. Exposed for diagnostics / the kernel bench. */
+int dz_sbmm_prefill(const dz_sbmm_args* args, void* stream);
+/* Gather rows: Xs[i] = X[perm[i]] (bf16, row strides in elements, 16-byte aligned rows). */
+int dz_gather_rows(const uint16_t* X, int64_t ldx, const int32_t* perm, int32_t T, int32_t in,
+                   uint16_t* Xs, int64_t ldxs, void* stream);
 /* Resident CTAs per SM of the fused kernel (diagnostics; < 0 on error). */
 int dz_sbmm_ctas_per_sm(void);
 int dz_sbmm(const dz_sbmm_args* args, void* stream);

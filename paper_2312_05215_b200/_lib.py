@@ -54,6 +54,8 @@ class DzSbmmArgs(C.Structure):
         ("jobs", C.c_void_p), ("n_jobs", C.c_int32),
         ("workspace", C.c_void_p),
         ("grid", C.c_int32), ("debug", C.c_int32),
+        ("perm", C.c_void_p), ("xs", C.c_void_p),
+        ("n_pf_jobs", C.c_int32), ("t_pf", C.c_int32),
     ]
 
 
@@ -77,7 +79,13 @@ SIGNATURES = {
     "dz_plan_max_jobs": (C.c_int32, [C.c_int32]),
     "dz_plan": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                           C.c_int32, C.POINTER(C.c_int32)]),
+    "dz_plan_mixed": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                C.POINTER(C.c_int32)]),
     "dz_sbmm_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int32]),
+    "dz_sbmm_prefill": (C.c_int, [C.POINTER(DzSbmmArgs), C.c_void_p]),
+    "dz_gather_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int64,
+                                 C.c_void_p]),
     "dz_sbmm": (C.c_int, [C.POINTER(DzSbmmArgs), C.c_void_p]),
     "dz_sbmm_ctas_per_sm": (C.c_int, []),
 }

@@ -21,7 +21,7 @@ extern "C" const char* dz_strerror(int status) {
   }
 }
 
-extern "C" int32_t dz_plan_max_jobs(int32_t T) { return T < 0 ? 0 : 2 * T + 2; }
+extern "C" int32_t dz_plan_max_jobs(int32_t T) { return T < 0 ? 0 : 2 * T + 2; }  // >= base + delta + prefill jobs
 
 // Stable sort of token rows by slot (inference.py:106-123: `sorted` is stable), then cut into
 // jobs: base token chunks of 64, sparse delta chunks of 8, dense delta chunks of 32.
@@ -57,5 +57,81 @@ extern "C" int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, in
       if (!push(s, start[s] + off, (c - off) < chunk ? (c - off) : chunk, kind)) return DZ_E_VALUE;
   }
   *n_jobs_out = nj;
+  return DZ_OK;
+}
+
+// Mixed plan (prefill + decode). Groups of >= pf_min tokens with a 2:4 sparse kind are staged
+// first (grouped by slot in slot order, stable inside a group) and cut into prefill jobs of <= 256
+// tokens, balanced so that no job is much smaller than the others; every other token follows in
+// its original order and is planned exactly like dz_plan over the staged rows.
+extern "C" int dz_plan_mixed(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t n_slots,
+                             int32_t with_base, int32_t pf_min, int32_t* perm_out, int32_t* order_out,
+                             dz_job* jobs_out, int32_t max_jobs, int32_t* n_jobs_out, int32_t* n_pf_jobs_out,
+                             int32_t* t_pf_out) {
+  if (T < 0 || n_slots < 0 || !n_jobs_out || !n_pf_jobs_out || !t_pf_out) return DZ_E_VALUE;
+  *n_jobs_out = *n_pf_jobs_out = *t_pf_out = 0;
+  for (int32_t t = 0; t < T; t++)
+    if (slots[t] < 0 || slots[t] >= n_slots) return DZ_E_UNKNOWN;  // inference.py:135-137
+  for (int32_t s = 0; s < n_slots; s++)
+    if (kinds[s] != DZ_KIND_SPARSE4 && kinds[s] != DZ_KIND_SPARSE2 && kinds[s] != DZ_KIND_SPARSE3 &&
+        kinds[s] != DZ_KIND_DENSE)
+      return DZ_E_VALUE;
+  std::vector<int32_t> count(static_cast<size_t>(n_slots), 0);
+  for (int32_t t = 0; t < T; t++) count[slots[t]]++;
+  std::vector<char> pf(static_cast<size_t>(n_slots), 0);
+  for (int32_t s = 0; s < n_slots; s++)
+    pf[s] = pf_min > 0 && count[s] >= pf_min && kinds[s] != DZ_KIND_DENSE;
+  // staged order: prefill groups by slot, then the decode tokens in original order
+  std::vector<int32_t> pstart(static_cast<size_t>(n_slots) + 1, 0);
+  for (int32_t s = 0; s < n_slots; s++) pstart[s + 1] = pstart[s] + (pf[s] ? count[s] : 0);
+  const int32_t t_pf = pstart[n_slots];
+  std::vector<int32_t> fill(pstart.begin(), pstart.end() - 1);
+  int32_t nd = t_pf;
+  std::vector<int32_t> dslot;  // slot of each decode staged row
+  dslot.reserve(static_cast<size_t>(T - t_pf));
+  for (int32_t t = 0; t < T; t++) {
+    if (pf[slots[t]]) {
+      perm_out[fill[slots[t]]++] = t;
+    } else {
+      perm_out[nd++] = t;
+      dslot.push_back(slots[t]);
+    }
+  }
+  int32_t nj = 0;
+  auto push = [&](int32_t slot, int32_t b, int32_t c, int32_t kind) -> bool {
+    if (nj >= max_jobs) return false;
+    jobs_out[nj++] = dz_job{slot, b, c, kind};
+    return true;
+  };
+  for (int32_t s = 0; s < n_slots; s++) {
+    if (!pf[s]) continue;
+    const int32_t c = count[s], nparts = (c + 255) / 256;
+    for (int32_t k = 0; k < nparts; k++) {
+      const int32_t b = pstart[s] + static_cast<int32_t>(static_cast<int64_t>(c) * k / nparts);
+      const int32_t e = pstart[s] + static_cast<int32_t>(static_cast<int64_t>(c) * (k + 1) / nparts);
+      if (!push(s, b, e - b, kinds[s])) return DZ_E_VALUE;
+    }
+  }
+  const int32_t n_pf = nj;
+  // decode part over staged rows [t_pf, T): base jobs, then delta jobs (dz_plan's rules)
+  const int32_t Td = T - t_pf;
+  std::vector<int32_t> dcount(static_cast<size_t>(n_slots) + 1, 0);
+  for (int32_t i = 0; i < Td; i++) dcount[dslot[i] + 1]++;
+  for (int32_t s = 0; s < n_slots; s++) dcount[s + 1] += dcount[s];
+  std::vector<int32_t> dstart(dcount.begin(), dcount.end() - 1), dfill(dstart);
+  for (int32_t i = 0; i < Td; i++) order_out[dfill[dslot[i]]++] = t_pf + i;
+  if (with_base)
+    for (int32_t b = t_pf; b < T; b += 64)
+      if (!push(-1, b, (T - b) < 64 ? (T - b) : 64, 0)) return DZ_E_VALUE;
+  for (int32_t s = 0; s < n_slots; s++) {
+    const int32_t c = dcount[s + 1] - dcount[s];
+    if (c == 0) continue;
+    const int32_t chunk = kinds[s] == DZ_KIND_DENSE ? 32 : 8;
+    for (int32_t off = 0; off < c; off += chunk)
+      if (!push(s, dstart[s] + off, (c - off) < chunk ? (c - off) : chunk, kinds[s])) return DZ_E_VALUE;
+  }
+  *n_jobs_out = nj;
+  *n_pf_jobs_out = n_pf;
+  *t_pf_out = t_pf;
   return DZ_OK;
 }

@@ -1,0 +1,422 @@
+// K3 — prefill SBMM on the 5th-generation tensor cores (sm_100a).
+//
+// Replaces inference.sbmm (inference.py:126-154) for delta groups with many tokens (prefill):
+// y_t = W_base x_t + ΔW_{slot(t)} x_t, where every token of a job shares one delta. The decode
+// kernel (K2) re-streams a delta per 8 tokens with legacy mma.sp; for a 256-token group that is
+// 32 re-reads and a CUDA-core decode per 8 tokens. Here the delta tile is decoded ONCE per
+// (row tile, job) and both products run on tcgen05:
+//
+//   TMEM acc[128 rows][N tokens] = Σ_k  W_base[rows, k] · X[tokens, k]ᵀ        (tcgen05, A = W tile)
+//                                 + Σ_k  ΔW[rows, k]    · X[tokens, k]ᵀ        (tcgen05, A = ΔW tile)
+//
+// with ΔW[r][c] = bf16(code · scale) written by CUDA-core warps from the native 2:4 blocks into a
+// SWIZZLE_128B K-major shared-memory tile (the layout TMA gives the W tile). The base and the
+// delta products accumulate into the same fp32 TMEM tile: no partial buffers, no add kernel.
+// Unlike a merged weight bf16(W + ΔW), the delta keeps its own rounding (one bf16 rounding of
+// code·scale, relative 2^-9), so the fine-tune signal is not swamped by the base's quantum.
+//
+// Item = (128-row tile, job of <= 256 consecutive staged tokens of one delta); items are taken
+// row-tile-major in a static round robin, so the W tile of a row tile is shared through L2 by the
+// jobs running at the same time and the staged X of every job stays L2-resident.
+//
+// Warp roles (10 warps, one CTA per SM, 206 KB shared memory, 512 TMEM columns):
+//  * warps 0-3  dequant: per 64-column stage, 2 row groups each: native block -> bf16 ΔW tile.
+//  * warps 4-7  epilogue: TMEM lane quarter (warp % 4) -> Y rows (tcgen05.ld 32x32b), activation.
+//  * warp 8     TMA producer: W tile (2-D tensor map of the base, box 64 x 128), X tile (box
+//               64 x 64, up to 4 per stage), and per 128 columns the 8 native blocks of the
+//               row tile (1-D bulk copies) into a 2-slot ring.
+//  * warp 9     TMEM owner + MMA issuer: 4 K=16 MMAs of W and 4 of ΔW per stage into a
+//               double-buffered accumulator (2 x 256 columns), so the epilogue of an item
+//               overlaps the next item's main loop.
+#include <cuda.h>
+
+#include <cstdint>
+
+#include "dz_common.cuh"
+#include "dz_tmap.h"
+
+namespace dz {
+namespace pf {
+
+constexpr int M = 128;                      // rows per item (one UMMA M tile)
+constexpr int NMAX = 256;                   // tokens per job (UMMA N <= 256)
+constexpr int KC = 64;                      // columns per stage (one 128-B swizzle row)
+constexpr int NSTAGE = 3;
+constexpr int NDQ = 4;                      // dequant warps
+constexpr int NEPI = 4;                     // epilogue warps
+constexpr int WARP_PROD = NDQ + NEPI;
+constexpr int WARP_MMA = WARP_PROD + 1;
+constexpr int NTHREADS = (WARP_MMA + 1) * 32;
+constexpr int RGS = M / kBlkRows;           // 8 row groups (native block rows) per item
+constexpr int W_BYTES = M * KC * 2;         // 16 KB
+constexpr int DW_BYTES = M * KC * 2;        // 16 KB
+constexpr int XBOX = 64;                    // tokens per X TMA box
+constexpr int X_BYTES = NMAX * KC * 2;      // 32 KB
+constexpr int STAGE = W_BYTES + DW_BYTES + X_BYTES;
+constexpr int DSLOT = RGS * sparse_block_bytes(4);  // 6656 B: one 128-column block column
+constexpr int NDSLOT = 2;
+constexpr int ACC_COLS = NMAX;
+constexpr int TMEM_COLS = 2 * ACC_COLS;
+
+struct Smem {
+  uint64_t full[NSTAGE];    // TMA: W + X of the stage landed
+  uint64_t empty[NSTAGE];   // MMA: the stage (W, ΔW, X) was consumed
+  uint64_t dq[NSTAGE];      // dequant warps: ΔW tile of the stage written
+  uint64_t dfull[NDSLOT];   // TMA: native blocks of a 128-column block column landed
+  uint64_t dempty[NDSLOT];  // dequant warps: done with the block column
+  uint64_t tfull[2];        // MMA: accumulator complete
+  uint64_t tempty[2];       // epilogue: accumulator drained
+  uint32_t tmem_base;
+};
+constexpr int SMEM_BYTES = 1024 + NSTAGE * STAGE + NDSLOT * DSLOT + static_cast<int>(sizeof(Smem));
+
+__device__ __forceinline__ void sts64(uint32_t addr, uint32_t lo, uint32_t hi) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(lo), "r"(hi) : "memory");
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+// byte offset of element (row, col) in a [rows][64] bf16 SWIZZLE_128B K-major tile (1024-B aligned)
+__device__ __forceinline__ uint32_t sw128(int row, int col) {
+  return static_cast<uint32_t>(row * 128 + ((((col >> 3) ^ row) & 7) << 4) + (col & 7) * 2);
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+struct Item {
+  int rt, tok_begin, tok_count, npad, slot, kind;
+};
+
+__device__ __forceinline__ Item item_at(const dz_sbmm_args& a, int item, int n_jobs) {
+  Item it;
+  it.rt = item / n_jobs;
+  const dz_job jb = a.jobs[item - it.rt * n_jobs];
+  it.tok_begin = jb.tok_begin;
+  it.tok_count = jb.tok_count;
+  it.npad = (jb.tok_count + 15) & ~15;
+  it.slot = jb.slot;
+  it.kind = jb.kind;
+  return it;
+}
+
+// Dequantise the 64-column half `h` of the current block column for row groups rg0, rg0+1 of the
+// item into the stage's ΔW tile. Native block layout: dz_codec.cu (k_repack_sparse).
+template <int FB>
+__device__ __forceinline__ void dequant_half(uint32_t dw, uint32_t dslot, int rg0, int n_valid, int h, int qmax,
+                                             int lane) {
+  constexpr int CODE = sparse_code_bytes(FB);
+  constexpr int BB = sparse_block_bytes(FB);
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int m = 0; m < 2; m++) {
+    const int rgl = rg0 + m;
+    const bool valid = rgl < n_valid;  // warp-uniform
+    const uint32_t blk = dslot + rgl * BB;
+    uint2 meta = make_uint2(0x44444444u, 0x44444444u);
+    float sA = 0.f, sB = 0.f;
+    if (valid) {
+      meta = lds64(blk + CODE + lane * 8);
+      const uint2 sv = lds64(blk + CODE + kMetaBytes + g * 8);
+      sA = __uint_as_float(sv.x);
+      sB = __uint_as_float(sv.y);
+    }
+    const uint32_t mw = h ? meta.y : meta.x;  // word i>>1 == h for MMAs i = 2h, 2h+1
+#pragma unroll
+    for (int ii = 0; ii < 2; ii++) {
+      const int i = 2 * h + ii;
+      // E(MMA i, half hh) lives in lane 4g + 2(i&1) + hh (see k_repack_sparse)
+      const uint32_t e0 = __shfl_sync(0xffffffffu, mw, 4 * g + 2 * ii + 0);
+      const uint32_t e1 = __shfl_sync(0xffffffffu, mw, 4 * g + 2 * ii + 1);
+      uint32_t u[8];
+      if (FB == 4) {
+        const uint32_t w = valid ? lds32(blk + lane * 16 + i * 4) : 0x77777777u;
+#pragma unroll
+        for (int k = 0; k < 8; k++) u[k] = (w >> (4 * k)) & 0xFu;
+      } else {
+        const uint32_t w = valid ? lds32(blk + lane * 8 + h * 4) : 0x55555555u;
+        const int o = 4 * ii;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          u[k] = (w >> (2 * (o + k))) & 3u;
+          u[k + 4] = (w >> (2 * (o + k + 8))) & 3u;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int r = g + ((k & 1) ? 8 : 0);
+        const int slot = t + ((k & 2) ? 4 : 0);
+        const uint32_t e = (slot >> 2) ? e1 : e0;
+        const uint32_t nib = (e >> (((k & 1) ? 16 : 0) + 4 * (slot & 3))) & 0xFu;
+        const float s = (k & 1) ? sB : sA;
+        const float v0 = static_cast<float>(static_cast<int>(u[k]) - qmax) * s;
+        const float v1 = static_cast<float>(static_cast<int>(u[k + 4]) - qmax) * s;
+        const int p0 = nib & 3, p1 = nib >> 2;
+        const float c0 = p0 == 0 ? v0 : 0.f, c1 = p0 == 1 ? v0 : (p1 == 1 ? v1 : 0.f);
+        const float c2 = p0 == 2 ? v0 : (p1 == 2 ? v1 : 0.f), c3 = p1 == 3 ? v1 : 0.f;
+        const int row = kBlkRows * rgl + r;
+        const int col = 32 * ii + 4 * slot;
+        sts64(dw + sw128(row, col), pack_bf16(c0, c1), pack_bf16(c2, c3));
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_prefill(const __grid_constant__ dz_sbmm_args a, const __grid_constant__ CUtensorMap xmap) {
+  extern __shared__ uint8_t smem_dyn[];
+  uint8_t* stages = smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);
+  uint8_t* dslots = stages + NSTAGE * STAGE;
+  Smem* sm = reinterpret_cast<Smem*>(dslots + NDSLOT * DSLOT);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  const int n_jobs = a.n_pf_jobs;
+  const int nrt = ceil_div(a.out, M);
+  const int n_items = nrt * n_jobs;
+  const int nch = ceil_div(a.in, KC);
+  const int nkb = ceil_div(a.in, kBlkCols);
+  const int n16 = ceil_div(a.out, kBlkRows);
+  const bool has_base = a.base != nullptr;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; s++) {
+      mbar_init(&sm->full[s], 1);
+      mbar_init(&sm->empty[s], 1);
+      mbar_init(&sm->dq[s], NDQ);
+    }
+    for (int s = 0; s < NDSLOT; s++) {
+      mbar_init(&sm->dfull[s], 1);
+      mbar_init(&sm->dempty[s], NDQ);
+    }
+    for (int b = 0; b < 2; b++) {
+      mbar_init(&sm->tfull[b], 1);
+      mbar_init(&sm->tempty[b], NEPI);
+    }
+    fence_mbar_init();
+  }
+  if (warp == WARP_MMA) {
+    tmem_alloc(&sm->tmem_base, TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = sm->tmem_base;
+
+  if (warp == WARP_PROD) {
+    // ===================== TMA producer =====================
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_keep = policy_evict_last();
+    if (lane == 0) prefetch_tmap(&xmap);
+    int s = 0, ds = 0;
+    uint32_t ph = 0, dph = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const Item it = item_at(a, item, n_jobs);
+      const dz_native_delta* ent = a.table + it.slot;
+      const uint8_t* blocks = static_cast<const uint8_t*>(ent->blocks);
+      const int bb = sparse_block_bytes(kind_fbits(it.kind));
+      const int nrg = min(RGS, n16 - it.rt * RGS);
+      const int nxb = ceil_div(it.npad, XBOX);
+      for (int ch = 0; ch < nch; ch++) {
+        if ((ch & 1) == 0) {  // native blocks of block column ch/2 for this row tile
+          mbar_wait(&sm->dempty[ds], dph ^ 1);
+          if (lane == 0) mbar_arrive_expect_tx(&sm->dfull[ds], static_cast<uint32_t>(nrg * bb));
+          __syncwarp();
+          if (lane < nrg)
+            tma_load_1d(dslots + ds * DSLOT + lane * bb,
+                        blocks + (static_cast<int64_t>(it.rt * RGS + lane) * nkb + (ch >> 1)) * bb,
+                        static_cast<uint32_t>(bb), &sm->dfull[ds], pol_stream);
+          if (++ds == NDSLOT) { ds = 0; dph ^= 1; }
+        }
+        mbar_wait(&sm->empty[s], ph ^ 1);
+        if (lane == 0) {
+          uint8_t* sb = stages + s * STAGE;
+          mbar_arrive_expect_tx(&sm->full[s], (has_base ? W_BYTES : 0) + nxb * XBOX * KC * 2);
+          if (has_base) tma_load_2d(sb, a.base->tmap, ch * KC, it.rt * M, &sm->full[s], pol_keep);
+          for (int b = 0; b < nxb; b++)
+            tma_load_2d(sb + W_BYTES + DW_BYTES + b * XBOX * KC * 2, &xmap, ch * KC, it.tok_begin + b * XBOX,
+                        &sm->full[s], pol_keep);
+        }
+        __syncwarp();
+        if (++s == NSTAGE) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == WARP_MMA) {
+    // ===================== tcgen05 issuer =====================
+    int s = 0, nacc = 0;
+    uint32_t ph = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const Item it = item_at(a, item, n_jobs);
+      const int buf = nacc & 1;
+      mbar_wait(&sm->tempty[buf], ((nacc >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t idesc = umma_idesc_bf16(M, it.npad);
+      const uint32_t tmem_d = tmem_base + buf * ACC_COLS;
+      for (int ch = 0; ch < nch; ch++) {
+        mbar_wait(&sm->full[s], ph);
+        mbar_wait(&sm->dq[s], ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sb = smem_u32(stages + s * STAGE);
+          const uint64_t xdesc = umma_desc_sw128(sb + W_BYTES + DW_BYTES);
+          if (has_base) {
+            const uint64_t wdesc = umma_desc_sw128(sb);
+#pragma unroll
+            for (int k = 0; k < KC / 16; k++)
+              umma_bf16(tmem_d, wdesc + 2 * k, xdesc + 2 * k, idesc, (ch | k) ? 1u : 0u);
+          }
+          const uint64_t ddesc = umma_desc_sw128(sb + W_BYTES);
+#pragma unroll
+          for (int k = 0; k < KC / 16; k++)
+            umma_bf16(tmem_d, ddesc + 2 * k, xdesc + 2 * k, idesc, (has_base || (ch | k)) ? 1u : 0u);
+          umma_commit(&sm->empty[s]);
+          if (ch == nch - 1) umma_commit(&sm->tfull[buf]);
+        }
+        __syncwarp();
+        if (++s == NSTAGE) { s = 0; ph ^= 1; }
+      }
+      nacc++;
+    }
+  } else if (warp < NDQ) {
+    // ===================== dequant warps =====================
+    int s = 0, ds = 0;
+    uint32_t ph = 0, dph = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const Item it = item_at(a, item, n_jobs);
+      const int nrg = min(RGS, n16 - it.rt * RGS);
+      const int qmax = kind_qmax(it.kind);
+      const bool two_bit = it.kind == DZ_KIND_SPARSE2;
+      for (int ch = 0; ch < nch; ch++) {
+        if ((ch & 1) == 0) mbar_wait(&sm->dfull[ds], dph);
+        mbar_wait(&sm->empty[s], ph ^ 1);  // the MMAs that last read this ΔW tile are done
+        const uint32_t dw = smem_u32(stages + s * STAGE + W_BYTES);
+        const uint32_t dsl = smem_u32(dslots + ds * DSLOT);
+        if (two_bit)
+          dequant_half<2>(dw, dsl, 2 * warp, nrg, ch & 1, qmax, lane);
+        else
+          dequant_half<4>(dw, dsl, 2 * warp, nrg, ch & 1, qmax, lane);
+        fence_proxy_async();  // generic-proxy st.shared -> visible to the tensor core (async proxy)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm->dq[s]);
+        if ((ch & 1) == 1 || ch == nch - 1) {
+          if (lane == 0) mbar_arrive(&sm->dempty[ds]);
+          if (++ds == NDSLOT) { ds = 0; dph ^= 1; }
+        }
+        if (++s == NSTAGE) { s = 0; ph ^= 1; }
+      }
+    }
+  } else {
+    // ===================== epilogue warps =====================
+    const int q = warp & 3;
+    int nacc = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const Item it = item_at(a, item, n_jobs);
+      const int buf = nacc & 1;
+      mbar_wait(&sm->tfull[buf], (nacc >> 1) & 1);
+      tc_fence_after();
+      const int row = it.rt * M + 32 * q + lane;
+      const uint32_t taddr = tmem_base + buf * ACC_COLS + (static_cast<uint32_t>(32 * q) << 16);
+#pragma unroll 1
+      for (int c = 0; c < it.npad / 16; c++) {
+        uint32_t v[16];
+        tmem_ld16(taddr + c * 16, v);
+        const int i0 = it.tok_begin + c * 16;
+        int yr = i0 + (lane & 15);
+        if (a.perm != nullptr && c * 16 + (lane & 15) < it.tok_count) yr = a.perm[yr];
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+          const int yrow = __shfl_sync(0xffffffffu, yr, j);
+          if (c * 16 + j < it.tok_count && row < a.out) {
+            float y = __uint_as_float(v[j]);
+            if (a.act == DZ_ACT_TANH) y = tanhf(y);
+            const int64_t yo = static_cast<int64_t>(yrow) * a.ldy + row;
+            if (a.y_dtype == DZ_F32)
+              reinterpret_cast<float*>(a.Y)[yo] = y;
+            else
+              reinterpret_cast<__nv_bfloat16*>(a.Y)[yo] = __float2bfloat16_rn(y);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm->tempty[buf]);
+      nacc++;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == WARP_MMA) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+// Staging gather: Xs[i] = X[perm[i]], 16 B per thread.
+__global__ void k_gather_rows(const uint16_t* __restrict__ X, int64_t ldx, const int32_t* __restrict__ perm, int T,
+                              int in8, uint16_t* __restrict__ Xs, int64_t ldxs) {
+  const int64_t n = static_cast<int64_t>(T) * in8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / in8), c = static_cast<int>(i - static_cast<int64_t>(r) * in8);
+    const int src = __ldg(perm + r);
+    reinterpret_cast<uint4*>(Xs + r * ldxs)[c] = __ldg(reinterpret_cast<const uint4*>(X + src * ldx) + c);
+  }
+}
+
+}  // namespace pf
+}  // namespace dz
+
+using namespace dz;
+
+static_assert(pf::SMEM_BYTES <= 232448, "prefill kernel shared memory");
+static_assert(pf::STAGE % 1024 == 0 && pf::W_BYTES % 1024 == 0 && pf::DW_BYTES % 1024 == 0, "SW128 tile alignment");
+
+extern "C" int dz_gather_rows(const uint16_t* X, int64_t ldx, const int32_t* perm, int32_t T, int32_t in,
+                              uint16_t* Xs, int64_t ldxs, void* stream) {
+  if (T < 0 || in < 1) return DZ_E_SHAPE;
+  if (!X || !perm || !Xs) return DZ_E_VALUE;
+  if ((ldx % 8) || (ldxs % 8) || (reinterpret_cast<uintptr_t>(X) & 15) || (reinterpret_cast<uintptr_t>(Xs) & 15))
+    return DZ_E_SHAPE;
+  if (T == 0) return DZ_OK;
+  const int in8 = ceil_div(static_cast<int>(ldx < ldxs ? ldx : ldxs), 8);  // whole padded rows (zero tail kept)
+  const int64_t n = static_cast<int64_t>(T) * in8;
+  const int blocks = static_cast<int>((n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8);
+  pf::k_gather_rows<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(X, ldx, perm, T, in8, Xs, ldxs);
+  return cudaGetLastError() == cudaSuccess ? DZ_OK : DZ_E_CUDA;
+}
+
+// Launch K3 over jobs[0:n_pf_jobs]; X is the staged buffer (xs when perm is set).
+extern "C" int dz_sbmm_prefill(const dz_sbmm_args* a, void* stream) {
+  if (!a || !a->Y || !a->table || !a->jobs) return DZ_E_VALUE;
+  if (a->T < 0 || a->out < 1 || a->in < 1) return DZ_E_SHAPE;
+  if (a->n_pf_jobs <= 0 || a->T == 0) return DZ_OK;
+  const uint16_t* X = a->perm ? static_cast<const uint16_t*>(a->xs) : a->X;
+  if (!X) return DZ_E_VALUE;
+  if ((a->ldx % 8) != 0 || (reinterpret_cast<uintptr_t>(X) & 15) != 0 || a->ldx < a->in) return DZ_E_SHAPE;
+  if (a->y_dtype != DZ_F32 && a->y_dtype != DZ_BF16) return DZ_E_VALUE;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(pf::k_prefill, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::SMEM_BYTES);
+  });
+  if (attr_err != cudaSuccess) return DZ_E_CUDA;
+  CUtensorMap xmap;  // staged X [T][in] bf16, 64-column x 64-token SWIZZLE_128B boxes (UMMA B operand)
+  const int st = encode_2d(&xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, X, static_cast<uint64_t>(a->in),
+                           static_cast<uint64_t>(a->T), static_cast<uint64_t>(a->ldx) * 2, pf::KC, pf::XBOX,
+                           CU_TENSOR_MAP_SWIZZLE_128B);
+  if (st) return st;
+  dz_sbmm_args k = *a;
+  k.X = X;
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return DZ_E_CUDA;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return DZ_E_CUDA;
+  const int n_items = ceil_div(a->out, pf::M) * a->n_pf_jobs;
+  int grid = a->grid > 0 ? a->grid : sms;
+  if (grid > n_items) grid = n_items;
+  pf::k_prefill<<<grid, pf::NTHREADS, pf::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(k, xmap);
+  return cudaGetLastError() == cudaSuccess ? DZ_OK : DZ_E_CUDA;
+}

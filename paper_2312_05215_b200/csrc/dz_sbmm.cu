@@ -1,22 +1,24 @@
-// K2 — fused base GEMM + selective batched (2:4, low-bit) delta matmul for sm_100a.
+// K2 — fused base GEMM + selective batched (2:4, low-bit) delta matmul for sm_100a (decode regime).
 //
 // Replaces inference.sbmm (inference.py:126-154): y_t = W_base x_t + ΔW_{slot(t)} x_t.
 //
-// Work decomposition. An item is (row tile of RT=128 output rows, job); a job is either the base
-// GEMM for up to 64 tokens or one delta group for up to 16 (sparse) / 64 (dense) of its tokens
-// (dz_plan = group_by_delta, inference.py:106-123). Items are ordered job-major (all base items
-// first, the big ones) and pulled by persistent CTAs from an atomic counter (2 CTAs per SM).
+// Work decomposition. An item is (row tile, job); a job is either the base GEMM for up to 64
+// tokens (row tile = 128 rows, one UMMA M tile) or one delta group for up to 8 (2:4 sparse) / 32
+// (dense) of its tokens (row tile = 256 rows; dz_plan = group_by_delta, inference.py:106-123).
+// Base items come first, then delta items row-tile-major; one persistent CTA per SM pulls items
+// from a self-resetting atomic counter with one item of lookahead.
 //
-// Warp roles per CTA:
-//  * producer (1 warp): per chunk ONE 2-D TMA tensor copy of the item's A operand — the base W
-//    tile in its natural layout (128 rows x 64 cols, SWIZZLE_128B), or the delta's native blocks
-//    viewed as a 2-D uint64 array — plus the X tile: one swizzled tensor copy for the base
-//    (contiguous tokens, OOB rows zero-filled) or one 1-D bulk copy per routed token for a delta.
-//    Stages form a 4-deep shared-memory ring with full/empty mbarriers.
-//  * MMA issuer (1 warp, one elected thread): base stages become tcgen05.mma kind::f16
-//    (M=128 rows, N=64 tokens, K=16 x 4 per stage) into a double-buffered TMEM accumulator;
-//    tcgen05.commit frees the stage and, on the last chunk, signals the accumulator full.
-//  * consumers (4 warps, two 16-row groups each): 2:4 delta stages — decode codes in registers
+// Warp roles per CTA (11 warps):
+//  * TMA producer (1 warp): per stage ONE tensor copy of the A operand — two 64-col x 128-row
+//    SWIZZLE_128B tiles of the base W in its natural layout, or a 3-D box of 4 native blocks x 16
+//    row groups of a delta (53 KB) — plus, for base stages, the swizzled X tile (contiguous tokens,
+//    OOB rows zero-filled). 3-deep ring with full/empty mbarriers; the next item's id, descriptor
+//    and token ids are prefetched while the current item streams.
+//  * X producer (1 warp): one 1-D bulk copy per routed token row of a delta stage.
+//  * MMA issuer (1 warp, one elected thread): base stages become tcgen05.mma kind::f16 (M=128,
+//    N=64 tokens, K=16 x 8 per stage) into a double-buffered TMEM accumulator; tcgen05.commit
+//    frees the stage and, on the last chunk, signals the accumulator full.
+//  * consumers (8 warps, two 16-row groups each): 2:4 delta stages — decode codes in registers
 //    (LOP3 magic-number bf16 conversion; deferred per-(row,128-col) scaling) and mma.sp m16n8k32
 //    (the reference's index nibble IS the sparse-MMA metadata), fp32 accumulation; dense-delta
 //    stages use mma m16n8k16. They also drain the base accumulator from TMEM (tcgen05.ld).
@@ -27,6 +29,10 @@
 // fp32 addition is commutative, so the result does not depend on arrival order), applies the
 // activation, writes Y and resets the word. No partial buffers, no combine pass, no separate add
 // kernel; deterministic and batch-invariant (a token's K order never depends on the batch).
+//
+// Mixed batches: groups large enough for the tensor-core prefill kernel (K3, dz_prefill.cu) are
+// staged first in a permuted copy of X; this kernel then covers the remaining (decode) rows and
+// writes row i of the staged X to Y row perm[i].
 #include <cuda.h>
 
 #include <cstddef>
@@ -35,6 +41,7 @@
 #include <mutex>
 
 #include "dz_common.cuh"
+#include "dz_tmap.h"
 
 #ifdef DZ_TRACE
 // Per-warp private event slots of the traced CTA (the one that took item 0): plain stores, no
@@ -314,6 +321,7 @@ __device__ __forceinline__ void dense_dispatch(int nt, float (&acc)[MR][NT_DN][4
 
 struct MergeCtx {
   unsigned long long* slots;  // [T][out] {fp32 value bits, count} words, zero between launches
+  const int32_t* perm;        // staged row -> Y row (mixed plans), or NULL
   void* Y;
   int64_t ldy;
   int out, y_dtype, act;
@@ -322,7 +330,8 @@ struct MergeCtx {
 
 __device__ __forceinline__ void store_y(const MergeCtx& m, int tok, int row, float v) {
   if (m.act == DZ_ACT_TANH) v = tanhf(v);
-  const int64_t yo = static_cast<int64_t>(tok) * m.ldy + row;
+  const int yrow = m.perm != nullptr ? __ldg(m.perm + tok) : tok;
+  const int64_t yo = static_cast<int64_t>(yrow) * m.ldy + row;
   if (m.y_dtype == DZ_F32)
     reinterpret_cast<float*>(m.Y)[yo] = v;
   else
@@ -432,12 +441,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int nkb = ceil_div(a.in, kBlkCols);
   const int nch_base = ceil_div(a.in, BASE_CH * KC_DN);
   const int nbt = ceil_div(a.out, BASE_RT);
-  const int n_base = a.base != nullptr ? ceil_div(a.T, BASE_N) : 0;  // dz_plan: base jobs first
+  const int n_base = a.base != nullptr ? ceil_div(a.T - a.t_pf, BASE_N) : 0;  // dz_plan: base jobs first
   const int n_items = nbt * n_base + nrt * (a.n_jobs - n_base);
 
   int* sched = reinterpret_cast<int*>(a.workspace);  // [0] item counter, [1] finished CTAs
   MergeCtx mctx;
   mctx.slots = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(a.workspace) + 256);
+  mctx.perm = a.perm;
   mctx.Y = a.Y;
   mctx.ldy = a.ldy;
   mctx.out = a.out;
@@ -757,39 +767,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
-// ------------------------------------------------------------------------------------------
-// Host: TMA descriptors (driver entry point fetched through the runtime; no -lcuda)
-// ------------------------------------------------------------------------------------------
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeTiledFn encode_fn() {
-  static std::once_flag once;
-  static EncodeTiledFn fn = nullptr;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  });
-  return fn;
-}
-
-static int encode_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t dim0, uint64_t dim1,
-                     uint64_t stride1_bytes, uint32_t box0, uint32_t box1, CUtensorMapSwizzle swz) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn) return DZ_E_CUDA;
-  const cuuint64_t dims[2] = {dim0, dim1};
-  const cuuint64_t strides[1] = {stride1_bytes};
-  const cuuint32_t box[2] = {box0, box1};
-  const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? DZ_OK : DZ_E_CUDA;
-}
-
 }  // namespace dz
 
 using namespace dz;
@@ -877,14 +854,7 @@ extern "C" int dz_sbmm_ctas_per_sm(void) {
   return n;
 }
 
-extern "C" int dz_sbmm(const dz_sbmm_args* a, void* stream) {
-  if (!a || !a->X || !a->Y || !a->workspace) return DZ_E_VALUE;
-  if (a->T < 0 || a->out < 1 || a->in < 1) return DZ_E_SHAPE;
-  if (a->T == 0 || a->n_jobs == 0) return DZ_OK;
-  const int in_pad = ceil_div(a->in, kBlkCols) * kBlkCols;
-  if (a->ldx < in_pad || (a->ldx % 8) != 0 || (reinterpret_cast<uintptr_t>(a->X) & 15) != 0) return DZ_E_SHAPE;
-  if (a->ldy < a->out) return DZ_E_SHAPE;
-  if (a->y_dtype != DZ_F32 && a->y_dtype != DZ_BF16) return DZ_E_VALUE;
+static int launch_decode(const dz_sbmm_args* a, void* stream) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   static int ctas_per_sm = 1;
@@ -907,10 +877,41 @@ extern "C" int dz_sbmm(const dz_sbmm_args* a, void* stream) {
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return DZ_E_CUDA;
     grid = sms * ctas_per_sm;
   }
-  const int n_items = ceil_div(a->out, RT) * a->n_jobs;
+  const int n_items = ceil_div(a->out, RT) * a->n_jobs + ceil_div(a->out, BASE_RT) * ceil_div(a->T, BASE_N);
   if (grid > n_items) grid = n_items;
   k_sbmm<<<grid, NTHREADS, SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(*a, xmap);
   return cudaGetLastError() == cudaSuccess ? DZ_OK : DZ_E_CUDA;
+}
+
+extern "C" int dz_sbmm(const dz_sbmm_args* a, void* stream) {
+  if (!a || !a->X || !a->Y || !a->workspace) return DZ_E_VALUE;
+  if (a->T < 0 || a->out < 1 || a->in < 1) return DZ_E_SHAPE;
+  if (a->T == 0 || a->n_jobs == 0) return DZ_OK;
+  const int in_pad = ceil_div(a->in, kBlkCols) * kBlkCols;
+  if (a->ldx < in_pad || (a->ldx % 8) != 0 || (reinterpret_cast<uintptr_t>(a->X) & 15) != 0) return DZ_E_SHAPE;
+  if (a->ldy < a->out) return DZ_E_SHAPE;
+  if (a->y_dtype != DZ_F32 && a->y_dtype != DZ_BF16) return DZ_E_VALUE;
+  if (a->perm == nullptr) {
+    if (a->n_pf_jobs != 0 || a->t_pf != 0) return DZ_E_VALUE;
+    return launch_decode(a, stream);
+  }
+  // mixed plan: stage X in plan order, prefill jobs on K3, the rest on K2
+  if (!a->xs || a->n_pf_jobs < 0 || a->n_pf_jobs > a->n_jobs || a->t_pf < 0 || a->t_pf > a->T) return DZ_E_VALUE;
+  int st = dz_gather_rows(a->X, a->ldx, a->perm, a->T, a->in, static_cast<uint16_t*>(a->xs), a->ldx, stream);
+  if (st) return st;
+  if (a->n_pf_jobs > 0) {
+    st = dz_sbmm_prefill(a, stream);
+    if (st) return st;
+  }
+  if (a->n_jobs > a->n_pf_jobs) {
+    dz_sbmm_args k = *a;
+    k.X = static_cast<const uint16_t*>(a->xs);
+    k.jobs = a->jobs + a->n_pf_jobs;
+    k.n_jobs = a->n_jobs - a->n_pf_jobs;
+    k.n_pf_jobs = 0;
+    return launch_decode(&k, stream);
+  }
+  return DZ_OK;
 }
 
 #ifdef DZ_TRACE

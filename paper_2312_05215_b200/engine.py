@@ -15,6 +15,7 @@
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -142,36 +143,49 @@ class DeltaTable:
         return len(self.deltas)
 
 
+PF_MIN = int(os.environ.get("DZ_PF_MIN", "128"))  # tokens per delta group routed to the prefill kernel
+
+
 class Plan:
-    """Batch plan: stable sort of tokens by slot + job list (dz_plan), uploaded to the device."""
+    """Batch plan (group_by_delta, inference.py:106-123), uploaded to the device.
+
+    Decode plan (no group reaches `pf_min` tokens): stable sort of tokens by slot + job list
+    (dz_plan). Mixed plan: groups of >= pf_min tokens become prefill jobs for K3 over a staged
+    (permuted) copy of X and the remaining tokens are planned for K2 (dz_plan_mixed)."""
 
     def __init__(self, slots, kinds: np.ndarray, n_slots: int, with_base: bool = True, device=None,
-                 upload: bool = True):
+                 upload: bool = True, pf_min: int | None = None):
         s = np.ascontiguousarray(np.asarray(slots, dtype=np.int32).ravel())
         self.T = int(s.size)
         lib = L.lib()
         maxj = lib.dz_plan_max_jobs(self.T)
         order = np.zeros(max(self.T, 1), dtype=np.int32)
+        perm = np.zeros(max(self.T, 1), dtype=np.int32)
         jobs = (L.DzJob * max(maxj, 1))()
-        nj = C.c_int32(0)
+        nj, npf, tpf = C.c_int32(0), C.c_int32(0), C.c_int32(0)
         kinds = np.ascontiguousarray(kinds, dtype=np.int32)
-        st = lib.dz_plan(s.ctypes.data, self.T, kinds.ctypes.data, n_slots, 1 if with_base else 0,
-                         order.ctypes.data, jobs, maxj, C.byref(nj))
+        self.pf_min = PF_MIN if pf_min is None else int(pf_min)
+        st = lib.dz_plan_mixed(s.ctypes.data, self.T, kinds.ctypes.data, n_slots, 1 if with_base else 0,
+                               self.pf_min, perm.ctypes.data, order.ctypes.data, jobs, maxj, C.byref(nj),
+                               C.byref(npf), C.byref(tpf))
         if st == L.DZ_E_UNKNOWN:
             raise UnknownDeltaError("a token references a slot outside the delta table")
         L.check(st, "plan")
-        self.n_jobs = int(nj.value)
+        self.n_jobs, self.n_pf_jobs, self.t_pf = int(nj.value), int(npf.value), int(tpf.value)
         self.order_host = order[: self.T].copy()
+        self.perm_host = perm[: self.T].copy() if self.t_pf > 0 else None
         self.jobs_host = np.frombuffer(C.string_at(C.addressof(jobs), C.sizeof(L.DzJob) * max(self.n_jobs, 1)),
                                        dtype=np.int32).reshape(-1, 4)[: self.n_jobs].copy()
         self.jobs_bytes = np.frombuffer(C.string_at(C.addressof(jobs), C.sizeof(L.DzJob) * max(maxj, 1)),
                                         dtype=np.uint8).copy()
         self.with_base = with_base
-        self.order = self.jobs = None
+        self.order = self.jobs = self.perm = None
         if upload:
             dev = device or require_cuda()
             self.order = torch.from_numpy(order).to(dev)
             self.jobs = torch.from_numpy(self.jobs_bytes).to(dev)
+            if self.t_pf > 0:
+                self.perm = torch.from_numpy(perm).to(dev)
 
 
 class Workspace:
@@ -236,6 +250,10 @@ def sbmm_forward(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: De
     a.workspace = ws.data_ptr()
     a.grid = grid
     a.debug = debug
+    if plan.perm is not None:  # mixed plan: staged copy of X (same padded row stride)
+        xs = torch.empty_like(Xp)
+        a.perm, a.xs = plan.perm.data_ptr(), xs.data_ptr()
+        a.n_pf_jobs, a.t_pf = plan.n_pf_jobs, plan.t_pf
     L.check(L.lib().dz_sbmm(C.byref(a), stream_ptr()), "sbmm")
     return Y
 
