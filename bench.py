@@ -6,13 +6,18 @@ One step = one decode step through all 32 layers x 7 linears (q,k,v,o 4096x4096;
 11008x4096; down 4096x11008): 224 fused SBMM launches, each reading the bf16 base weight once and
 every delta of the 32 routed deltas once (97.5 GB per step, far larger than L2 — no L2 flush
 needed). Attention/norm/activation are out of scope (the reference hot path is the decoupled
-linear): o consumes v's output, down consumes up's output, the next layer consumes
-down's output. The step is captured in one CUDA graph.
+linear): o consumes the q slice of the QKV output, down the up slice of the gate/up
+output, the next layer down's output (paper_2312_05215_b200/stack.py). The step is captured in
+one CUDA graph.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N>1 (torchrun): Megatron tensor parallelism of the same stack — q,k,v,gate,up column-parallel,
-o,down row-parallel + NCCL all-reduce; intermediate (11008) sharded in 128-column blocks.
+N>1 (torchrun): Megatron tensor parallelism of the same stack (strong scaling) — q,k,v,gate,up
+column-parallel, o,down row-parallel + NCCL all-reduce; shared dimensions cut on 128-column
+native-block edges (7B intermediate 11008 = 86 blocks, uneven at TP 4/8).
+
+--impl reference: the reference algorithm (oracle port of inference.sbmm, numpy f64) on the
+host cores, one process per core over the active deltas.
 """
 
 from __future__ import annotations
@@ -52,6 +57,11 @@ def parse():
     return p.parse_args()
 
 
+METRIC = "decode tokens/s (Llama-2-7B-shaped stack, 32 x 4-bit 2:4 deltas, batch 64)"
+WORKLOAD = ("llama2-7b decoder stack, {layers} layers x 7 linears (q,k,v,o,gate,up,down; QKV and gate/up row-fused "
+            "into one launch each), D=32 4-bit 2:4 deltas (gs=128), T=64 decode tokens, ids=perm(i%32)")
+
+
 def token_ids():
     rng = np.random.default_rng(ID_SEED)
     return rng.permutation([i % D_DELTAS for i in range(T_TOKENS)]).astype(np.int32)
@@ -60,65 +70,92 @@ def token_ids():
 # ----------------------------------------------------------------------------- CPU reference arm
 
 
-def cpu_reference_sample(model: str = MODEL, deltas_per_shape: int = 1, tokens: int = 4):
-    """Time the oracle port (numpy f64, the reference's algorithm) on a bounded sample of the
-    same workload: per distinct linear shape, sbmm over `deltas_per_shape` deltas and `tokens`
-    tokens; extrapolate linearly in active deltas (cost per active delta is the dequantise,
-    inference.py:145-153) to the full step. Returns (tokens_per_s, seconds_of_work, desc)."""
+def _delta_task(args):
+    """One active delta of the reference sbmm on one linear shape (oracle port, numpy f64):
+    dequantise + the routed tokens' GEMV (inference.py:140-153). Runs in a worker process."""
+    out, inp, seed, tokens = args
     import oracle as O
-    from paper_2312_05215_b200.synth import llama_linears
+    rng = np.random.default_rng(seed)
+    W = rng.normal(0, 1 / math.sqrt(inp), (out, inp)).astype(np.float32).astype(np.float64)
+    ld = O.random_packed_delta(rng, out, inp, BITS)
+    X = rng.normal(0, 1, (tokens, inp))
+    t0 = time.perf_counter()
+    O.sbmm_matrix(W, {0: ld}, np.zeros(tokens, np.int64), X)
+    return time.perf_counter() - t0
 
-    rng = np.random.default_rng(0)
-    t_work = 0.0
-    per_shape = {}
-    shapes = {}
-    for name, out, inp in llama_linears(model):
-        shapes.setdefault((out, inp), []).append(name)
-    for (out, inp), names in shapes.items():
-        W = rng.normal(0, 1 / math.sqrt(inp), (out, inp)).astype(np.float32).astype(np.float64)
-        ds = {d: O.random_packed_delta(rng, out, inp, BITS) for d in range(deltas_per_shape)}
-        X = rng.normal(0, 1, (tokens, inp))
-        ids = np.arange(tokens) % deltas_per_shape
-        t0 = time.perf_counter()
-        O.sbmm_matrix(W, ds, ids, X)
-        dt = time.perf_counter() - t0
-        t_work += dt
-        # base GEMM for the full batch (64 tokens) measured too
-        X64 = rng.normal(0, 1, (T_TOKENS, inp))
-        t1 = time.perf_counter()
-        _ = X64 @ W.T
-        tb = time.perf_counter() - t1
-        t_work += tb
-        per_delta = dt / deltas_per_shape
-        per_shape[(out, inp)] = (D_DELTAS * per_delta + tb, len(names))
-    layers = 32
-    step_s = layers * sum(t * n for t, n in per_shape.values())
-    desc = (f"oracle sbmm (numpy f64) per distinct 7B linear shape with {deltas_per_shape} delta(s) x "
-            f"{tokens} tokens + 64-token base GEMM, extrapolated x{D_DELTAS} active deltas x{layers} layers")
-    return T_TOKENS / step_s, t_work, desc
+
+def _base_task(args):
+    out, inp, seed = args
+    rng = np.random.default_rng(seed)
+    W = rng.normal(0, 1 / math.sqrt(inp), (out, inp))
+    X = rng.normal(0, 1, (T_TOKENS, inp))
+    t0 = time.perf_counter()
+    _ = X @ W.T
+    return time.perf_counter() - t0
+
+
+class CpuReference:
+    """The reference algorithm (oracle port of inference.sbmm, numpy f64) on the host cores.
+
+    The reference's cost is one dequantise + GEMV per ACTIVE delta per linear (inference.py:
+    140-153, single-threaded numpy masked gathers), so the step parallelises over deltas: a pool
+    of `cores` processes runs one active delta each, concurrently, per distinct 7B linear shape.
+    A sample = one such round per shape (cores deltas x 2 tokens) + the 64-token base GEMM;
+    the step time is extrapolated to 32 active deltas x 32 layers."""
+
+    def __init__(self, cores: int | None = None):
+        import multiprocessing as mp
+        from paper_2312_05215_b200.synth import llama_linears
+        self.cores = cores or min(os.cpu_count() or 1, 32)  # ~1.5 GB of numpy temporaries per worker
+        self.pool = mp.get_context("fork").Pool(self.cores)
+        self.shapes = {}
+        for name, out, inp in llama_linears(MODEL):
+            self.shapes.setdefault((out, inp), []).append(name)
+        self.round = 0
+
+    def sample(self):
+        per_shape, work = {}, 0.0
+        for k, ((out, inp), names) in enumerate(self.shapes.items()):
+            seeds = [(out, inp, 1000 * self.round + 31 * k + c, T_TOKENS // D_DELTAS) for c in range(self.cores)]
+            # each task times only its own sbmm (inputs are generated before its clock starts);
+            # the tasks run concurrently, one per core, so `cores` deltas take max(times)
+            times = self.pool.map(_delta_task, seeds, chunksize=1)
+            tb = _base_task((out, inp, k))
+            work += max(times) + tb
+            per_delta = max(times) / self.cores
+            per_shape[(out, inp)] = (D_DELTAS * per_delta + tb, len(names))
+        self.round += 1
+        step_s = 32 * sum(t * n for t, n in per_shape.values())
+        desc = (f"oracle port of inference.sbmm (numpy f64): per distinct 7B linear shape, {self.cores} active "
+                f"deltas x {T_TOKENS // D_DELTAS} tokens dequantised concurrently on {self.cores} processes + the "
+                f"64-token base GEMM; extrapolated to {D_DELTAS} active deltas x 32 layers "
+                f"({work:.1f} s wall per sample)")
+        return T_TOKENS / step_s, work, desc
+
+    def close(self):
+        self.pool.terminate()
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cores = os.cpu_count()
-    for _ in range(args.warmup):
-        pass  # the sample has no warm state worth warming beyond numpy import
-    vals, work = [], 0.0
+    ref = CpuReference()
+    for _ in range(min(args.warmup, 1)):
+        ref.sample()  # forks warm (numpy imported, pages touched)
+    vals = []
     for _ in range(max(1, args.steps)):
-        v, w, desc = cpu_reference_sample()
+        v, w, desc = ref.sample()
         vals.append(v)
-        work += w
+    ref.close()
     v = float(np.median(vals))
     line = {
-        "impl": "reference", "metric": "decode tokens/s (Llama-2-7B-shaped stack, 32 x 4-bit 2:4 deltas, batch 64)",
+        "impl": "reference", "metric": METRIC,
         "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * T_TOKENS / v, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "llama2-7b decoder stack, 32 layers x 7 linears, D=32 4-bit 2:4 deltas, T=64 decode",
-                   "parallelism": "cpu"},
-        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": desc},
+        "config": {"workload": WORKLOAD.format(layers=32), "global_batch": T_TOKENS, "parallelism": "cpu"},
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": ref.cores, "kind": "port", "sample": desc},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -188,47 +225,15 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
-FUSED = {"qkv": ("q", "k", "v"), "o": ("o",), "gate_up": ("gate", "up"), "down": ("down",)}
-
-
-def build_stack(layers, rank, world, device):
-    """Per layer 4 fused linears (QKV and gate/up row-concatenated: they read the same input),
-    each = (base W, delta table of 32 natives). Deltas are generated per original linear and
-    concatenated, so bytes and math are exactly those of the 7 separate linears."""
-    import torch
-    from paper_2312_05215_b200.device import ErrFlag
-    from paper_2312_05215_b200.engine import DeltaTable, NativeBase, concat_rows
-    from paper_2312_05215_b200.synth import llama_linears, random_base, random_native_delta
-    from paper_2312_05215_b200.tp import TpLinear
-
-    gen = torch.Generator(device=device)
-    err = ErrFlag(device)
-    shapes = {n: (o, i) for n, o, i in llama_linears(MODEL)}
-    names = [n for n, _, _ in llama_linears(MODEL)]
-    stack = []
-    for l in range(layers):
-        lin = {}
-        for fname, members in FUSED.items():
-            Ws, per_delta = [], [[] for _ in range(D_DELTAS)]
-            for m in members:
-                out, inp = shapes[m]
-                gen.manual_seed(10_000 + 7 * l + names.index(m))
-                Ws.append(random_base(out, inp, gen, device))
-                for d in range(D_DELTAS):
-                    per_delta[d].append(random_native_delta(out, inp, BITS, gen, device, err))
-            W = torch.cat(Ws) if len(Ws) > 1 else Ws[0]
-            nats = [concat_rows(p) if len(p) > 1 else p[0] for p in per_delta]
-            out, inp = int(W.shape[0]), int(W.shape[1])
-            if world == 1:
-                lin[fname] = (NativeBase(W), DeltaTable(nats, out, inp), out, inp)
-            else:
-                axis = "row" if fname in ("o", "down") else "column"
-                lin[fname] = TpLinear(W, nats, axis, rank, world)
-            del W, Ws, per_delta
-        stack.append(lin)
-        torch.cuda.synchronize()
-    err.raise_if_set("synthetic delta upload")
-    return stack
+def ncu_traffic():
+    """Per-launch DRAM bytes (read + write) of the fused kernel from the committed ncu --set full
+    capture (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "r01_ncu_traffic_v10.json")
+    if not os.path.exists(p):
+        return None, None
+    with open(p) as f:
+        d = json.load(f)
+    return float(d["mean_dram_bytes_per_launch"]), float(d["mean_algorithmic_bytes_per_launch"])
 
 
 def main():
@@ -247,79 +252,40 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
 
-    from paper_2312_05215_b200 import _lib as L
-    from paper_2312_05215_b200.engine import Plan, Workspace, sbmm_forward
-    from paper_2312_05215_b200.synth import linear_algorithmic_bytes, llama_linears
+    from paper_2312_05215_b200.engine import Plan
+    from paper_2312_05215_b200.stack import STEP_ORDER, LlamaStack
 
     t_build = time.time()
-    stack = build_stack(args.layers, rank, world, device)
+    st = LlamaStack(MODEL, args.layers, D_DELTAS, BITS, device, rank=rank, world=world)
     t_build = time.time() - t_build
 
     ids = token_ids()
-    kinds = np.full(D_DELTAS, L.DZ_KIND_SPARSE4, dtype=np.int32)
+    kinds = st.kinds
     plan = Plan(ids, kinds, D_DELTAS, device=device)
-    ws = Workspace()
-    shapes = dict((n, (o, i)) for n, o, i in llama_linears(MODEL))
-    hid, inter = shapes["q"][1], shapes["gate"][0]
-
-    # activation buffers (static addresses for graph capture). Attention is out of scope: o reads
-    # the v slice of the fused QKV output, down reads the up slice of the fused gate/up output.
-    def buf(cols):
-        return torch.zeros(T_TOKENS, cols, dtype=torch.bfloat16, device=device)
-
-    fshape = {f: (sum(shapes[m][0] for m in ms), shapes[ms[0]][1]) for f, ms in FUSED.items()}
-    x_in = buf(hid)
-    if world == 1:
-        outs = {f: buf(fshape[f][0]) for f in FUSED}
-        v_in = outs["qkv"][:, shapes["q"][0] + shapes["k"][0]:]
-        up_in = outs["gate_up"][:, shapes["gate"][0]:]
-    else:
-        outs = {f: buf(stack[0][f].table.out if f in ("qkv", "gate_up") else hid) for f in FUSED}
-        v_in = outs["qkv"][:, 2 * outs["qkv"].shape[1] // 3:]
-        up_in = outs["gate_up"][:, outs["gate_up"].shape[1] // 2:]
-
-    def linear(lin, name, X, Y):
-        if world == 1:
-            base, table, _, _ = lin
-            sbmm_forward(X, plan, base, table, Y=Y, workspace=ws)
-        else:
-            Yl = lin.forward(X, plan)
-            Y.copy_(Yl) if Yl.data_ptr() != Y.data_ptr() else None
-
-    step_order = [("qkv", "h"), ("o", "v"), ("gate_up", "h"), ("down", "up")]
-
-    def step():
-        h = x_in
-        for lin in stack:
-            src = {"h": h, "v": v_in, "up": up_in}
-            for f, s_ in step_order:
-                linear(lin[f], f, src[s_], outs[f])
-                src = {"h": h, "v": v_in, "up": up_in}
-            h = outs["down"]
-        return h
-
+    assert plan.t_pf == 0  # 2 tokens per delta: pure decode plan
+    bufs = st.buffers(T_TOKENS)
     stream = torch.cuda.current_stream()
-    # eager warm-up (sets kernel attributes, checks the path), then capture
-    step()
+
+    st.step(plan, bufs)  # eager warm-up (sets kernel attributes, NCCL communicators)
     torch.cuda.synchronize()
     graph = None
     if not args.no_graph:
-        s = torch.cuda.Stream()
-        s.wait_stream(stream)
-        with torch.cuda.stream(s):
-            step()
-        stream.wait_stream(s)
+        s_ = torch.cuda.Stream()
+        s_.wait_stream(stream)
+        with torch.cuda.stream(s_):
+            st.step(plan, bufs)
+        stream.wait_stream(s_)
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            step()
+            st.step(plan, bufs)
         torch.cuda.synchronize()
 
     def run_step():
         if graph is not None:
             graph.replay()
         else:
-            step()
+            st.step(plan, bufs)
 
     for _ in range(args.warmup):
         run_step()
@@ -349,44 +315,42 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
-    # ---- per-launch kernel durations (eager, events between consecutive launches on the stream)
-    lin_bytes = {n: linear_algorithmic_bytes(o, i, BITS, D_DELTAS, T_TOKENS) for n, (o, i) in shapes.items()}
-    f_bytes = {f: sum(lin_bytes[m] for m in ms) - (len(ms) - 1) * (2 * T_TOKENS * fshape[f][1] + 4 * T_TOKENS)
-               for f, ms in FUSED.items()}  # the shared input x is read once per fused launch
-    if world > 1:
-        f_bytes = {n: b // world for n, b in f_bytes.items()}
-    evs = []
+    # ---- per-launch kernel durations: eager step with events around every fused launch (the
+    # events bracket the kernel(s) of one linear on the launching stream; TP adds the all-reduce
+    # of o/down, which is excluded by bracketing sbmm_forward only)
+    lin_bytes = st.launch_bytes(T_TOKENS, D_DELTAS)
+    evs, order = [], []
+    h = bufs["x"]
     torch.cuda.synchronize()
-    h = x_in
-    order = []
-    for lin in stack:
-        src = {"h": h, "v": v_in, "up": up_in}
-        for f, s_ in step_order:
+    from paper_2312_05215_b200.engine import sbmm_forward
+    for lin in st.stack:
+        src = {"h": h, "v": bufs["v"], "up": bufs["up"]}
+        for f, s_ in STEP_ORDER:
             a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a_.record(stream)
-            linear(lin[f], f, src[s_], outs[f])
+            sbmm_forward(src[s_], plan, lin[f].base, lin[f].table, Y=bufs[f], workspace=st.ws)
             b_.record(stream)
             evs.append((a_, b_))
             order.append(f)
-        h = outs["down"]
+        h = bufs["down"]
     torch.cuda.synchronize()
     durs = np.array([a_.elapsed_time(b_) for a_, b_ in evs])  # ms
     per_name = {}
     for n, d in zip(order, durs):
         per_name.setdefault(n, []).append(d)
-    lin_bytes = f_bytes
     kern_bytes = sum(lin_bytes[n] for n in order)
     kern_ms = float(durs.sum())
     achieved = kern_bytes / (kern_ms * 1e-3) / 1e9
     peak, peak_kind = measured_peaks()
     step_bytes = args.layers * sum(lin_bytes.values())
     tokens_per_s = T_TOKENS / (ms * 1e-3)  # TP: the step serves T tokens across all ranks
+    traffic, traffic_alg = ncu_traffic() if world == 1 and args.layers == 32 else (None, None)
 
-    # ---- e2e through the public API: host X (pinned) -> plan on host -> H2D -> step -> D2H
+    # ---- e2e through the public API: pinned host X -> host plan (group_by_delta, dz_plan) ->
+    # H2D of X + plan -> step -> D2H of the step's output, all inside the timed region.
     e2e = None
     if not args.no_e2e:
-        # e2e through the public API: pinned host X -> host plan (group_by_delta, dz_plan) ->
-        # H2D of X + plan -> step -> D2H of the step's output, all inside the timed region.
+        hid = bufs["x"].shape[1]
         xh = torch.randn(T_TOKENS, hid).to(torch.bfloat16).pin_memory()
         yh = torch.empty(T_TOKENS, hid, dtype=torch.bfloat16).pin_memory()
         order_pin = torch.empty(plan.order.numel(), dtype=torch.int32).pin_memory()
@@ -398,11 +362,11 @@ def main():
             hp = Plan(ids, kinds, D_DELTAS, upload=False)
             order_pin[: hp.T].copy_(torch.from_numpy(hp.order_host))
             jobs_pin[: hp.jobs_bytes.size].copy_(torch.from_numpy(hp.jobs_bytes))
-            x_in.copy_(xh, non_blocking=True)
+            bufs["x"].copy_(xh, non_blocking=True)
             plan.order.copy_(order_pin, non_blocking=True)
             plan.jobs.copy_(jobs_pin, non_blocking=True)
             run_step()
-            yh.copy_(outs["down"], non_blocking=True)
+            yh.copy_(bufs["down"], non_blocking=True)
         f1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = f0.elapsed_time(f1) / args.steps
@@ -417,27 +381,28 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick:
-        v, wsec, desc = cpu_reference_sample()
-        cpu = {"value": v, "unit": "tokens/s", "cores": 1, "kind": "port",
-               "sample": desc + f" ({wsec:.1f} s of CPU work; numpy dequant is single-threaded)"}
+        ref = CpuReference()
+        v, wsec, desc = ref.sample()
+        ref.close()
+        cpu = {"value": v, "unit": "tokens/s", "cores": ref.cores, "kind": "port", "sample": desc}
 
     if rank == 0:
         line = {
-            "metric": "decode tokens/s (Llama-2-7B-shaped stack, 32 x 4-bit 2:4 deltas, batch 64)",
+            "metric": METRIC,
             "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random bf16 base, random reference-layout 4-bit 2:4 deltas uploaded via dz_repack_sparse)",
-            "config": {"workload": f"llama2-7b decoder stack, {args.layers} layers x 7 linears (q,k,v,o,gate,up,down; "
-                                   f"QKV and gate/up row-fused into one launch each), "
-                                   f"D={D_DELTAS} 4-bit 2:4 deltas (gs=128), T={T_TOKENS} decode tokens, ids=perm(i%32)",
+            "config": {"workload": WORKLOAD.format(layers=args.layers),
                        "global_batch": T_TOKENS, "parallelism": f"tp{world}" if world > 1 else "single",
-                       "l2": "inputs > L2 (97.5 GB streamed per step)", "cuda_graph": graph is not None,
-                       "step_bytes": step_bytes},
+                       "l2": "inputs > L2 (97.5 GB streamed per step at N=1)", "cuda_graph": graph is not None,
+                       "step_bytes_rank0": step_bytes},
             "gpu_launches": len(order) * args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "k_sbmm (fused base GEMM + SBMM), all 4 x layers launches of one step (QKV, o, gate/up, down)",
+                         "traffic": traffic, "traffic_algorithmic": traffic_alg, "peak_kind": peak_kind,
+                         "kernel": "k_sbmm (fused base GEMM + SBMM), all 4 x layers launches of one step (QKV, o, "
+                                   "gate/up, down); achieved = algorithmic bytes / summed launch time; traffic = "
+                                   "mean DRAM bytes per launch from ncu --set full (profiles/r01_ncu_full_v10.md)",
                          "per_launch_us": {n: float(np.mean(v) * 1e3) for n, v in per_name.items()},
                          "step_GBps": step_bytes / (ms * 1e-3) / 1e9},
             "clocks": clocks,

@@ -23,6 +23,8 @@ LLAMA_SHAPES = {
     "7b": dict(hidden=4096, inter=11008, layers=32, kv=4096),
     "13b": dict(hidden=5120, inter=13824, layers=40, kv=5120),
     "70b": dict(hidden=8192, inter=28672, layers=80, kv=1024),
+    # test-sized Llama layer: GQA-style kv, intermediate of 11 native blocks (uneven at TP 2/4)
+    "tiny": dict(hidden=1024, inter=1408, layers=2, kv=512),
 }
 
 
