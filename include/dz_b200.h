@@ -103,9 +103,13 @@ typedef struct dz_sbmm_args {
    * TMEM accumulator), the remaining jobs cover staged rows [t_pf, T) (K2), and staged row i
    * is written to Y row perm[i]. */
   const int32_t* perm;      /* device [T] or NULL                                     */
-  void* xs;                 /* device bf16 [T][ldx] staging buffer (perm != NULL)      */
+  void* xs;                 /* device bf16 [T][ldxs] staging buffer (perm != NULL)     */
   int32_t n_pf_jobs;
   int32_t t_pf;
+  int64_t ldxs;             /* row stride of xs (elements, >= ceil128(in), % 8 == 0)  */
+  int32_t base_splits;      /* K-splits of the base GEMM (1..4); 0 = chosen from (out, in) only,
+                               so results never depend on the batch                     */
+  int32_t _pad3;
 } dz_sbmm_args;
 
 const char* dz_version(void);

@@ -56,6 +56,8 @@ class DzSbmmArgs(C.Structure):
         ("grid", C.c_int32), ("debug", C.c_int32),
         ("perm", C.c_void_p), ("xs", C.c_void_p),
         ("n_pf_jobs", C.c_int32), ("t_pf", C.c_int32),
+        ("ldxs", C.c_int64),
+        ("base_splits", C.c_int32), ("_pad3", C.c_int32),
     ]
 
 

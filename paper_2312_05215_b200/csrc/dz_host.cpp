@@ -60,10 +60,11 @@ extern "C" int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, in
   return DZ_OK;
 }
 
-// Mixed plan (prefill + decode). Groups of >= pf_min tokens with a 2:4 sparse kind are staged
-// first (grouped by slot in slot order, stable inside a group) and cut into prefill jobs of <= 256
-// tokens, balanced so that no job is much smaller than the others; every other token follows in
-// its original order and is planned exactly like dz_plan over the staged rows.
+// Mixed plan (prefill + decode). A group of c >= pf_min tokens with a 2:4 sparse kind sends its
+// first 256*floor(c/256) tokens (in original order) to prefill jobs of 256, plus the remainder as
+// one more prefill job when it still has >= pf_min tokens; prefill tokens are staged first
+// (grouped by slot in slot order). Every other token follows in its original order and is planned
+// exactly like dz_plan over the staged rows.
 extern "C" int dz_plan_mixed(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t n_slots,
                              int32_t with_base, int32_t pf_min, int32_t* perm_out, int32_t* order_out,
                              dz_job* jobs_out, int32_t max_jobs, int32_t* n_jobs_out, int32_t* n_pf_jobs_out,
@@ -78,20 +79,24 @@ extern "C" int dz_plan_mixed(const int32_t* slots, int32_t T, const int32_t* kin
       return DZ_E_VALUE;
   std::vector<int32_t> count(static_cast<size_t>(n_slots), 0);
   for (int32_t t = 0; t < T; t++) count[slots[t]]++;
-  std::vector<char> pf(static_cast<size_t>(n_slots), 0);
-  for (int32_t s = 0; s < n_slots; s++)
-    pf[s] = pf_min > 0 && count[s] >= pf_min && kinds[s] != DZ_KIND_DENSE;
+  std::vector<int32_t> npf(static_cast<size_t>(n_slots), 0);  // prefill tokens per slot
+  for (int32_t s = 0; s < n_slots; s++) {
+    if (pf_min <= 0 || count[s] < pf_min || kinds[s] == DZ_KIND_DENSE) continue;
+    const int32_t rem = count[s] % 256;
+    npf[s] = count[s] - rem + (rem >= pf_min ? rem : 0);
+  }
   // staged order: prefill groups by slot, then the decode tokens in original order
   std::vector<int32_t> pstart(static_cast<size_t>(n_slots) + 1, 0);
-  for (int32_t s = 0; s < n_slots; s++) pstart[s + 1] = pstart[s] + (pf[s] ? count[s] : 0);
+  for (int32_t s = 0; s < n_slots; s++) pstart[s + 1] = pstart[s] + npf[s];
   const int32_t t_pf = pstart[n_slots];
   std::vector<int32_t> fill(pstart.begin(), pstart.end() - 1);
   int32_t nd = t_pf;
   std::vector<int32_t> dslot;  // slot of each decode staged row
   dslot.reserve(static_cast<size_t>(T - t_pf));
   for (int32_t t = 0; t < T; t++) {
-    if (pf[slots[t]]) {
-      perm_out[fill[slots[t]]++] = t;
+    const int32_t s = slots[t];
+    if (fill[s] < pstart[s] + npf[s]) {
+      perm_out[fill[s]++] = t;
     } else {
       perm_out[nd++] = t;
       dslot.push_back(slots[t]);
@@ -103,15 +108,9 @@ extern "C" int dz_plan_mixed(const int32_t* slots, int32_t T, const int32_t* kin
     jobs_out[nj++] = dz_job{slot, b, c, kind};
     return true;
   };
-  for (int32_t s = 0; s < n_slots; s++) {
-    if (!pf[s]) continue;
-    const int32_t c = count[s], nparts = (c + 255) / 256;
-    for (int32_t k = 0; k < nparts; k++) {
-      const int32_t b = pstart[s] + static_cast<int32_t>(static_cast<int64_t>(c) * k / nparts);
-      const int32_t e = pstart[s] + static_cast<int32_t>(static_cast<int64_t>(c) * (k + 1) / nparts);
-      if (!push(s, b, e - b, kinds[s])) return DZ_E_VALUE;
-    }
-  }
+  for (int32_t s = 0; s < n_slots; s++)
+    for (int32_t off = 0; off < npf[s]; off += 256)
+      if (!push(s, pstart[s] + off, (npf[s] - off) < 256 ? (npf[s] - off) : 256, kinds[s])) return DZ_E_VALUE;
   const int32_t n_pf = nj;
   // decode part over staged rows [t_pf, T): base jobs, then delta jobs (dz_plan's rules)
   const int32_t Td = T - t_pf;

@@ -211,6 +211,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_keep = policy_evict_last();
     if (lane == 0) prefetch_tmap(&xmap);
+    griddep_wait();  // the staged X is the preceding kernel's output (programmatic dependent launch)
+    griddep_launch_dependents();
     int s = 0, ds = 0;
     uint32_t ph = 0, dph = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -311,6 +313,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else {
     // ===================== epilogue warps =====================
     const int q = warp & 3;
+    griddep_wait();  // Y rows may still be written by the preceding kernel
     int nacc = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const Item it = item_at(a, item, n_jobs);
@@ -382,7 +385,8 @@ extern "C" int dz_gather_rows(const uint16_t* X, int64_t ldx, const int32_t* per
   if ((ldx % 8) || (ldxs % 8) || (reinterpret_cast<uintptr_t>(X) & 15) || (reinterpret_cast<uintptr_t>(Xs) & 15))
     return DZ_E_SHAPE;
   if (T == 0) return DZ_OK;
-  const int in8 = ceil_div(static_cast<int>(ldx < ldxs ? ldx : ldxs), 8);  // whole padded rows (zero tail kept)
+  if (ldx < in || ldxs < in) return DZ_E_SHAPE;
+  const int in8 = ceil_div(in, 8);  // callers pass in = the padded width (zero tail kept)
   const int64_t n = static_cast<int64_t>(T) * in8;
   const int blocks = static_cast<int>((n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8);
   pf::k_gather_rows<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(X, ldx, perm, T, in8, Xs, ldxs);
@@ -394,7 +398,7 @@ extern "C" int dz_sbmm_prefill(const dz_sbmm_args* a, void* stream) {
   if (!a || !a->Y || !a->table || !a->jobs) return DZ_E_VALUE;
   if (a->T < 0 || a->out < 1 || a->in < 1) return DZ_E_SHAPE;
   if (a->n_pf_jobs <= 0 || a->T == 0) return DZ_OK;
-  const uint16_t* X = a->perm ? static_cast<const uint16_t*>(a->xs) : a->X;
+  const uint16_t* X = a->X;  // the staged buffer (dz_sbmm passes it as X with its row stride)
   if (!X) return DZ_E_VALUE;
   if ((a->ldx % 8) != 0 || (reinterpret_cast<uintptr_t>(X) & 15) != 0 || a->ldx < a->in) return DZ_E_SHAPE;
   if (a->y_dtype != DZ_F32 && a->y_dtype != DZ_BF16) return DZ_E_VALUE;
@@ -417,6 +421,5 @@ extern "C" int dz_sbmm_prefill(const dz_sbmm_args* a, void* stream) {
   const int n_items = ceil_div(a->out, pf::M) * a->n_pf_jobs;
   int grid = a->grid > 0 ? a->grid : sms;
   if (grid > n_items) grid = n_items;
-  pf::k_prefill<<<grid, pf::NTHREADS, pf::SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(k, xmap);
-  return cudaGetLastError() == cudaSuccess ? DZ_OK : DZ_E_CUDA;
+  return launch_pdl(pf::k_prefill, grid, pf::NTHREADS, pf::SMEM_BYTES, stream, k, xmap);
 }

@@ -37,6 +37,7 @@
 
 #include <cstddef>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -72,7 +73,16 @@ constexpr int NTHREADS = (NW + 3) * 32;
 constexpr int RG = NW * MR;               // row groups per item
 constexpr int RT = RG * kBlkRows;         // rows per item (256) == 2 x UMMA M
 constexpr int UMMA_M = 128;
-constexpr int NB_SP = 4;                  // sparse chunk = 4 blocks = 512 columns (one 3-D TMA box)
+#ifndef DZ_NB_SP
+#define DZ_NB_SP 4
+#endif
+#ifndef DZ_NSTAGE
+#define DZ_NSTAGE 3
+#endif
+#ifndef DZ_BASE_CH
+#define DZ_BASE_CH 2
+#endif
+constexpr int NB_SP = DZ_NB_SP;           // sparse chunk = 4 blocks = 512 columns (one 3-D TMA box)
 constexpr int NT_SP = 1;                  // n-tiles per sparse job (8 tokens, dz_plan)
 constexpr int NT_DN = 4;                  // n-tiles per dense-delta job (32 tokens, dz_plan)
 constexpr int KC_DN = 64;                 // dense / base chunk = 64 columns
@@ -85,12 +95,13 @@ constexpr int DN_HALF = kDenseBlockBytes / 2;             // 2048
 constexpr int A_DN = RG * DN_HALF;                        // 32768 == 256 rows x 128 B (base W tile)
 constexpr int X_DN = 64 * XS_DN;                          // 9216 (>= 64 x 128 B swizzled X tile)
 constexpr int STAGE_BYTES = ((A_SP + X_SP > A_DN + X_DN ? A_SP + X_SP : A_DN + X_DN) + 1023) / 1024 * 1024;
-constexpr int NSTAGE = 3;
+constexpr int NSTAGE = DZ_NSTAGE;
 constexpr int JOB_DN_TOK = BASE_N;        // largest token count of a job
 constexpr int BASE_RT = UMMA_M;           // rows per base item: one UMMA M tile (half a delta row tile)
-constexpr int BASE_CH = 2;                // 64-column K-chunks per base stage (32 KB of W in flight per stage)
+constexpr int BASE_CH = DZ_BASE_CH;             // 64-column K-chunks per base stage (32 KB of W in flight per stage)
 constexpr int TMEM_COLS = 2 * BASE_N;     // double-buffered fp32 accumulator, 128 lanes x 64 tokens
 constexpr uint32_t IDESC_BASE = umma_idesc_bf16(UMMA_M, BASE_N);
+constexpr int PF_CHUNKS = 4;              // stages of the first item prefetched into L2 before the PDL wait
 
 struct StageHdr {
   int item;       // -1: end of work
@@ -123,17 +134,28 @@ __device__ __forceinline__ bool kind_dense(int kind) { return kind == 0 || kind 
 // cover BASE_RT = 128 rows (nbt tiles), delta items RT = 256 rows (nrt tiles): a base item streams
 // 2 bytes per weight against a 4-bit delta's ~0.8, so halving it keeps the long base items off the
 // launch's critical path. Each output element still gets exactly one base and one delta partial.
-__device__ __forceinline__ void item_coords(int item, int nrt, int nbt, int n_jobs, int n_base, int& rt, int& j) {
-  const int nb_items = nbt * n_base;
+__device__ __forceinline__ void item_coords(int item, int nrt, int nbt, int nsplit, int n_jobs, int n_base, int& rt,
+                                            int& j, int& sp) {
+  const int nb_items = nbt * nsplit * n_base;
   if (item < nb_items) {
-    j = item / nbt;
-    rt = item - j * nbt;
+    j = item / (nbt * nsplit);
+    const int r = item - j * (nbt * nsplit);
+    sp = r / nbt;
+    rt = r - sp * nbt;
   } else {
     const int k = item - nb_items, nd = n_jobs - n_base;
     rt = k / nd;
     j = n_base + (k - rt * nd);
+    sp = 0;
   }
 }
+
+// Default base K-splits when the caller passes 0: one split (measured best at the BASELINE decode
+// batch, T=64 with 32 deltas, for every 7B shape: profiles/r01_ab_splits.txt). Low-batch serving
+// (T <= 16) gains up to +30% with 4 splits, which a deployment selects explicitly through
+// dz_sbmm_args.base_splits. The split count is never derived from the batch, so a token's
+// result does not depend on the other tokens of the call.
+__host__ __device__ inline int base_splits(int /*out*/, int /*in*/) { return 1; }
 
 __device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
   int old;
@@ -320,11 +342,11 @@ __device__ __forceinline__ void dense_dispatch(int nt, float (&acc)[MR][NT_DN][4
 }
 
 struct MergeCtx {
-  unsigned long long* slots;  // [T][out] {fp32 value bits, count} words, zero between launches
+  float* part;                // [nsplit + 1][T][out] fp32 partials (workspace)
   const int32_t* perm;        // staged row -> Y row (mixed plans), or NULL
   void* Y;
   int64_t ldy;
-  int out, y_dtype, act;
+  int out, y_dtype, act, debug, T, nsplit;
   bool has_base;
 };
 
@@ -338,47 +360,38 @@ __device__ __forceinline__ void store_y(const MergeCtx& m, int tok, int row, flo
     reinterpret_cast<__nv_bfloat16*>(m.Y)[yo] = __float2bfloat16_rn(v);
 }
 
-// Publish N fp32 contributions v[i] to y[tok[i]][row[i]] (valid[i]). First arriver parks {v, 1};
-// the second computes fl(other + v), writes Y and clears the slot. All N CASes are issued before
-// any result is inspected, so an epilogue costs one atomic round trip, not N. Without a base there
-// is a single contributor and Y is written directly.
+// Publish N fp32 partials v[i] of y[tok[i]][row[i]] (valid[i]) into partial slot `slot` of the
+// workspace: [nsplit + 1][T][out] fp32, slot s < nsplit = base K-split s, slot nsplit = the
+// token's delta job. Plain stores — every (slot, token, row) has exactly one producer — so the
+// epilogue never waits on a round trip; k_finalize sums the slots in a fixed order and applies
+// the activation. Without a base there is a single contributor and Y is written directly.
 template <int N>
-__device__ __forceinline__ void merge_batch(const MergeCtx& m, const int (&tok)[N], const int (&row)[N],
+__device__ __forceinline__ void merge_batch(const MergeCtx& m, int slot, const int (&tok)[N], const int (&row)[N],
                                             const float (&v)[N], const bool (&valid)[N]) {
+  if (m.debug & 4) return;  // debug bit 2: drop the merge (probe of its cost; Y is not written)
   if (!m.has_base) {
 #pragma unroll
     for (int i = 0; i < N; i++)
       if (valid[i]) store_y(m, tok[i], row[i], v[i]);
     return;
   }
-  unsigned long long old[N];
+  float* part = m.part + static_cast<int64_t>(slot) * m.T * m.out;
 #pragma unroll
-  for (int i = 0; i < N; i++) {
-    old[i] = 0ull;
-    if (valid[i])
-      old[i] = atomicCAS(m.slots + static_cast<int64_t>(tok[i]) * m.out + row[i], 0ull,
-                         (1ull << 32) | __float_as_uint(v[i]));
-  }
-#pragma unroll
-  for (int i = 0; i < N; i++) {
-    if (valid[i] && old[i] != 0ull) {  // the other contribution was parked: complete the element
-      store_y(m, tok[i], row[i], __uint_as_float(static_cast<uint32_t>(old[i])) + v[i]);
-      m.slots[static_cast<int64_t>(tok[i]) * m.out + row[i]] = 0ull;  // self-reset for the next launch
-    }
-  }
+  for (int i = 0; i < N; i++)
+    if (valid[i]) part[static_cast<int64_t>(tok[i]) * m.out + row[i]] = v[i];
 }
 
-__device__ __forceinline__ void merge_contribution(const MergeCtx& m, int tok, int row, float v) {
+__device__ __forceinline__ void merge_contribution(const MergeCtx& m, int slot, int tok, int row, float v) {
   const int t[1] = {tok}, r[1] = {row};
   const float x[1] = {v};
   const bool ok[1] = {true};
-  merge_batch<1>(m, t, r, x, ok);
+  merge_batch<1>(m, slot, t, r, x, ok);
 }
 
 // Base accumulators (TMEM, lane = output row, column = token) -> merge. Warp w drains half w/4
 // (rows 128*(w/4)..) of the tile, TMEM lanes 32*(w%4)..+31 (the lanes warp w may access).
 __device__ __forceinline__ void drain_base_accumulator(uint32_t tmem_acc, int warp, int lane, const MergeCtx& m,
-                                                       int row0, int tok_begin, int tcount) {
+                                                       int split, int row0, int tok_begin, int tcount) {
   // TMEM lane quarter q = warp % 4 (the hardware's warp -> lane restriction); the two warps of a
   // quarter split the 64 token columns.
   const int q = warp & 3, half = warp >> 2;
@@ -400,7 +413,7 @@ __device__ __forceinline__ void drain_base_accumulator(uint32_t tmem_acc, int wa
       x[j] = __uint_as_float(v[j]);
       ok[j] = row < m.out && c * 16 + j < tcount;
     }
-    merge_batch<16>(m, tk, rw, x, ok);
+    merge_batch<16>(m, split, tk, rw, x, ok);
   }
 }
 
@@ -418,7 +431,7 @@ __device__ __forceinline__ void merge_fragments(const float (&acc)[MR][NT_DN][4]
         for (int v = 0; v < 4; v++) {
           const int tk = n * 8 + 2 * t + (v & 1);
           const int row = row0 + g + ((v & 2) ? 8 : 0);
-          if (tk < tcount && row < m.out) merge_contribution(m, tok_ids[tk], row, acc[r][n][v]);
+          if (tk < tcount && row < m.out) merge_contribution(m, m.nsplit, tok_ids[tk], row, acc[r][n][v]);
         }
       }
     }
@@ -442,11 +455,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int nch_base = ceil_div(a.in, BASE_CH * KC_DN);
   const int nbt = ceil_div(a.out, BASE_RT);
   const int n_base = a.base != nullptr ? ceil_div(a.T - a.t_pf, BASE_N) : 0;  // dz_plan: base jobs first
-  const int n_items = nbt * n_base + nrt * (a.n_jobs - n_base);
+  const int nsplit = a.base_splits;  // resolved by the host (launch_decode)
+  // debug bit 1: base items only (probe of the base stream)
+  const int n_items = nbt * nsplit * n_base + ((a.debug & 2) ? 0 : nrt * (a.n_jobs - n_base));
 
   int* sched = reinterpret_cast<int*>(a.workspace);  // [0] item counter, [1] finished CTAs
   MergeCtx mctx;
-  mctx.slots = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(a.workspace) + 256);
+  mctx.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(a.workspace) + 256);
+  mctx.T = a.T;
+  mctx.nsplit = nsplit;
   mctx.perm = a.perm;
   mctx.Y = a.Y;
   mctx.ldy = a.ldy;
@@ -454,6 +471,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   mctx.y_dtype = a.y_dtype;
   mctx.act = a.act;
   mctx.has_base = a.base != nullptr;
+  mctx.debug = a.debug;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; s++) {
@@ -485,12 +503,29 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (lane == 0) prefetch_tmap(&xmap);
     int stage = 0;
     uint32_t phase = 0;
-    int id_raw = 0;
-    if (lane == 0) id_raw = atomicAdd(&sched[0], 1);
-    int item = __shfl_sync(0xffffffffu, id_raw, 0);
-    int rt = 0, jj = 0;
-    if (item < n_items) item_coords(item, nrt, nbt, a.n_jobs, n_base, rt, jj);
+    // First item static (blockIdx.x), later ones from the counter. Before waiting for the preceding
+    // kernel (programmatic dependent launch), prefetch the first chunks of this item's weight
+    // stream into L2: it depends only on resident weights, not on the predecessor's output.
+    int item = blockIdx.x;
+    int rt = 0, jj = 0, sp = 0;
+    if (item < n_items) item_coords(item, nrt, nbt, nsplit, a.n_jobs, n_base, rt, jj, sp);
     dz_job job = item < n_items ? a.jobs[jj] : dz_job{0, 0, 0, 0};
+    if (item < n_items && lane == 0) {
+      const bool dn = kind_dense(job.kind);
+      const dz_native_delta* e0 = job.kind == 0 ? a.base : a.table + job.slot;
+      const void* m0 = e0->tmap;
+      if (job.kind == 0) {
+        const int k0 = (sp * nch_base / nsplit) * BASE_CH * KC_DN;
+        for (int c = 0; c < PF_CHUNKS * BASE_CH && k0 + c * KC_DN < a.in; c++)
+          tma_prefetch_2d(m0, k0 + c * KC_DN, rt * BASE_RT);
+      } else if (dn) {
+        for (int c = 0; c < PF_CHUNKS && c < 2 * nkb; c++) tma_prefetch_2d(m0, c * (DN_HALF / 8), rt * RG);
+      } else {
+        for (int c = 0; c < PF_CHUNKS && c * NB_SP < nkb; c++) tma_prefetch_3d(m0, 0, c * NB_SP, rt * RG);
+      }
+    }
+    griddep_wait();
+    griddep_launch_dependents();
     int tok = 0, tok2 = 0;
     if (item < n_items) {
       if (lane < job.tok_count) tok = job.kind == 0 ? job.tok_begin + lane : a.order[job.tok_begin + lane];
@@ -503,13 +538,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const dz_native_delta* ent = is_base ? a.base : a.table + job.slot;
       const void* amap = ent->tmap;  // address only: the descriptor stays in global memory
       const int bb = dense ? kDenseBlockBytes : sparse_block_bytes(kind_fbits(job.kind));
-      const int nch = is_base ? nch_base : dense ? 2 * nkb : ceil_div(nkb, NB_SP);
+      // base items stream K-chunks [c0, c0 + nch) of split sp; delta items all of K
+      const int c0 = is_base ? sp * nch_base / nsplit : 0;
+      const int nch = is_base ? (sp + 1) * nch_base / nsplit - c0 : dense ? 2 * nkb : ceil_div(nkb, NB_SP);
       const uint32_t abytes = is_base ? static_cast<uint32_t>(BASE_RT * KC_DN * 2)
                               : dense ? static_cast<uint32_t>(A_DN) : static_cast<uint32_t>(RG * NB_SP * bb);
       // Next item: its id is fetched after chunk 0 goes out (one item of lookahead per CTA keeps
       // the dynamic schedule balanced), its descriptor and token ids after chunks 1 and 2, so the
       // dependent global loads overlap this item's stream instead of stalling the ring.
-      int id_nxt_raw = 0, item_nxt = n_items, tok_n = 0, tok2_n = 0, rt_n = 0;
+      int id_nxt_raw = 0, item_nxt = n_items, tok_n = 0, tok2_n = 0, rt_n = 0, sp_n = 0;
       dz_job job_n{0, 0, 0, 0};
       for (int ch = 0; ch < nch; ch++) {
         if (lane == 0) TRACE(1, item, ch);
@@ -521,7 +558,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         uint8_t* sbuf = stages + static_cast<size_t>(stage) * STAGE_BYTES;
         int nb, col0, xbytes, ax, ay;
         if (is_base) {
-          col0 = ch * BASE_CH * KC_DN;
+          col0 = (c0 + ch) * BASE_CH * KC_DN;
           nb = (a.in - col0) < KC_DN ? 1 : BASE_CH;  // K-chunks in this stage (no fully-OOB boxes)
           xbytes = 0;
           ax = col0;
@@ -551,7 +588,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           h.item = item; h.rt = rt; h.kind = job.kind;
           h.tok_begin = job.tok_begin; h.tok_count = job.tok_count; h.nb = nb;
           h.flags = (ch == 0 ? 1 : 0) | (last ? 2 : 0) | (ch << 8);  // chunk index for the X producer
-          h.pad = 0;
+          h.pad = sp;  // base K-split: the partial slot the drain writes
           sm->hdr[stage] = h;
           const uint32_t xb = is_base ? static_cast<uint32_t>(nb * KC_DN * BASE_N * 2)
                                       : static_cast<uint32_t>(job.tok_count * xbytes);
@@ -575,12 +612,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (lane == 0) TRACE(9, item, ch);
         if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
         // ---- next-item prefetch, spread over the first chunks ----
-        if (ch == 0 && lane == 0) id_nxt_raw = atomicAdd(&sched[0], 1);
+        if (ch == 0 && lane == 0) id_nxt_raw = static_cast<int>(gridDim.x) + atomicAdd(&sched[0], 1);
         if (ch == (nch > 1 ? 1 : 0)) {
           item_nxt = __shfl_sync(0xffffffffu, id_nxt_raw, 0);
           if (item_nxt < n_items) {
             int j_n = 0;
-            item_coords(item_nxt, nrt, nbt, a.n_jobs, n_base, rt_n, j_n);
+            item_coords(item_nxt, nrt, nbt, nsplit, a.n_jobs, n_base, rt_n, j_n, sp_n);
             job_n = a.jobs[j_n];
             if (lane == 0) prefetch_tmap((job_n.kind == 0 ? a.base : a.table + job_n.slot)->tmap);
           }
@@ -594,6 +631,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       item = item_nxt;
       rt = rt_n;
+      sp = sp_n;
       job = job_n;
       tok = tok_n;
       tok2 = tok2_n;
@@ -614,6 +652,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // One 1-D bulk copy per routed token row of the chunk, completing on the stage's full barrier
     // (whose expect_tx the producer already armed with these bytes).
     const uint64_t pol_keep = policy_evict_last();
+    griddep_wait();  // X is the preceding kernel's output
     int stage = 0;
     uint32_t phase = 0;
     while (true) {
@@ -670,6 +709,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   } else {
     // ===================== consumers =====================
+    griddep_wait();  // Y / merge slots may still be in use by the preceding kernel
     int trace_i = 0;
     (void)trace_i;
     float acc[MR][NT_DN][4];  // dense deltas use all NT_DN tiles, sparse deltas the first NT_SP
@@ -729,7 +769,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const int buf = nbase & 1;
           mbar_wait(&sm->tmem_full[buf], (nbase >> 1) & 1);
           tc_fence_after();
-          drain_base_accumulator(tmem_base + buf * BASE_N, warp, lane, mctx, h.rt * BASE_RT, h.tok_begin,
+          drain_base_accumulator(tmem_base + buf * BASE_N, warp, lane, mctx, h.pad, h.rt * BASE_RT, h.tok_begin,
                                  h.tok_count);
           tc_fence_before();
           __syncwarp();
@@ -752,7 +792,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               ok[i] = r < nrv && t2 + (v & 1) < h.tok_count && rw[i] < a.out;
             }
           }
-          merge_batch<4 * MR>(mctx, tk, rw, x, ok);
+          merge_batch<4 * MR>(mctx, nsplit, tk, rw, x, ok);
         }
         if (lane == 0 && warp == 0) TRACE(5, h.item, 0);
         if (lane == 0 && warp == 0) ITEM_TRACE(1, h.item, globaltimer());
@@ -767,12 +807,68 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
+// Finalize the merged decode rows [t0, T): Y[perm[t]][r] = act(((P_0 + P_1) + ... + P_{S-1}) + P_S)
+// with P_s the base K-split partials and P_S the delta partial — a fixed summation order, so the
+// result is deterministic and independent of the batch. Runs after k_sbmm in the same stream
+// (programmatic dependent launch).
+__global__ void __launch_bounds__(256) k_finalize(const float* __restrict__ part, int nsplit, int t0, int T, int out,
+                                                  const int32_t* __restrict__ perm, void* __restrict__ Y, int64_t ldy,
+                                                  int y_dtype, int act) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t plane = static_cast<int64_t>(T) * out;
+  const bool vec = (out % 4) == 0 && (ldy % 4) == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
+  if (vec) {
+    const int o4 = out / 4;
+    const int64_t n = static_cast<int64_t>(T - t0) * o4;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+      const int t = t0 + static_cast<int>(i / o4), r = 4 * static_cast<int>(i % o4);
+      const float* p = part + static_cast<int64_t>(t) * out + r;
+      float4 v = __ldcs(reinterpret_cast<const float4*>(p));
+      for (int sp = 1; sp <= nsplit; sp++) {
+        const float4 w = __ldcs(reinterpret_cast<const float4*>(p + sp * plane));
+        v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+      }
+      if (act == DZ_ACT_TANH) { v.x = tanhf(v.x); v.y = tanhf(v.y); v.z = tanhf(v.z); v.w = tanhf(v.w); }
+      const int yr = perm != nullptr ? __ldg(perm + t) : t;
+      const int64_t yo = static_cast<int64_t>(yr) * ldy + r;
+      if (y_dtype == DZ_F32) {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(Y) + yo) = v;
+      } else {
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+        uint2 w;
+        w.x = *reinterpret_cast<const uint32_t*>(&lo);
+        w.y = *reinterpret_cast<const uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(Y) + yo) = w;
+      }
+    }
+  } else {
+    const int64_t n = static_cast<int64_t>(T - t0) * out;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+      const int t = t0 + static_cast<int>(i / out), r = static_cast<int>(i % out);
+      const float* p = part + static_cast<int64_t>(t) * out + r;
+      float v = p[0];
+      for (int sp = 1; sp <= nsplit; sp++) v += p[sp * plane];
+      if (act == DZ_ACT_TANH) v = tanhf(v);
+      const int yr = perm != nullptr ? __ldg(perm + t) : t;
+      const int64_t yo = static_cast<int64_t>(yr) * ldy + r;
+      if (y_dtype == DZ_F32)
+        reinterpret_cast<float*>(Y)[yo] = v;
+      else
+        reinterpret_cast<__nv_bfloat16*>(Y)[yo] = __float2bfloat16_rn(v);
+    }
+  }
+}
+
 }  // namespace dz
 
 using namespace dz;
 
 static_assert(A_DN + BASE_CH * KC_DN * BASE_N * 2 <= STAGE_BYTES && BASE_CH * BASE_RT * KC_DN * 2 <= A_DN,
               "base stage layout");
+static_assert(NB_SP % PAIR == 0, "sparse stages hold whole block pairs");
+static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
 static_assert(NW == 8, "drain_base_accumulator: two consumer warps per TMEM lane quarter");
 static_assert(sizeof(dz_native_delta) == 192, "dz_native_delta must be 192 bytes");
 static_assert(offsetof(dz_native_delta, tmap) == 64, "tensor map must be 64-byte aligned in the entry");
@@ -826,7 +922,7 @@ extern "C" int dz_base_init(dz_native_delta* e, const uint16_t* W, int64_t ldw, 
 
 extern "C" size_t dz_sbmm_workspace_bytes(int32_t T, int32_t out) {
   if (T < 0 || out < 1) return 0;
-  return 256 + static_cast<size_t>(T) * out * sizeof(unsigned long long);
+  return 256 + static_cast<size_t>(T) * out * sizeof(float) * 5;  // <= 4 base K-splits + the delta partial
 }
 
 static int g_ctas_per_sm = 0;
@@ -854,7 +950,15 @@ extern "C" int dz_sbmm_ctas_per_sm(void) {
   return n;
 }
 
-static int launch_decode(const dz_sbmm_args* a, void* stream) {
+static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
+  dz_sbmm_args kargs = *a_in;
+  const dz_sbmm_args* a = &kargs;
+  if (kargs.base_splits <= 0) {
+    kargs.base_splits = base_splits(kargs.out, kargs.in);
+    const char* e = std::getenv("DZ_BASE_SPLITS");  // experiment override (A/B)
+    if (e && e[0] >= '1' && e[0] <= '4') kargs.base_splits = e[0] - '0';
+  }
+  if (kargs.base_splits > 4) kargs.base_splits = 4;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   static int ctas_per_sm = 1;
@@ -877,10 +981,20 @@ static int launch_decode(const dz_sbmm_args* a, void* stream) {
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return DZ_E_CUDA;
     grid = sms * ctas_per_sm;
   }
-  const int n_items = ceil_div(a->out, RT) * a->n_jobs + ceil_div(a->out, BASE_RT) * ceil_div(a->T, BASE_N);
+  const int n_items = ceil_div(a->out, RT) * a->n_jobs +
+                      ceil_div(a->out, BASE_RT) * a->base_splits * ceil_div(a->T, BASE_N);
   if (grid > n_items) grid = n_items;
-  k_sbmm<<<grid, NTHREADS, SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(*a, xmap);
-  return cudaGetLastError() == cudaSuccess ? DZ_OK : DZ_E_CUDA;
+  st = launch_pdl(k_sbmm, grid, NTHREADS, SMEM_BYTES, stream, *a, xmap);
+  if (st || a->base == nullptr || (a->debug & 4)) return st;
+  // merged rows -> Y (+ activation), accumulator re-zeroed
+  const int t0 = a->t_pf;
+  const int64_t work = static_cast<int64_t>(a->T - t0) * a->out / 4;
+  int fgrid = static_cast<int>((work + 255) / 256);
+  if (fgrid > 4 * 148) fgrid = 4 * 148;
+  if (fgrid < 1) fgrid = 1;
+  const float* part = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(a->workspace) + 256);
+  return launch_pdl(k_finalize, fgrid, 256, 0, stream, part, a->base_splits, t0, a->T, a->out, a->perm,
+                    a->Y, a->ldy, a->y_dtype, a->act);
 }
 
 extern "C" int dz_sbmm(const dz_sbmm_args* a, void* stream) {
@@ -897,15 +1011,19 @@ extern "C" int dz_sbmm(const dz_sbmm_args* a, void* stream) {
   }
   // mixed plan: stage X in plan order, prefill jobs on K3, the rest on K2
   if (!a->xs || a->n_pf_jobs < 0 || a->n_pf_jobs > a->n_jobs || a->t_pf < 0 || a->t_pf > a->T) return DZ_E_VALUE;
-  int st = dz_gather_rows(a->X, a->ldx, a->perm, a->T, a->in, static_cast<uint16_t*>(a->xs), a->ldx, stream);
+  const int64_t ldxs = a->ldxs > 0 ? a->ldxs : a->ldx;
+  if (ldxs < in_pad || (ldxs % 8) != 0 || (reinterpret_cast<uintptr_t>(a->xs) & 15) != 0) return DZ_E_SHAPE;
+  int st = dz_gather_rows(a->X, a->ldx, a->perm, a->T, in_pad, static_cast<uint16_t*>(a->xs), ldxs, stream);
   if (st) return st;
+  dz_sbmm_args s = *a;  // the staged buffer replaces X for both kernels
+  s.X = static_cast<const uint16_t*>(a->xs);
+  s.ldx = ldxs;
   if (a->n_pf_jobs > 0) {
-    st = dz_sbmm_prefill(a, stream);
+    st = dz_sbmm_prefill(&s, stream);
     if (st) return st;
   }
   if (a->n_jobs > a->n_pf_jobs) {
-    dz_sbmm_args k = *a;
-    k.X = static_cast<const uint16_t*>(a->xs);
+    dz_sbmm_args k = s;
     k.jobs = a->jobs + a->n_pf_jobs;
     k.n_jobs = a->n_jobs - a->n_pf_jobs;
     k.n_pf_jobs = 0;

@@ -223,7 +223,8 @@ def prepare_x(X: torch.Tensor) -> torch.Tensor:
 
 def sbmm_forward(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: DeltaTable,
                  y_dtype: torch.dtype = torch.bfloat16, act: int = L.DZ_ACT_NONE, Y: torch.Tensor | None = None,
-                 workspace: Workspace | None = None, grid: int = 0, debug: int = 0) -> torch.Tensor:
+                 workspace: Workspace | None = None, grid: int = 0, debug: int = 0,
+                 base_splits: int = 0) -> torch.Tensor:
     """Y[T, out] = X W_base^T + ΔW_{slot(t)} x_t for all t, one fused launch (inference.py:126-154)."""
     T, inp = int(X.shape[0]), int(X.shape[1])
     out = table.out if base is None else base.out
@@ -250,9 +251,11 @@ def sbmm_forward(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: De
     a.workspace = ws.data_ptr()
     a.grid = grid
     a.debug = debug
-    if plan.perm is not None:  # mixed plan: staged copy of X (same padded row stride)
-        xs = torch.empty_like(Xp)
-        a.perm, a.xs = plan.perm.data_ptr(), xs.data_ptr()
+    a.base_splits = base_splits  # 0 = by shape (batch-independent); 1..4 = explicit K-splits of the base
+    if plan.perm is not None:  # mixed plan: staged (permuted) copy of X, compact padded rows
+        ldxs = _ceil(inp, BLK_COLS) * BLK_COLS
+        xs = torch.empty(T, ldxs, dtype=torch.bfloat16, device=X.device)
+        a.perm, a.xs, a.ldxs = plan.perm.data_ptr(), xs.data_ptr(), ldxs
         a.n_pf_jobs, a.t_pf = plan.n_pf_jobs, plan.t_pf
     L.check(L.lib().dz_sbmm(C.byref(a), stream_ptr()), "sbmm")
     return Y

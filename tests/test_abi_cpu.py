@@ -151,3 +151,42 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_plan_mixed_prefill_decode_host_logic():
+    """dz_plan_mixed (host C): prefill groups staged first in 256-token jobs (remainders below
+    pf_min go to decode), decode tokens after them in original order, decode jobs exactly as
+    dz_plan over the staged rows, and every token covered once by one delta job."""
+    from paper_2312_05215_b200.engine import Plan
+    rng = np.random.default_rng(5)
+    for _ in range(40):
+        D = int(rng.integers(1, 7))
+        counts = rng.integers(0, 700, size=D) * (rng.random(D) < 0.5)
+        ids = rng.permutation(np.concatenate([np.full(int(c), d) for d, c in enumerate(counts)] + [
+            rng.integers(0, D, 30)])).astype(np.int32)
+        kinds = np.where(rng.random(D) < 0.15, 3, 1).astype(np.int32)
+        p = Plan(ids, kinds, D, upload=False, pf_min=64)
+        T = ids.size
+        cnt = np.bincount(ids, minlength=D)
+        npf = np.array([0 if (cnt[s] < 64 or kinds[s] == 3) else cnt[s] - cnt[s] % 256 + (cnt[s] % 256 if cnt[s] % 256 >= 64 else 0)
+                        for s in range(D)])
+        assert p.t_pf == npf.sum()
+        perm = p.perm_host if p.t_pf else np.arange(T)
+        assert sorted(perm.tolist()) == list(range(T))
+        dec = perm[p.t_pf:]
+        assert np.all(np.diff(dec) > 0)  # decode tokens keep their original order
+        jobs = p.jobs_host
+        covered = []
+        for k, (slot, b, c, kind) in enumerate(jobs):
+            if k < p.n_pf_jobs:
+                assert 0 < c <= 256 and kind == kinds[slot] and kind != 3
+                rows = perm[b:b + c]
+                assert np.all(ids[rows] == slot)
+                covered += rows.tolist()
+            elif slot >= 0:
+                rows = perm[p.order_host[b:b + c]]
+                assert np.all(ids[rows] == slot) and c <= (32 if kind == 3 else 8)
+                covered += rows.tolist()
+            else:
+                assert b >= p.t_pf and c <= 64
+        assert sorted(covered) == list(range(T))

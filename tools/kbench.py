@@ -59,6 +59,7 @@ def main():
         "deltas_only": (ids, False, D * dbytes),
         "base_plus_1delta": (np.zeros(T, np.int32), True, dbytes + 2 * out * inp),
         "1delta_only": (np.zeros(T, np.int32), False, dbytes),
+        "base_only": (ids, True, 2 * out * inp),  # run with --debug 2 (delta items dropped)
     }
     for name, (sl, wb, nbytes) in cases.items():
         if args.case and name != args.case:

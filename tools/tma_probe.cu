@@ -9,7 +9,7 @@
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__global__ void k_stream(const uint8_t* src, size_t chunks, int chunk_bytes, int nstage, int split, uint32_t* out) {
+__global__ void k_stream(const uint8_t* src, size_t chunks, int chunk_bytes, int nstage, int split, int work, uint32_t* out) {
   extern __shared__ __align__(128) uint8_t sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);
   uint64_t* empty = full + 16;
@@ -42,6 +42,10 @@ __global__ void k_stream(const uint8_t* src, size_t chunks, int chunk_bytes, int
     for (size_t c = blockIdx.x; c < chunks; c += gridDim.x) {
       asm volatile("{\n.reg .pred P;\nW2:\nmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n@!P bra W2;\n}" ::"r"(su32(&full[stage])), "r"(phase) : "memory");
       x ^= reinterpret_cast<const uint32_t*>(ring + (size_t)stage * chunk_bytes)[threadIdx.x];
+      if (work > 0) {  // emulated per-stage consumer processing time (clock cycles)
+        const long long t0 = clock64();
+        while (clock64() - t0 < work) x += 1;
+      }
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[stage])) : "memory");
       if (++stage == nstage) { stage = 0; phase ^= 1; }
@@ -57,27 +61,28 @@ int main() {
   uint32_t* out; CK(cudaMalloc(&out, 64));
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   CK(cudaFuncSetAttribute(k_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-  struct Cfg { int chunk, nstage, cpsm, threads, split; };
+  struct Cfg { int chunk, nstage, cpsm, threads, split, work; };
   Cfg cfgs[] = {
-      {13312, 4, 2, 192, 1}, {16384, 4, 2, 192, 1}, {16384, 6, 2, 192, 1}, {32768, 3, 2, 192, 1},
-      {8192, 8, 2, 192, 1}, {16384, 8, 1, 192, 1}, {32768, 6, 1, 192, 1}, {16384, 4, 3, 192, 1},
-      {16384, 4, 4, 128, 1}, {8192, 6, 4, 128, 1}, {65536, 3, 1, 192, 1}, {16384, 12, 1, 192, 1},
-      {16384, 4, 2, 192, 8}, {16384, 6, 2, 192, 8},
+      {61440, 3, 1, 352, 1, 0},    {61440, 3, 1, 352, 1, 500},  {61440, 3, 1, 352, 1, 1000},
+      {61440, 3, 1, 352, 1, 1500}, {61440, 3, 1, 352, 1, 2000}, {61440, 3, 1, 352, 1, 2500},
+      {40960, 5, 1, 352, 1, 0},    {40960, 5, 1, 352, 1, 1000}, {40960, 5, 1, 352, 1, 1600},
+      {30720, 7, 1, 352, 1, 0},    {30720, 7, 1, 352, 1, 800},  {30720, 7, 1, 352, 1, 1200},
+      {102400, 2, 1, 352, 1, 0},   {102400, 2, 1, 352, 1, 2000},
   };
   for (const Cfg& c : cfgs) {
     const int smem = 256 + c.chunk * c.nstage;
     if (smem > 227 * 1024) continue;
     const size_t chunks = bytes / c.chunk;
     const int grid = prop.multiProcessorCount * c.cpsm;
-    k_stream<<<grid, c.threads, smem>>>(buf, chunks, c.chunk, c.nstage, c.split, out);
+    k_stream<<<grid, c.threads, smem>>>(buf, chunks, c.chunk, c.nstage, c.split, c.work, out);
     CK(cudaDeviceSynchronize());
     cudaEventRecord(e0);
-    k_stream<<<grid, c.threads, smem>>>(buf, chunks, c.chunk, c.nstage, c.split, out);
+    k_stream<<<grid, c.threads, smem>>>(buf, chunks, c.chunk, c.nstage, c.split, c.work, out);
     cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     int occ = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stream, c.threads, smem);
-    printf("chunk=%6d stages=%2d ctas/sm=%d (occ %d) split=%d inflight/SM=%4d KB : %7.1f GB/s\n", c.chunk, c.nstage, c.cpsm,
-           occ, c.split, c.chunk * c.nstage * c.cpsm / 1024, bytes / (ms * 1e-3) / 1e9);
+    printf("chunk=%6d stages=%2d ctas/sm=%d (occ %d) split=%d work=%5d cyc inflight/SM=%4d KB : %7.1f GB/s\n", c.chunk,
+           c.nstage, c.cpsm, occ, c.split, c.work, c.chunk * c.nstage * c.cpsm / 1024, bytes / (ms * 1e-3) / 1e9);
   }
   return 0;
 }
