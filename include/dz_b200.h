@@ -200,6 +200,32 @@ int dz_gather_rows(const uint16_t* X, int64_t ldx, const int32_t* perm, int32_t 
 int dz_sbmm_ctas_per_sm(void);
 int dz_sbmm(const dz_sbmm_args* args, void* stream);
 
+/* ---- DZDL container (formats.py:60-169): the delta swap-in path ------------------- */
+typedef struct dz_dzdl_info {
+  int32_t version, flags;   /* flags bit 0 = deflate payloads (FLAG_LOSSLESS)          */
+  int32_t lossless, _pad;
+  int64_t header_off, header_len; /* JSON header bytes (configuration; parsed by the caller) */
+  int64_t layers_off;       /* first layer record                                     */
+} dz_dzdl_info;
+typedef struct dz_dzdl_layer {
+  int64_t name_off;         /* byte ranges inside the container buffer                 */
+  int32_t name_len, rows, cols, _pad;
+  int64_t scales_off, scales_len;
+  int64_t index_off, index_len;
+  int64_t payload_off, payload_len; /* stored payload (deflate stream when lossless)   */
+} dz_dzdl_layer;
+/* Replaces the magic/version/header part of formats.read_delta (formats.py:102-130):
+ * DZ_E_FORMAT (bad magic / truncated, *err_offset = byte offset), DZ_E_UNSUPPORTED (version). */
+int dz_dzdl_parse_header(const uint8_t* buf, int64_t len, dz_dzdl_info* info, int64_t* err_offset);
+/* Replaces the per-layer loop of formats.read_delta (formats.py:132-162): byte ranges of
+ * layer_count records starting at layers_off. DZ_E_FORMAT on truncation (*err_offset = the
+ * offset where reading failed), DZ_E_VALUE on trailing bytes (*err_offset = end of the last layer). */
+int dz_dzdl_parse_layers(const uint8_t* buf, int64_t len, int64_t layers_off, int32_t layer_count,
+                         dz_dzdl_layer* layers, int64_t* err_offset);
+/* Replaces compress.lossless_decode (compress.py:560-564, zlib): inflate src into dst[cap].
+ * *out_len = inflated bytes; DZ_E_FORMAT = corrupt stream; DZ_E_ENCODING = dst too small
+ * (*out_len = the size needed; call again). dst may be NULL to size the output. */
+int dz_inflate(const uint8_t* src, int64_t n, uint8_t* dst, int64_t cap, int64_t* out_len);
 #ifdef __cplusplus
 }
 #endif

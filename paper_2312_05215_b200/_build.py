@@ -17,7 +17,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
            "--expt-relaxed-constexpr", f"-I{os.path.join(ROOT, 'include')}"]
 
-SOURCES = ["dz_codec.cu", "dz_sbmm.cu", "dz_prefill.cu", "dz_host.cpp"]
+SOURCES = ["dz_codec.cu", "dz_sbmm.cu", "dz_prefill.cu", "dz_host.cpp", "dz_dzdl.cpp"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:
@@ -55,7 +55,7 @@ def build(verbose: bool = False, force: bool = False, trace: bool = False, varia
             if verbose:
                 sys.stderr.write(r.stderr)
     if force or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lz"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

@@ -61,6 +61,18 @@ class DzSbmmArgs(C.Structure):
     ]
 
 
+class DzDzdlInfo(C.Structure):
+    _fields_ = [("version", C.c_int32), ("flags", C.c_int32), ("lossless", C.c_int32), ("_pad", C.c_int32),
+                ("header_off", C.c_int64), ("header_len", C.c_int64), ("layers_off", C.c_int64)]
+
+
+class DzDzdlLayer(C.Structure):
+    _fields_ = [("name_off", C.c_int64), ("name_len", C.c_int32), ("rows", C.c_int32), ("cols", C.c_int32),
+                ("_pad", C.c_int32), ("scales_off", C.c_int64), ("scales_len", C.c_int64),
+                ("index_off", C.c_int64), ("index_len", C.c_int64), ("payload_off", C.c_int64),
+                ("payload_len", C.c_int64)]
+
+
 # symbol -> (restype, argtypes); every symbol include/dz_b200.h declares
 SIGNATURES = {
     "dz_version": (C.c_char_p, []),
@@ -90,6 +102,10 @@ SIGNATURES = {
                                  C.c_void_p]),
     "dz_sbmm": (C.c_int, [C.POINTER(DzSbmmArgs), C.c_void_p]),
     "dz_sbmm_ctas_per_sm": (C.c_int, []),
+    "dz_dzdl_parse_header": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(DzDzdlInfo), C.POINTER(C.c_int64)]),
+    "dz_dzdl_parse_layers": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_void_p,
+                                       C.POINTER(C.c_int64)]),
+    "dz_inflate": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]),
 }
 
 _lib = None

@@ -72,3 +72,28 @@ class RefDeltaDevice:
             self.packed.data_ptr(), pv.size, self.index.data_ptr(), idx.size,
             self.scales.data_ptr(), sc.size, self.rows, self.cols, self.bits,
             1 if self.sparse else 0, self.group_size, 0)
+
+    @classmethod
+    def from_pinned(cls, ld, pin: torch.Tensor, r_packed, r_index, r_scales, device) -> "RefDeltaDevice":
+        """Same device layout, filled by asynchronous copies from slices of a pinned host buffer
+        (the DZDL loader's staging; the caller keeps `pin` alive until the stream syncs)."""
+        self = cls.__new__(cls)
+        self.rows, self.cols, self.bits = int(ld.rows), int(ld.cols), int(ld.bits)
+        self.sparse = ld.sparsity == "two_of_four"
+        self.group_size = int(ld.group_size)
+        npk = (r_packed[1] - r_packed[0]) // 4
+        nix = r_index[1] - r_index[0]
+        nsc = (r_scales[1] - r_scales[0]) // 4
+        self.packed = torch.zeros(npk + 4, dtype=torch.int32, device=device)
+        self.index = torch.zeros(nix + 16, dtype=torch.uint8, device=device)
+        self.scales = torch.zeros(nsc + 4, dtype=torch.float32, device=device)
+        if npk:
+            self.packed.view(torch.uint8)[: 4 * npk].copy_(pin[r_packed[0]: r_packed[1]], non_blocking=True)
+        if nix:
+            self.index[:nix].copy_(pin[r_index[0]: r_index[1]], non_blocking=True)
+        if nsc:
+            self.scales.view(torch.uint8)[: 4 * nsc].copy_(pin[r_scales[0]: r_scales[1]], non_blocking=True)
+        self.struct = L.DzRefDelta(
+            self.packed.data_ptr(), npk, self.index.data_ptr(), nix, self.scales.data_ptr(), nsc,
+            self.rows, self.cols, self.bits, 1 if self.sparse else 0, self.group_size, 0)
+        return self

@@ -51,7 +51,13 @@ class NativeDelta:
     @classmethod
     def from_layer_delta(cls, ld, device=None) -> "NativeDelta":
         dev = device or require_cuda()
-        ref = RefDeltaDevice(ld, dev)
+        return cls.from_ref_device(RefDeltaDevice(ld, dev), ld)
+
+    @classmethod
+    def from_ref_device(cls, ref: RefDeltaDevice, ld) -> "NativeDelta":
+        """Upload-time re-layout of reference-layout bytes already on the device (`ld` supplies
+        the configuration: sparsity, bits, group size)."""
+        dev = ref.packed.device
         lib = L.lib()
         err = ErrFlag(dev)
         if cls.sparse_native_ok(ld):

@@ -1,0 +1,279 @@
+"""DZDL delta containers -> device-resident deltas (the swap-in path).
+
+Reference: formats.py:60-169 (write_delta / read_delta / inspect_delta), compress.py:560-564
+(zlib lossless codec). The container is parsed in place by the native parser
+(`dz_dzdl_parse_header` / `dz_dzdl_parse_layers`, dz_dzdl.cpp) over an mmap of the file, deflate
+payloads are inflated by `dz_inflate`, and `load_delta` stages every layer through pinned host
+memory with asynchronous copies before the upload-time re-layout (`dz_repack_sparse`), which
+validates every index nibble (FormatError at load time, not at first use).
+
+`read_delta` / `inspect_delta` keep the reference signatures and error contract (FormatError
+with the byte offset of truncations, bad magic, unsupported version, trailing bytes) for host
+callers; `DeltaPool` is the serving-side store of resident deltas with tensor-parallel
+resharding of the packed format (stack.shard_sub).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import json
+import mmap
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .compress import SPARSITY_2_4, LayerDelta
+from .errors import FormatError
+
+DELTA_MAGIC = b"DZDL"
+LOSSLESS_OFF, LOSSLESS_DEFLATE = "off", "deflate"
+
+
+@dataclass(frozen=True)
+class CompressConfig:
+    """The configuration fields a DZDL header carries (reference compress.py:44-69)."""
+
+    bits: int = 4
+    sparsity: str = SPARSITY_2_4
+    group_size: int = 128
+    damping: float = 0.01
+    block_size: int = 32
+    lossless: str = LOSSLESS_OFF
+
+
+@dataclass
+class CompressedDelta:
+    """reference compress.py:147-161"""
+
+    base_model_id: str
+    layers: list
+    config: CompressConfig
+    calibration_fingerprint: int
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, CompressedDelta):
+            return NotImplemented
+        return (self.base_model_id == other.base_model_id and self.config == other.config
+                and self.calibration_fingerprint == other.calibration_fingerprint and self.layers == other.layers)
+
+
+@dataclass
+class LayerSizes:
+    """reference formats.py:172-186"""
+
+    name: str
+    rows: int
+    cols: int
+    scales_bytes: int
+    index_bytes: int
+    payload_bytes: int
+
+    @property
+    def total_bytes(self) -> int:
+        return self.scales_bytes + self.index_bytes + self.payload_bytes
+
+    @property
+    def dense16_bytes(self) -> int:
+        return self.rows * self.cols * 2
+
+
+@dataclass
+class _Parsed:
+    data: object  # bytes-like (mmap or bytes)
+    header: dict
+    config: CompressConfig
+    layers: list = field(default_factory=list)  # DzDzdlLayer records
+
+
+def _buf_ptr(data) -> tuple[int, object]:
+    arr = np.frombuffer(data, dtype=np.uint8)
+    return arr.ctypes.data, arr
+
+
+def _parse(data, strict_header: bool = True) -> _Parsed:
+    lib = L.lib()
+    ptr, keep = _buf_ptr(data)
+    n = len(data)
+    info = L.DzDzdlInfo()
+    off = C.c_int64(0)
+    st = lib.dz_dzdl_parse_header(ptr, n, C.byref(info), C.byref(off))
+    if st == L.DZ_E_FORMAT:
+        if n >= 4 and bytes(data[:4]) != DELTA_MAGIC:
+            raise FormatError(f"bad magic {bytes(data[:4])!r}, expected {DELTA_MAGIC!r}", offset=0)
+        raise FormatError("truncated file while reading the container header", offset=off.value)
+    if st == L.DZ_E_UNSUPPORTED:
+        raise FormatError(f"unsupported version {info.version}", offset=4)
+    L.check(st, "dzdl header")
+    try:
+        header = json.loads(bytes(data[info.header_off: info.header_off + info.header_len]).decode("utf-8"))
+    except (UnicodeDecodeError, json.JSONDecodeError) as exc:
+        raise FormatError(f"bad header json: {exc}", offset=12) from exc
+    try:
+        cfg = CompressConfig(bits=int(header["bits"]), sparsity=header["sparsity"], group_size=int(header["group_size"]),
+                             damping=header.get("damping", 0.01), block_size=header.get("block_size", 32),
+                             lossless=LOSSLESS_DEFLATE if info.lossless else LOSSLESS_OFF)
+        count = int(header["layer_count"])
+        header["base_model_id"], header["calibration_fingerprint"]  # noqa: B018 (required keys)
+    except (KeyError, ValueError, TypeError) as exc:
+        raise FormatError(f"invalid header: {exc}", offset=12) from exc
+    recs = (L.DzDzdlLayer * max(count, 1))()
+    st = lib.dz_dzdl_parse_layers(ptr, n, info.layers_off, count, recs, C.byref(off))
+    if st == L.DZ_E_FORMAT:
+        raise FormatError("truncated file while reading a layer record", offset=off.value)
+    if st == L.DZ_E_VALUE and strict_header:
+        raise FormatError(f"{n - off.value} trailing bytes after last layer", offset=off.value)
+    if st not in (L.DZ_OK, L.DZ_E_VALUE):
+        L.check(st, "dzdl layers")
+    del keep
+    return _Parsed(data, header, cfg, list(recs)[:count])
+
+
+def _inflate(src: np.ndarray, rows: int, cols: int, cfg: CompressConfig) -> np.ndarray:
+    """zlib payload -> uint8 array (compress.py:560-564, FormatError on a corrupt stream)."""
+    lib = L.lib()
+    n_vals = rows * cols // 2 if cfg.sparsity == SPARSITY_2_4 else rows * cols
+    guess = 8 * n_vals if cfg.bits == 16 else 4 * (-(-n_vals * cfg.bits // 32)) + 64
+    out = np.empty(max(guess, 16), dtype=np.uint8)
+    got = C.c_int64(0)
+    st = lib.dz_inflate(src.ctypes.data, src.size, out.ctypes.data, out.size, C.byref(got))
+    if st == L.DZ_E_ENCODING:
+        out = np.empty(got.value, dtype=np.uint8)
+        st = lib.dz_inflate(src.ctypes.data, src.size, out.ctypes.data, out.size, C.byref(got))
+    if st == L.DZ_E_FORMAT:
+        raise FormatError("corrupt lossless stream")
+    L.check(st, "inflate")
+    return out[: got.value]
+
+
+def _layer_arrays(p: _Parsed, rec) -> tuple[str, np.ndarray, bytes, np.ndarray]:
+    buf = np.frombuffer(p.data, dtype=np.uint8)
+    name = bytes(buf[rec.name_off: rec.name_off + rec.name_len]).decode("utf-8")
+    scales = buf[rec.scales_off: rec.scales_off + rec.scales_len]
+    index = buf[rec.index_off: rec.index_off + rec.index_len]
+    payload = buf[rec.payload_off: rec.payload_off + rec.payload_len]
+    if p.config.lossless == LOSSLESS_DEFLATE:
+        payload = _inflate(np.ascontiguousarray(payload), rec.rows, rec.cols, p.config)
+    if payload.size % 4:
+        raise FormatError("payload not a whole number of 32-bit words", offset=int(rec.payload_off + rec.payload_len))
+    return name, payload, index, scales
+
+
+def read_delta(path) -> CompressedDelta:
+    """Reference formats.read_delta (formats.py:102-169): host LayerDeltas of a DZDL file."""
+    with open(path, "rb") as f:
+        data = f.read()
+    p = _parse(data)
+    layers = []
+    for rec in p.layers:
+        name, payload, index, scales = _layer_arrays(p, rec)
+        layers.append(LayerDelta(name=name, rows=int(rec.rows), cols=int(rec.cols),
+                                 packed_values=payload.view("<u4").copy(), index_stream=index.tobytes(),
+                                 scales=scales.view("<f4").copy(), bits=p.config.bits, sparsity=p.config.sparsity,
+                                 group_size=p.config.group_size))
+    return CompressedDelta(base_model_id=p.header["base_model_id"], layers=layers, config=p.config,
+                           calibration_fingerprint=p.header["calibration_fingerprint"])
+
+
+def inspect_delta(path) -> tuple[dict, list[LayerSizes], float]:
+    """Reference formats.inspect_delta (formats.py:189-218)."""
+    with open(path, "rb") as f:
+        data = f.read()
+    p = _parse(data)
+    sizes = []
+    for rec in p.layers:
+        name = bytes(np.frombuffer(data, np.uint8)[rec.name_off: rec.name_off + rec.name_len]).decode("utf-8")
+        sizes.append(LayerSizes(name, int(rec.rows), int(rec.cols), int(rec.scales_len), int(rec.index_len),
+                                int(rec.payload_len)))
+    dense = sum(s.dense16_bytes for s in sizes)
+    return p.header, sizes, (dense / len(data) if data else 0.0)
+
+
+class _PinnedLayer:
+    """One layer's reference-layout bytes staged in pinned host memory and copied to the device
+    asynchronously (the copy overlaps the parsing of the next layer)."""
+
+    def __init__(self, ld_fields, device):
+        from .device import RefDeltaDevice
+        name, payload, index, scales, rows, cols, cfg = ld_fields
+        self.ld = LayerDelta(name=name, rows=rows, cols=cols, packed_values=np.zeros(0, "<u4"), index_stream=b"",
+                             scales=np.zeros(0, "<f4"), bits=cfg.bits, sparsity=cfg.sparsity,
+                             group_size=cfg.group_size)
+        pin = torch.empty(payload.size + index.size + scales.size + 48, dtype=torch.uint8).pin_memory()
+        hv = pin.numpy()
+        o1, o2 = payload.size, payload.size + index.size
+        hv[:o1] = payload
+        hv[o1:o2] = index
+        hv[o2:o2 + scales.size] = scales
+        self.pin = pin
+        self.dev = RefDeltaDevice.from_pinned(self.ld, pin, (0, o1), (o1, o2), (o2, o2 + scales.size), device)
+
+
+def load_delta(path, device=None):
+    """Parse a DZDL file (mmap), inflate deflate payloads, stage each layer through pinned memory
+    with async H2D copies, and re-lay it out on the GPU (nibbles validated). Returns
+    (CompressedDelta metadata with empty host arrays, list of NativeDelta)."""
+    from .device import require_cuda
+    from .engine import NativeDelta
+    dev = device or require_cuda()
+    with open(path, "rb") as f:
+        mm = mmap.mmap(f.fileno(), 0, access=mmap.ACCESS_READ) if os.path.getsize(path) else b""
+        try:
+            p = _parse(mm)
+            staged = []
+            for rec in p.layers:
+                name, payload, index, scales = _layer_arrays(p, rec)
+                staged.append(_PinnedLayer((name, payload, index, scales, int(rec.rows), int(rec.cols), p.config), dev))
+                del payload, index, scales  # views into the mapping: released before it closes
+            natives = [NativeDelta.from_ref_device(s.dev, s.ld) for s in staged]
+            torch.cuda.current_stream(dev).synchronize()  # pinned staging buffers may be released now
+            meta = CompressedDelta(base_model_id=p.header["base_model_id"], layers=[s.ld for s in staged],
+                                   config=p.config, calibration_fingerprint=p.header["calibration_fingerprint"])
+        finally:
+            if isinstance(mm, mmap.mmap):
+                del p
+                mm.close()
+    return meta, natives
+
+
+class DeltaPool:
+    """Device-resident deltas of the served models: delta id -> one NativeDelta per layer.
+
+    `load` swaps a DZDL file in (optionally as this rank's tensor-parallel shard: per-layer axes,
+    "column" splits W's output rows, "row" its input columns, on native-block edges like
+    stack.tp_bounds); `table(layer, ids)` builds the device table one fused launch routes to."""
+
+    def __init__(self, device=None):
+        from .device import require_cuda
+        self.device = device or require_cuda()
+        self.deltas: dict[int, list] = {}
+
+    def load(self, delta_id: int, path, rank: int = 0, world: int = 1, axes=None) -> None:
+        from .stack import shard_sub, split_units
+        _, natives = load_delta(path, self.device)
+        if world > 1:
+            out = []
+            for i, nat in enumerate(natives):
+                ax = (axes or ["column"] * len(natives))[i]
+                if ax == "column":
+                    r0, r1 = split_units(nat.rows, world, 16)[rank]
+                    out.append(shard_sub(nat, r0, r1, 0, nat.cols))
+                else:
+                    c0, c1 = split_units(nat.cols, world, 128)[rank]
+                    out.append(shard_sub(nat, 0, nat.rows, c0, c1))
+            natives = out
+        self.deltas[int(delta_id)] = natives
+
+    def evict(self, delta_id: int) -> None:
+        self.deltas.pop(int(delta_id), None)
+
+    def table(self, layer: int, ids):
+        from .engine import DeltaTable
+        nats = [self.deltas[int(d)][layer] for d in ids]
+        return DeltaTable(nats, nats[0].rows, nats[0].cols)
+
+    @property
+    def nbytes(self) -> int:
+        return sum(n.nbytes for v in self.deltas.values() for n in v)

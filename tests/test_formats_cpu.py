@@ -1,0 +1,113 @@
+"""DZDL container parsing on the host (native parser dz_dzdl.cpp + zlib inflate) against fixtures
+written by the REFERENCE writer (tests/golden/make_dzdl.py runs formats.write_delta on deltas
+from compress_model): field-by-field equality with the reference's read_delta output, the
+inspect_delta sizes, and the reference error contract (formats.py:102-169)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+GOLD = os.path.join(ROOT, "tests", "golden")
+CASES = ["dzdl_b4", "dzdl_b4_deflate", "dzdl_b2", "dzdl_b16_dense"]
+
+
+@pytest.fixture(scope="module")
+def F():
+    from paper_2312_05215_b200 import formats
+    return formats
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_read_delta_matches_reference(F, case):
+    cd = F.read_delta(os.path.join(GOLD, case + ".dzdl"))
+    z = np.load(os.path.join(GOLD, case + ".npz"))
+    meta = json.load(open(os.path.join(GOLD, case + ".json")))
+    h = meta["header"]
+    assert cd.base_model_id == h["base_model_id"] and cd.calibration_fingerprint == h["calibration_fingerprint"]
+    assert (cd.config.bits, cd.config.sparsity, cd.config.group_size) == (h["bits"], h["sparsity"], h["group_size"])
+    assert cd.config.lossless == h["codec"]
+    assert len(cd.layers) == h["layer_count"] == len(meta["layers"])
+    for i, (ld, lm) in enumerate(zip(cd.layers, meta["layers"])):
+        assert (ld.name, ld.rows, ld.cols) == (lm["name"], lm["rows"], lm["cols"])
+        assert np.array_equal(ld.packed_values, z[f"l{i}_packed"])
+        assert ld.index_stream == z[f"l{i}_index"].tobytes()
+        assert np.array_equal(ld.scales.view(np.uint32), z[f"l{i}_scales"].view(np.uint32))
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_inspect_delta_matches_reference(F, case):
+    header, sizes, ratio = F.inspect_delta(os.path.join(GOLD, case + ".dzdl"))
+    meta = json.load(open(os.path.join(GOLD, case + ".json")))
+    assert header == meta["header"]
+    assert [[s.scales_bytes, s.index_bytes, s.payload_bytes] for s in sizes] == meta["sizes"]
+    assert ratio == pytest.approx(meta["ratio"], rel=1e-12)
+
+
+def _blob(case="dzdl_b4"):
+    return open(os.path.join(GOLD, case + ".dzdl"), "rb").read()
+
+
+def test_bad_magic(F, tmp_path):
+    p = tmp_path / "bad.dzdl"
+    p.write_bytes(b"NOPE" + bytes(64))
+    with pytest.raises(F.FormatError, match="magic"):
+        F.read_delta(p)
+
+
+def test_truncation_reports_offset(F, tmp_path):
+    blob = _blob()
+    for cut in (len(blob) - 10, 30, 6):
+        p = tmp_path / f"cut{cut}.dzdl"
+        p.write_bytes(blob[:cut])
+        with pytest.raises(F.FormatError, match="offset") as ei:
+            F.read_delta(p)
+        assert ei.value.offset is not None and ei.value.offset <= cut
+
+
+def test_trailing_bytes(F, tmp_path):
+    p = tmp_path / "t.dzdl"
+    p.write_bytes(_blob() + b"xx")
+    with pytest.raises(F.FormatError, match="trailing"):
+        F.read_delta(p)
+
+
+def test_unsupported_version(F, tmp_path):
+    b = bytearray(_blob())
+    b[4] = 7
+    p = tmp_path / "v.dzdl"
+    p.write_bytes(bytes(b))
+    with pytest.raises(F.FormatError, match="version"):
+        F.read_delta(p)
+
+
+def test_corrupt_deflate_stream(F, tmp_path):
+    cd = F.read_delta(os.path.join(GOLD, "dzdl_b4_deflate.dzdl"))
+    blob = bytearray(_blob("dzdl_b4_deflate"))
+    # flip bytes inside the first layer's payload (after its 4-byte length)
+    from paper_2312_05215_b200 import _lib as L
+    import ctypes as C
+    info, off = L.DzDzdlInfo(), C.c_int64(0)
+    arr = np.frombuffer(bytes(blob), np.uint8)
+    assert L.lib().dz_dzdl_parse_header(arr.ctypes.data, arr.size, C.byref(info), C.byref(off)) == 0
+    recs = (L.DzDzdlLayer * len(cd.layers))()
+    assert L.lib().dz_dzdl_parse_layers(arr.ctypes.data, arr.size, info.layers_off, len(cd.layers), recs,
+                                        C.byref(off)) == 0
+    o = recs[0].payload_off + 10
+    blob[o:o + 8] = b"\xff" * 8
+    p = tmp_path / "z.dzdl"
+    p.write_bytes(bytes(blob))
+    with pytest.raises(F.FormatError, match="lossless"):
+        F.read_delta(p)
+
+
+def test_bad_header_json(F, tmp_path):
+    b = bytearray(_blob())
+    b[12] = ord("!")
+    p = tmp_path / "j.dzdl"
+    p.write_bytes(bytes(b))
+    with pytest.raises(F.FormatError, match="header"):
+        F.read_delta(p)
