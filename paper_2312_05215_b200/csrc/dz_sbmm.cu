@@ -64,8 +64,11 @@ __device__ unsigned long long dz_item_trace[65536][3];  // per item: start, end,
 
 namespace dz {
 
-constexpr int NW = 8;                     // consumer warps per CTA (one CTA per SM)
-constexpr int MR = 2;                     // 16-row groups per consumer warp
+#ifndef DZ_NW
+#define DZ_NW 8
+#endif
+constexpr int NW = DZ_NW;                 // consumer warps per CTA (one CTA per SM)
+constexpr int MR = 16 / NW;               // 16-row groups per consumer warp (RG = 16 per item)
 constexpr int WARP_PROD = NW;             // TMA producer warp
 constexpr int WARP_MMA = NW + 1;          // tcgen05 issuer / TMEM owner warp
 constexpr int WARP_XPROD = NW + 2;        // per-token X copies of delta stages
@@ -73,6 +76,9 @@ constexpr int NTHREADS = (NW + 3) * 32;
 constexpr int RG = NW * MR;               // row groups per item
 constexpr int RT = RG * kBlkRows;         // rows per item (256) == 2 x UMMA M
 constexpr int UMMA_M = 128;
+#ifndef DZ_SHIFT_FMA
+#define DZ_SHIFT_FMA 0  // 1: code-field shifts on the FMA pipe (IMAD.HI); measured 15% slower (ab_shift)
+#endif
 #ifndef DZ_NB_SP
 #define DZ_NB_SP 4
 #endif
@@ -172,9 +178,12 @@ template <int FB, bool RAW>
 __device__ __forceinline__ void conv_codes(uint32_t (&a)[4], const uint32_t (&cw)[4], int i, uint32_t off2) {
   if (FB == 4) {
     const uint32_t w = cw[i];
+    // shifts on the FMA pipe (IMAD.HI): the ALU pipe carries the LOP3s (DZ_SHIFT_FMA=0: SHF on ALU)
+    const uint32_t sh[4] = {w, DZ_SHIFT_FMA ? mulhi_shr<4>(w) : w >> 4, DZ_SHIFT_FMA ? mulhi_shr<8>(w) : w >> 8,
+                            DZ_SHIFT_FMA ? mulhi_shr<12>(w) : w >> 12};
 #pragma unroll
     for (int k = 0; k < 4; k++) {
-      a[k] = lop3_and_or(w >> (4 * k), 0x000F000Fu, 0x43004300u);
+      a[k] = lop3_and_or(sh[k], 0x000F000Fu, 0x43004300u);
       if (!RAW) a[k] = bf16x2_sub(a[k], off2);
     }
   } else {
@@ -392,13 +401,14 @@ __device__ __forceinline__ void merge_contribution(const MergeCtx& m, int slot, 
 // (rows 128*(w/4)..) of the tile, TMEM lanes 32*(w%4)..+31 (the lanes warp w may access).
 __device__ __forceinline__ void drain_base_accumulator(uint32_t tmem_acc, int warp, int lane, const MergeCtx& m,
                                                        int split, int row0, int tok_begin, int tcount) {
-  // TMEM lane quarter q = warp % 4 (the hardware's warp -> lane restriction); the two warps of a
+  // TMEM lane quarter q = warp % 4 (the hardware's warp -> lane restriction); the NW/4 warps of a
   // quarter split the 64 token columns.
-  const int q = warp & 3, half = warp >> 2;
+  constexpr int PER = BASE_N / 16 / (NW / 4);  // 16-column chunks per warp
+  const int q = warp & 3, part = warp >> 2;
   const int row = row0 + 32 * q + lane;
   const uint32_t taddr = tmem_acc + (static_cast<uint32_t>(32 * q) << 16);
 #pragma unroll 1
-  for (int c = half * (BASE_N / 32); c < (half + 1) * (BASE_N / 32); c++) {
+  for (int c = part * PER; c < (part + 1) * PER; c++) {
     if (c * 16 >= tcount) break;
     uint32_t v[16];
     tmem_ld16(taddr + c * 16, v);
@@ -869,7 +879,7 @@ static_assert(A_DN + BASE_CH * KC_DN * BASE_N * 2 <= STAGE_BYTES && BASE_CH * BA
               "base stage layout");
 static_assert(NB_SP % PAIR == 0, "sparse stages hold whole block pairs");
 static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
-static_assert(NW == 8, "drain_base_accumulator: two consumer warps per TMEM lane quarter");
+static_assert((NW == 8 || NW == 16) && MR * NW == 16, "consumer warps: 8 (2 row groups each) or 16 (1 each)");
 static_assert(sizeof(dz_native_delta) == 192, "dz_native_delta must be 192 bytes");
 static_assert(offsetof(dz_native_delta, tmap) == 64, "tensor map must be 64-byte aligned in the entry");
 static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
