@@ -31,6 +31,7 @@
 #include <cuda.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "dz_common.cuh"
 #include "dz_tmap.h"
@@ -38,37 +39,54 @@
 namespace dz {
 namespace pf {
 
-constexpr int M = 128;                      // rows per item (one UMMA M tile)
+constexpr int M = 128;                      // rows per UMMA M tile
 constexpr int NMAX = 256;                   // tokens per job (UMMA N <= 256)
 constexpr int KC = 64;                      // columns per stage (one 128-B swizzle row)
-constexpr int NSTAGE = 3;
-constexpr int NDQ = 4;                      // dequant warps
+constexpr int NDQ = 8;                      // dequant warps
 constexpr int NEPI = 4;                     // epilogue warps
 constexpr int WARP_PROD = NDQ + NEPI;
 constexpr int WARP_MMA = WARP_PROD + 1;
 constexpr int NTHREADS = (WARP_MMA + 1) * 32;
-constexpr int RGS = M / kBlkRows;           // 8 row groups (native block rows) per item
-constexpr int W_BYTES = M * KC * 2;         // 16 KB
-constexpr int DW_BYTES = M * KC * 2;        // 16 KB
+constexpr int RGS = M / kBlkRows;           // 8 row groups (native block rows) per M tile
+constexpr int W_TILE = M * KC * 2;          // 16 KB: one W (or ΔW) tile of a stage
 constexpr int XBOX = 64;                    // tokens per X TMA box
 constexpr int X_BYTES = NMAX * KC * 2;      // 32 KB
-constexpr int STAGE = W_BYTES + DW_BYTES + X_BYTES;
-constexpr int DSLOT = RGS * sparse_block_bytes(4);  // 6656 B: one 128-column block column
-constexpr int NDSLOT = 2;
 constexpr int ACC_COLS = NMAX;
-constexpr int TMEM_COLS = 2 * ACC_COLS;
+constexpr int TMEM_COLS = 512;
 
+// MT = UMMA M tiles per item (rows per item = 128·MT). MT = 1: 3 stages, double-buffered TMEM
+// accumulator (the epilogue overlaps the next item). MT = 2: the two M tiles share every X tile
+// (half the L2 traffic per flop), 2 stages, one accumulator pair (the epilogue is exposed).
+// Each output element sees the same MMA sequence either way (W k-steps then ΔW k-steps per
+// stage), so the choice never changes a result bit.
+template <int MT>
+struct Cfg {
+  static constexpr int NSTAGE = MT == 1 ? 3 : 2;
+  static constexpr int NDSLOT = MT == 1 ? 4 : 2;  // native-block ring: 128-column block columns in flight
+  static constexpr int NBUF = MT == 1 ? 2 : 1;
+  static constexpr int W_BYTES = MT * W_TILE;
+  static constexpr int DW_BYTES = MT * W_TILE;
+  static constexpr int STAGE = W_BYTES + DW_BYTES + X_BYTES;
+  static constexpr int DSLOT = MT * RGS * sparse_block_bytes(4);  // one 128-column block column
+  static constexpr int ROWS = MT * M;
+};
+
+template <int MT>
 struct Smem {
-  uint64_t full[NSTAGE];    // TMA: W + X of the stage landed
-  uint64_t empty[NSTAGE];   // MMA: the stage (W, ΔW, X) was consumed
-  uint64_t dq[NSTAGE];      // dequant warps: ΔW tile of the stage written
-  uint64_t dfull[NDSLOT];   // TMA: native blocks of a 128-column block column landed
-  uint64_t dempty[NDSLOT];  // dequant warps: done with the block column
-  uint64_t tfull[2];        // MMA: accumulator complete
-  uint64_t tempty[2];       // epilogue: accumulator drained
+  uint64_t full[Cfg<MT>::NSTAGE];    // TMA: W + X of the stage landed
+  uint64_t empty[Cfg<MT>::NSTAGE];   // MMA: the stage (W, ΔW, X) was consumed
+  uint64_t dq[Cfg<MT>::NSTAGE];      // dequant warps: ΔW tiles of the stage written
+  uint64_t dfull[Cfg<MT>::NDSLOT];   // TMA: native blocks of a 128-column block column landed
+  uint64_t dempty[Cfg<MT>::NDSLOT];  // dequant warps: done with the block column
+  uint64_t tfull[2];                 // MMA: accumulator complete
+  uint64_t tempty[2];                // epilogue: accumulator drained
   uint32_t tmem_base;
 };
-constexpr int SMEM_BYTES = 1024 + NSTAGE * STAGE + NDSLOT * DSLOT + static_cast<int>(sizeof(Smem));
+template <int MT>
+constexpr int smem_bytes() {
+  return 1024 + Cfg<MT>::NSTAGE * Cfg<MT>::STAGE + Cfg<MT>::NDSLOT * Cfg<MT>::DSLOT +
+         static_cast<int>(sizeof(Smem<MT>));
+}
 
 __device__ __forceinline__ void sts64(uint32_t addr, uint32_t lo, uint32_t hi) {
   asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(lo), "r"(hi) : "memory");
@@ -105,14 +123,14 @@ __device__ __forceinline__ Item item_at(const dz_sbmm_args& a, int item, int n_j
 
 // Dequantise the 64-column half `h` of the current block column for row groups rg0, rg0+1 of the
 // item into the stage's ΔW tile. Native block layout: dz_codec.cu (k_repack_sparse).
-template <int FB>
+template <int FB, int NRG>
 __device__ __forceinline__ void dequant_half(uint32_t dw, uint32_t dslot, int rg0, int n_valid, int h, int qmax,
                                              int lane) {
   constexpr int CODE = sparse_code_bytes(FB);
   constexpr int BB = sparse_block_bytes(FB);
   const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-  for (int m = 0; m < 2; m++) {
+  for (int m = 0; m < NRG; m++) {
     const int rgl = rg0 + m;
     const bool valid = rgl < n_valid;  // warp-uniform
     const uint32_t blk = dslot + rgl * BB;
@@ -165,16 +183,21 @@ __device__ __forceinline__ void dequant_half(uint32_t dw, uint32_t dslot, int rg
   }
 }
 
+template <int MT>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_prefill(const __grid_constant__ dz_sbmm_args a, const __grid_constant__ CUtensorMap xmap) {
+  using C = Cfg<MT>;
+  constexpr int NSTAGE = C::NSTAGE, STAGE = C::STAGE, DSLOT = C::DSLOT, W_BYTES = C::W_BYTES;
+  constexpr int DW_BYTES = C::DW_BYTES, NBUF = C::NBUF, IRG = MT * RGS;  // row groups per item
+  constexpr int NDSLOT = C::NDSLOT;
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* stages = smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);
   uint8_t* dslots = stages + NSTAGE * STAGE;
-  Smem* sm = reinterpret_cast<Smem*>(dslots + NDSLOT * DSLOT);
+  Smem<MT>* sm = reinterpret_cast<Smem<MT>*>(dslots + NDSLOT * DSLOT);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   const int n_jobs = a.n_pf_jobs;
-  const int nrt = ceil_div(a.out, M);
+  const int nrt = ceil_div(a.out, C::ROWS);
   const int n_items = nrt * n_jobs;
   const int nch = ceil_div(a.in, KC);
   const int nkb = ceil_div(a.in, kBlkCols);
@@ -191,7 +214,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(&sm->dfull[s], 1);
       mbar_init(&sm->dempty[s], NDQ);
     }
-    for (int b = 0; b < 2; b++) {
+    for (int b = 0; b < NBUF; b++) {
       mbar_init(&sm->tfull[b], 1);
       mbar_init(&sm->tempty[b], NEPI);
     }
@@ -220,8 +243,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const dz_native_delta* ent = a.table + it.slot;
       const uint8_t* blocks = static_cast<const uint8_t*>(ent->blocks);
       const int bb = sparse_block_bytes(kind_fbits(it.kind));
-      const int nrg = min(RGS, n16 - it.rt * RGS);
+      const int nrg = min(IRG, n16 - it.rt * IRG);
       const int nxb = ceil_div(it.npad, XBOX);
+      const int ntile = min(MT, ceil_div(a.out - it.rt * C::ROWS, M));  // W tiles inside `out`
       for (int ch = 0; ch < nch; ch++) {
         if ((ch & 1) == 0) {  // native blocks of block column ch/2 for this row tile
           mbar_wait(&sm->dempty[ds], dph ^ 1);
@@ -229,15 +253,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           __syncwarp();
           if (lane < nrg)
             tma_load_1d(dslots + ds * DSLOT + lane * bb,
-                        blocks + (static_cast<int64_t>(it.rt * RGS + lane) * nkb + (ch >> 1)) * bb,
+                        blocks + (static_cast<int64_t>(it.rt * IRG + lane) * nkb + (ch >> 1)) * bb,
                         static_cast<uint32_t>(bb), &sm->dfull[ds], pol_stream);
           if (++ds == NDSLOT) { ds = 0; dph ^= 1; }
         }
         mbar_wait(&sm->empty[s], ph ^ 1);
         if (lane == 0) {
           uint8_t* sb = stages + s * STAGE;
-          mbar_arrive_expect_tx(&sm->full[s], (has_base ? W_BYTES : 0) + nxb * XBOX * KC * 2);
-          if (has_base) tma_load_2d(sb, a.base->tmap, ch * KC, it.rt * M, &sm->full[s], pol_keep);
+          mbar_arrive_expect_tx(&sm->full[s], (has_base ? ntile * W_TILE : 0) + nxb * XBOX * KC * 2);
+          if (has_base)
+            for (int h = 0; h < ntile; h++)
+              tma_load_2d(sb + h * W_TILE, a.base->tmap, ch * KC, it.rt * C::ROWS + h * M, &sm->full[s], pol_keep);
           for (int b = 0; b < nxb; b++)
             tma_load_2d(sb + W_BYTES + DW_BYTES + b * XBOX * KC * 2, &xmap, ch * KC, it.tok_begin + b * XBOX,
                         &sm->full[s], pol_keep);
@@ -252,11 +278,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint32_t ph = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const Item it = item_at(a, item, n_jobs);
-      const int buf = nacc & 1;
-      mbar_wait(&sm->tempty[buf], ((nacc >> 1) & 1) ^ 1);
+      const int buf = NBUF == 1 ? 0 : (nacc & 1);
+      const uint32_t tph = NBUF == 1 ? (nacc & 1) : ((nacc >> 1) & 1);
+      mbar_wait(&sm->tempty[buf], tph ^ 1);
       tc_fence_after();
       const uint32_t idesc = umma_idesc_bf16(M, it.npad);
-      const uint32_t tmem_d = tmem_base + buf * ACC_COLS;
       for (int ch = 0; ch < nch; ch++) {
         mbar_wait(&sm->full[s], ph);
         mbar_wait(&sm->dq[s], ph);
@@ -265,15 +291,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const uint32_t sb = smem_u32(stages + s * STAGE);
           const uint64_t xdesc = umma_desc_sw128(sb + W_BYTES + DW_BYTES);
           if (has_base) {
-            const uint64_t wdesc = umma_desc_sw128(sb);
+#pragma unroll
+            for (int h = 0; h < MT; h++) {
+              const uint64_t wdesc = umma_desc_sw128(sb + h * W_TILE);
+              const uint32_t tmem_d = tmem_base + (buf * MT + h) * ACC_COLS;
+#pragma unroll
+              for (int k = 0; k < KC / 16; k++)
+                umma_bf16(tmem_d, wdesc + 2 * k, xdesc + 2 * k, idesc, (ch | k) ? 1u : 0u);
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < MT; h++) {
+            const uint64_t ddesc = umma_desc_sw128(sb + W_BYTES + h * W_TILE);
+            const uint32_t tmem_d = tmem_base + (buf * MT + h) * ACC_COLS;
 #pragma unroll
             for (int k = 0; k < KC / 16; k++)
-              umma_bf16(tmem_d, wdesc + 2 * k, xdesc + 2 * k, idesc, (ch | k) ? 1u : 0u);
+              umma_bf16(tmem_d, ddesc + 2 * k, xdesc + 2 * k, idesc, (has_base || (ch | k)) ? 1u : 0u);
           }
-          const uint64_t ddesc = umma_desc_sw128(sb + W_BYTES);
-#pragma unroll
-          for (int k = 0; k < KC / 16; k++)
-            umma_bf16(tmem_d, ddesc + 2 * k, xdesc + 2 * k, idesc, (has_base || (ch | k)) ? 1u : 0u);
           umma_commit(&sm->empty[s]);
           if (ch == nch - 1) umma_commit(&sm->tfull[buf]);
         }
@@ -288,18 +322,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint32_t ph = 0, dph = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const Item it = item_at(a, item, n_jobs);
-      const int nrg = min(RGS, n16 - it.rt * RGS);
+      const int nrg = min(IRG, n16 - it.rt * IRG);
       const int qmax = kind_qmax(it.kind);
       const bool two_bit = it.kind == DZ_KIND_SPARSE2;
+      const int bb = sparse_block_bytes(kind_fbits(it.kind));
       for (int ch = 0; ch < nch; ch++) {
         if ((ch & 1) == 0) mbar_wait(&sm->dfull[ds], dph);
-        mbar_wait(&sm->empty[s], ph ^ 1);  // the MMAs that last read this ΔW tile are done
-        const uint32_t dw = smem_u32(stages + s * STAGE + W_BYTES);
-        const uint32_t dsl = smem_u32(dslots + ds * DSLOT);
+        mbar_wait(&sm->empty[s], ph ^ 1);  // the MMAs that last read these ΔW tiles are done
+        // warp w covers RPW consecutive row groups of the item (within one M tile)
+        constexpr int RPW = IRG / NDQ;
+        const int rg = RPW * warp, tile = rg / RGS;
+        const uint32_t dw = smem_u32(stages + s * STAGE + W_BYTES + tile * W_TILE);
+        const uint32_t dsl = smem_u32(dslots + ds * DSLOT) + tile * RGS * bb;
         if (two_bit)
-          dequant_half<2>(dw, dsl, 2 * warp, nrg, ch & 1, qmax, lane);
+          dequant_half<2, RPW>(dw, dsl, rg - tile * RGS, nrg - tile * RGS, ch & 1, qmax, lane);
         else
-          dequant_half<4>(dw, dsl, 2 * warp, nrg, ch & 1, qmax, lane);
+          dequant_half<4, RPW>(dw, dsl, rg - tile * RGS, nrg - tile * RGS, ch & 1, qmax, lane);
         fence_proxy_async();  // generic-proxy st.shared -> visible to the tensor core (async proxy)
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm->dq[s]);
@@ -317,13 +355,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     int nacc = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const Item it = item_at(a, item, n_jobs);
-      const int buf = nacc & 1;
-      mbar_wait(&sm->tfull[buf], (nacc >> 1) & 1);
+      const int buf = NBUF == 1 ? 0 : (nacc & 1);
+      mbar_wait(&sm->tfull[buf], NBUF == 1 ? (nacc & 1) : ((nacc >> 1) & 1));
       tc_fence_after();
-      const int row = it.rt * M + 32 * q + lane;
-      const uint32_t taddr = tmem_base + buf * ACC_COLS + (static_cast<uint32_t>(32 * q) << 16);
 #pragma unroll 1
-      for (int c = 0; c < it.npad / 16; c++) {
+      for (int cc = 0; cc < MT * (it.npad / 16); cc++) {
+        const int h = cc / (it.npad / 16), c = cc - h * (it.npad / 16);
+        const int row = it.rt * C::ROWS + h * M + 32 * q + lane;
+        const uint32_t taddr = tmem_base + (buf * MT + h) * ACC_COLS + (static_cast<uint32_t>(32 * q) << 16);
         uint32_t v[16];
         tmem_ld16(taddr + c * 16, v);
         const int i0 = it.tok_begin + c * 16;
@@ -375,8 +414,9 @@ __global__ void k_gather_rows(const uint16_t* __restrict__ X, int64_t ldx, const
 
 using namespace dz;
 
-static_assert(pf::SMEM_BYTES <= 232448, "prefill kernel shared memory");
-static_assert(pf::STAGE % 1024 == 0 && pf::W_BYTES % 1024 == 0 && pf::DW_BYTES % 1024 == 0, "SW128 tile alignment");
+static_assert(pf::smem_bytes<1>() <= 232448 && pf::smem_bytes<2>() <= 232448, "prefill kernel shared memory");
+static_assert(pf::Cfg<1>::STAGE % 1024 == 0 && pf::Cfg<2>::STAGE % 1024 == 0 && pf::W_TILE % 1024 == 0,
+              "SW128 tile alignment");
 
 extern "C" int dz_gather_rows(const uint16_t* X, int64_t ldx, const int32_t* perm, int32_t T, int32_t in,
                               uint16_t* Xs, int64_t ldxs, void* stream) {
@@ -393,7 +433,21 @@ extern "C" int dz_gather_rows(const uint16_t* X, int64_t ldx, const int32_t* per
   return cudaGetLastError() == cudaSuccess ? DZ_OK : DZ_E_CUDA;
 }
 
-// Launch K3 over jobs[0:n_pf_jobs]; X is the staged buffer (xs when perm is set).
+template <int MT>
+static int launch_prefill(const dz_sbmm_args& k, const CUtensorMap& xmap, int grid, void* stream) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(pf::k_prefill<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    pf::smem_bytes<MT>());
+  });
+  if (attr_err != cudaSuccess) return DZ_E_CUDA;
+  return launch_pdl(pf::k_prefill<MT>, grid, pf::NTHREADS, pf::smem_bytes<MT>(), stream, k, xmap);
+}
+
+// Launch K3 over jobs[0:n_pf_jobs]; X is the staged buffer (dz_sbmm passes it as X).
+// Items of 128 or 256 rows: the one with fewer item rounds per SM, weighted by the measured
+// per-item efficiency (MT=2 shares each X tile between two M tiles). Results are identical.
 extern "C" int dz_sbmm_prefill(const dz_sbmm_args* a, void* stream) {
   if (!a || !a->Y || !a->table || !a->jobs) return DZ_E_VALUE;
   if (a->T < 0 || a->out < 1 || a->in < 1) return DZ_E_SHAPE;
@@ -402,24 +456,24 @@ extern "C" int dz_sbmm_prefill(const dz_sbmm_args* a, void* stream) {
   if (!X) return DZ_E_VALUE;
   if ((a->ldx % 8) != 0 || (reinterpret_cast<uintptr_t>(X) & 15) != 0 || a->ldx < a->in) return DZ_E_SHAPE;
   if (a->y_dtype != DZ_F32 && a->y_dtype != DZ_BF16) return DZ_E_VALUE;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(pf::k_prefill, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::SMEM_BYTES);
-  });
-  if (attr_err != cudaSuccess) return DZ_E_CUDA;
   CUtensorMap xmap;  // staged X [T][in] bf16, 64-column x 64-token SWIZZLE_128B boxes (UMMA B operand)
   const int st = encode_2d(&xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, X, static_cast<uint64_t>(a->in),
                            static_cast<uint64_t>(a->T), static_cast<uint64_t>(a->ldx) * 2, pf::KC, pf::XBOX,
                            CU_TENSOR_MAP_SWIZZLE_128B);
   if (st) return st;
-  dz_sbmm_args k = *a;
-  k.X = X;
   int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return DZ_E_CUDA;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return DZ_E_CUDA;
-  const int n_items = ceil_div(a->out, pf::M) * a->n_pf_jobs;
-  int grid = a->grid > 0 ? a->grid : sms;
-  if (grid > n_items) grid = n_items;
-  return launch_pdl(pf::k_prefill, grid, pf::NTHREADS, pf::SMEM_BYTES, stream, k, xmap);
+  const int g = a->grid > 0 ? a->grid : sms;
+  const int items1 = ceil_div(a->out, pf::M) * a->n_pf_jobs;
+  const int items2 = ceil_div(a->out, 2 * pf::M) * a->n_pf_jobs;
+  // time ~ rounds x rows per item / per-item efficiency. Measured (profiles/r01_pf_mt.txt): MT=2 is
+  // 7-33% slower at every 13B shape (2-stage ring, exposed epilogue), so MT=1 unless overridden.
+  const double t1 = ceil_div(items1, g) * 1.0 / 0.75, t2 = ceil_div(items2, g) * 2.0 / 0.62;
+  int mt = t2 < t1 ? 2 : 1;
+  const char* e = std::getenv("DZ_PF_MT");  // experiment override (A/B)
+  if (e && (e[0] == '1' || e[0] == '2')) mt = e[0] - '0';
+  const int n_items = mt == 2 ? items2 : items1;
+  const int grid = g > n_items ? n_items : g;
+  return mt == 2 ? launch_prefill<2>(*a, xmap, grid, stream) : launch_prefill<1>(*a, xmap, grid, stream);
 }

@@ -167,3 +167,22 @@ def test_prefill_strided_input_view(E):
     Y = E.sbmm_forward(Xv, plan, base, table, y_dtype=torch.float32).cpu().double().numpy()
     R = O.sbmm_matrix(W, dict(enumerate(ods)), ids, X)
     assert rel_err_rows(Y, R).max() <= REL_TOL
+
+
+@pytest.mark.parametrize("rows,cols,bits", [(640, 512, 4), (300, 448, 2)])
+def test_prefill_item_height_does_not_change_results(E, rows, cols, bits, monkeypatch):
+    """K3 items of 128 rows (MT=1) and 256 rows (MT=2, two M tiles sharing each X tile) issue the
+    same MMA sequence per output element: bit-identical results, both within tolerance."""
+    rng = np.random.default_rng(rows + bits)
+    W, ods, table, base = _setup(E, rng, rows, cols, [bits] * 3)
+    ids = _ids(rng, [256, 140, 9])
+    X = bf16_round(rng.normal(0, 1, (ids.size, cols)))
+    Xd = torch.from_numpy(X.astype(np.float32)).cuda().to(torch.bfloat16)
+    plan = E.Plan(ids, table.kinds, 3, pf_min=64)
+    ys = []
+    for mt in ("1", "2"):
+        monkeypatch.setenv("DZ_PF_MT", mt)
+        ys.append(E.sbmm_forward(Xd, plan, base, table, y_dtype=torch.float32))
+    assert torch.equal(ys[0], ys[1])
+    R = O.sbmm_matrix(W, dict(enumerate(ods)), ids, X)
+    assert rel_err_rows(ys[1].cpu().double().numpy(), R).max() <= REL_TOL
