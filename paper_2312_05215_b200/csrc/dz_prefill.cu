@@ -109,13 +109,44 @@ struct Item {
   int rt, tok_begin, tok_count, npad, slot, kind;
 };
 
-__device__ __forceinline__ Item item_at(const dz_sbmm_args& a, int item, int n_jobs) {
+// Static round-robin schedule with a split tail: when the last round of (row tile, job) items would
+// leave most CTAs idle, its items are cut into `split` (2 or 4) token slices, so the tail round
+// streams the same weights with fewer tokens per CTA. Each output column's MMA sequence is the
+// same whatever the slice width, so this never changes a result bit.
+struct Sched {
+  int tail0, split, n_items;
+};
+__device__ __forceinline__ Sched make_sched(int n_full, int grid) {
+  Sched sc;
+  const int tail = n_full % grid;
+  int split = 1;
+  if (tail)
+    while (split < 4 && tail * split * 2 <= grid) split *= 2;
+  sc.split = split;
+  sc.tail0 = split > 1 ? n_full - tail : n_full;
+  sc.n_items = sc.tail0 + (n_full - sc.tail0) * split;
+  return sc;
+}
+
+__device__ __forceinline__ Item item_at(const dz_sbmm_args& a, int item, int n_jobs, const Sched& sc) {
+  int base = item, part = 0;
+  if (item >= sc.tail0) {
+    const int j = item - sc.tail0;
+    base = sc.tail0 + j / sc.split;
+    part = j - (j / sc.split) * sc.split;
+  }
   Item it;
-  it.rt = item / n_jobs;
-  const dz_job jb = a.jobs[item - it.rt * n_jobs];
-  it.tok_begin = jb.tok_begin;
-  it.tok_count = jb.tok_count;
-  it.npad = (jb.tok_count + 15) & ~15;
+  it.rt = base / n_jobs;
+  const dz_job jb = a.jobs[base - it.rt * n_jobs];
+  int b0 = 0, cnt = jb.tok_count;
+  if (item >= sc.tail0) {
+    const int ps = ((jb.tok_count + sc.split - 1) / sc.split + 15) & ~15;
+    b0 = part * ps;
+    cnt = max(0, min(jb.tok_count, b0 + ps) - b0);
+  }
+  it.tok_begin = jb.tok_begin + b0;
+  it.tok_count = cnt;
+  it.npad = (cnt + 15) & ~15;
   it.slot = jb.slot;
   it.kind = jb.kind;
   return it;
@@ -198,7 +229,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   const int n_jobs = a.n_pf_jobs;
   const int nrt = ceil_div(a.out, C::ROWS);
-  const int n_items = nrt * n_jobs;
+  const Sched sc = make_sched(nrt * n_jobs, static_cast<int>(gridDim.x));
+  const int n_items = sc.n_items;
   const int nch = ceil_div(a.in, KC);
   const int nkb = ceil_div(a.in, kBlkCols);
   const int n16 = ceil_div(a.out, kBlkRows);
@@ -239,7 +271,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     int s = 0, ds = 0;
     uint32_t ph = 0, dph = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const Item it = item_at(a, item, n_jobs);
+      const Item it = item_at(a, item, n_jobs, sc);
+      if (it.tok_count == 0) continue;  // empty tail slice (same decision in every role)
       const dz_native_delta* ent = a.table + it.slot;
       const uint8_t* blocks = static_cast<const uint8_t*>(ent->blocks);
       const int bb = sparse_block_bytes(kind_fbits(it.kind));
@@ -277,7 +310,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     int s = 0, nacc = 0;
     uint32_t ph = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const Item it = item_at(a, item, n_jobs);
+      const Item it = item_at(a, item, n_jobs, sc);
+      if (it.tok_count == 0) continue;  // empty tail slice (same decision in every role)
       const int buf = NBUF == 1 ? 0 : (nacc & 1);
       const uint32_t tph = NBUF == 1 ? (nacc & 1) : ((nacc >> 1) & 1);
       mbar_wait(&sm->tempty[buf], tph ^ 1);
@@ -321,7 +355,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     int s = 0, ds = 0;
     uint32_t ph = 0, dph = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const Item it = item_at(a, item, n_jobs);
+      const Item it = item_at(a, item, n_jobs, sc);
+      if (it.tok_count == 0) continue;  // empty tail slice (same decision in every role)
       const int nrg = min(IRG, n16 - it.rt * IRG);
       const int qmax = kind_qmax(it.kind);
       const bool two_bit = it.kind == DZ_KIND_SPARSE2;
@@ -354,7 +389,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     griddep_wait();  // Y rows may still be written by the preceding kernel
     int nacc = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const Item it = item_at(a, item, n_jobs);
+      const Item it = item_at(a, item, n_jobs, sc);
+      if (it.tok_count == 0) continue;  // empty tail slice (same decision in every role)
       const int buf = NBUF == 1 ? 0 : (nacc & 1);
       mbar_wait(&sm->tfull[buf], NBUF == 1 ? (nacc & 1) : ((nacc >> 1) & 1));
       tc_fence_after();
