@@ -41,14 +41,15 @@ inline int encode_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, u
   return r == CUDA_SUCCESS ? DZ_OK : DZ_E_CUDA;
 }
 
-// Launch with programmatic dependent launch (the kernel starts while its predecessor in the
-// stream drains and calls griddepcontrol.wait before touching the predecessor's output).
-// DZ_PDL=0 in the environment launches normally (A/B switch).
+// Optional programmatic dependent launch (the kernel starts while its predecessor in the stream
+// drains; every kernel calls griddepcontrol.wait before touching the predecessor's output, so
+// both modes are correct). Off by default: on the 7B decode step it measured 0.4-0.8% slower
+// (two A/B pairs, profiles/r01_ab_pdl.txt). DZ_PDL=1 in the environment enables it.
 inline bool pdl_enabled() {
   static int on = -1;
   if (on < 0) {
     const char* e = std::getenv("DZ_PDL");
-    on = (e && e[0] == '0') ? 0 : 1;
+    on = (e && e[0] == '1') ? 1 : 0;
   }
   return on == 1;
 }
