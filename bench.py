@@ -84,6 +84,16 @@ def _delta_task(args):
     return time.perf_counter() - t0
 
 
+def _worker_init():
+    """One BLAS thread per worker process: the pool already puts one process on every core
+    (otherwise each forked numpy would start a full OpenBLAS pool and oversubscribe the host)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except ImportError:  # pragma: no cover
+        pass
+
+
 def _base_task(args):
     out, inp, seed = args
     rng = np.random.default_rng(seed)
@@ -107,7 +117,7 @@ class CpuReference:
         import multiprocessing as mp
         from paper_2312_05215_b200.synth import llama_linears
         self.cores = cores or min(os.cpu_count() or 1, 32)  # ~1.5 GB of numpy temporaries per worker
-        self.pool = mp.get_context("fork").Pool(self.cores)
+        self.pool = mp.get_context("fork").Pool(self.cores, initializer=_worker_init)
         self.shapes = {}
         for name, out, inp in llama_linears(MODEL):
             self.shapes.setdefault((out, inp), []).append(name)
@@ -247,10 +257,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # DZ_BENCH_SHARE_GPU=1 (testing the N>1 path on a one-GPU box): every rank on cuda:0 and the
+    # collective over gloo (NCCL refuses two ranks on one device); gloo cannot be graph-captured.
+    share = world > 1 and os.environ.get("DZ_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
+        args.no_graph = True
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=device)
 
     from paper_2312_05215_b200.engine import Plan
     from paper_2312_05215_b200.stack import STEP_ORDER, LlamaStack
