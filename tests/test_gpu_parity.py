@@ -55,13 +55,20 @@ def test_unpack_bit_exact(P, path):
     assert torch.equal(gotbf.view(torch.int16), torch.from_numpy(ref).to(torch.bfloat16).view(torch.int16))
 
 
-@pytest.mark.parametrize("path", golden_files("unpack_*.npz"), ids=os.path.basename)
+def _sparse_native_fixture(path):
+    """2:4 with 2/3/4-bit codes and gs % 128 == 0 (or one group per row): the native-block layout
+    (engine.NativeDelta.sparse_native_ok); the other fixtures are served through the dense path."""
+    rows, cols, bits, sparse, gs = (int(v) for v in np.load(path)["meta"])
+    return sparse and bits in (2, 3, 4) and (gs % 128 == 0 or -(-cols // gs) == 1)
+
+
+@pytest.mark.parametrize("path", [p for p in golden_files("unpack_*.npz") if _sparse_native_fixture(p)],
+                         ids=os.path.basename)
 def test_native_relayout_lossless(P, path):
     from paper_2312_05215_b200.engine import NativeDelta
     z = np.load(path)
     ld = _ld(P, z)
-    if not NativeDelta.sparse_native_ok(ld):
-        pytest.skip("not a sparse-native layout (served through the dense path)")
+    assert NativeDelta.sparse_native_ok(ld)
     nat = NativeDelta.from_layer_delta(ld)
     got = nat.to_dense_f32().cpu().numpy()
     assert np.array_equal(got, z["dequant"].astype(np.float32))
