@@ -19,15 +19,16 @@
 // row-tile-major in a static round robin, so the W tile of a row tile is shared through L2 by the
 // jobs running at the same time and the staged X of every job stays L2-resident.
 //
-// Warp roles (10 warps, one CTA per SM, 206 KB shared memory, 512 TMEM columns):
-//  * warps 0-3  dequant: per 64-column stage, 2 row groups each: native block -> bf16 ΔW tile.
-//  * warps 4-7  epilogue: TMEM lane quarter (warp % 4) -> Y rows (tcgen05.ld 32x32b), activation.
-//  * warp 8     TMA producer: W tile (2-D tensor map of the base, box 64 x 128), X tile (box
-//               64 x 64, up to 4 per stage), and per 128 columns the 8 native blocks of the
-//               row tile (1-D bulk copies) into a 2-slot ring.
-//  * warp 9     TMEM owner + MMA issuer: 4 K=16 MMAs of W and 4 of ΔW per stage into a
+// Warp roles (15 warps, one CTA per SM, 224 KB shared memory, 512 TMEM columns):
+//  * warps 0-7  dequant: per 64-column stage, one 16-row group each: native block -> bf16 ΔW tile.
+//  * warps 8-11 epilogue: TMEM lane quarter (warp % 4) -> Y rows (tcgen05.ld 32x32b), activation.
+//  * warp 12    TMA producer: W tile (2-D tensor map of the base, box 64 x 128) and X tiles
+//               (box 64 x 64, up to 4 per stage) into a 3-stage ring.
+//  * warp 13    TMEM owner + MMA issuer: 4 K=16 MMAs of W and 4 of ΔW per stage into a
 //               double-buffered accumulator (2 x 256 columns), so the epilogue of an item
 //               overlaps the next item's main loop.
+//  * warp 14    native-block producer: per 128 columns the row tile's native blocks (one 1-D bulk
+//               copy per 16-row group) into a 4-slot ring that runs ahead of the stage ring.
 #include <cuda.h>
 
 #include <cstdint>
@@ -46,7 +47,8 @@ constexpr int NDQ = 8;                      // dequant warps
 constexpr int NEPI = 4;                     // epilogue warps
 constexpr int WARP_PROD = NDQ + NEPI;
 constexpr int WARP_MMA = WARP_PROD + 1;
-constexpr int NTHREADS = (WARP_MMA + 1) * 32;
+constexpr int WARP_DPROD = WARP_MMA + 1;    // native-block producer (runs ahead of the stage ring)
+constexpr int NTHREADS = (WARP_DPROD + 1) * 32;
 constexpr int RGS = M / kBlkRows;           // 8 row groups (native block rows) per M tile
 constexpr int W_TILE = M * KC * 2;          // 16 KB: one W (or ΔW) tile of a stage
 constexpr int XBOX = 64;                    // tokens per X TMA box
@@ -262,34 +264,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const uint32_t tmem_base = sm->tmem_base;
 
   if (warp == WARP_PROD) {
-    // ===================== TMA producer =====================
-    const uint64_t pol_stream = policy_evict_first();
+    // ===================== TMA producer (W and X tiles) =====================
     const uint64_t pol_keep = policy_evict_last();
     if (lane == 0) prefetch_tmap(&xmap);
     griddep_wait();  // the staged X is the preceding kernel's output (programmatic dependent launch)
     griddep_launch_dependents();
-    int s = 0, ds = 0;
-    uint32_t ph = 0, dph = 0;
+    int s = 0;
+    uint32_t ph = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const Item it = item_at(a, item, n_jobs, sc);
       if (it.tok_count == 0) continue;  // empty tail slice (same decision in every role)
-      const dz_native_delta* ent = a.table + it.slot;
-      const uint8_t* blocks = static_cast<const uint8_t*>(ent->blocks);
-      const int bb = sparse_block_bytes(kind_fbits(it.kind));
-      const int nrg = min(IRG, n16 - it.rt * IRG);
       const int nxb = ceil_div(it.npad, XBOX);
       const int ntile = min(MT, ceil_div(a.out - it.rt * C::ROWS, M));  // W tiles inside `out`
       for (int ch = 0; ch < nch; ch++) {
-        if ((ch & 1) == 0) {  // native blocks of block column ch/2 for this row tile
-          mbar_wait(&sm->dempty[ds], dph ^ 1);
-          if (lane == 0) mbar_arrive_expect_tx(&sm->dfull[ds], static_cast<uint32_t>(nrg * bb));
-          __syncwarp();
-          if (lane < nrg)
-            tma_load_1d(dslots + ds * DSLOT + lane * bb,
-                        blocks + (static_cast<int64_t>(it.rt * IRG + lane) * nkb + (ch >> 1)) * bb,
-                        static_cast<uint32_t>(bb), &sm->dfull[ds], pol_stream);
-          if (++ds == NDSLOT) { ds = 0; dph ^= 1; }
-        }
         mbar_wait(&sm->empty[s], ph ^ 1);
         if (lane == 0) {
           uint8_t* sb = stages + s * STAGE;
@@ -303,6 +290,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         __syncwarp();
         if (++s == NSTAGE) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == WARP_DPROD) {
+    // ===================== native-block producer =====================
+    // Per 128-column block column, the item's native blocks (one 1-D bulk copy per 16-row group)
+    // into an NDSLOT-deep ring, independent of the W/X stage ring so the delta stream runs ahead.
+    const uint64_t pol_stream = policy_evict_first();
+    int ds = 0;
+    uint32_t dph = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const Item it = item_at(a, item, n_jobs, sc);
+      if (it.tok_count == 0) continue;
+      const uint8_t* blocks = static_cast<const uint8_t*>((a.table + it.slot)->blocks);
+      const int bb = sparse_block_bytes(kind_fbits(it.kind));
+      const int nrg = min(IRG, n16 - it.rt * IRG);
+      for (int kb = 0; kb < ceil_div(nch, 2); kb++) {
+        mbar_wait(&sm->dempty[ds], dph ^ 1);
+        if (lane == 0) mbar_arrive_expect_tx(&sm->dfull[ds], static_cast<uint32_t>(nrg * bb));
+        __syncwarp();
+        if (lane < nrg)
+          tma_load_1d(dslots + ds * DSLOT + lane * bb,
+                      blocks + (static_cast<int64_t>(it.rt * IRG + lane) * nkb + kb) * bb, static_cast<uint32_t>(bb),
+                      &sm->dfull[ds], pol_stream);
+        if (++ds == NDSLOT) { ds = 0; dph ^= 1; }
       }
     }
   } else if (warp == WARP_MMA) {
