@@ -489,7 +489,7 @@ static int launch_prefill(const dz_sbmm_args& k, const CUtensorMap& xmap, int gr
                                     pf::smem_bytes<MT>());
   });
   if (attr_err != cudaSuccess) return DZ_E_CUDA;
-  return launch_pdl(pf::k_prefill<MT>, grid, pf::NTHREADS, pf::smem_bytes<MT>(), stream, k, xmap);
+  return launch_pdl(1, pf::k_prefill<MT>, grid, pf::NTHREADS, pf::smem_bytes<MT>(), stream, k, xmap);
 }
 
 // Launch K3 over jobs[0:n_pf_jobs]; X is the staged buffer (dz_sbmm passes it as X).

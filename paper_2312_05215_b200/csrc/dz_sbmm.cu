@@ -994,7 +994,7 @@ static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
   const int n_items = ceil_div(a->out, RT) * a->n_jobs +
                       ceil_div(a->out, BASE_RT) * a->base_splits * ceil_div(a->T, BASE_N);
   if (grid > n_items) grid = n_items;
-  st = launch_pdl(k_sbmm, grid, NTHREADS, SMEM_BYTES, stream, *a, xmap);
+  st = launch_pdl(1, k_sbmm, grid, NTHREADS, SMEM_BYTES, stream, *a, xmap);
   if (st || a->base == nullptr || (a->debug & 4)) return st;
   // merged rows -> Y (+ activation), accumulator re-zeroed
   const int t0 = a->t_pf;
@@ -1003,7 +1003,7 @@ static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
   if (fgrid > 4 * 148) fgrid = 4 * 148;
   if (fgrid < 1) fgrid = 1;
   const float* part = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(a->workspace) + 256);
-  return launch_pdl(k_finalize, fgrid, 256, 0, stream, part, a->base_splits, t0, a->T, a->out, a->perm,
+  return launch_pdl(2, k_finalize, fgrid, 256, 0, stream, part, a->base_splits, t0, a->T, a->out, a->perm,
                     a->Y, a->ldy, a->y_dtype, a->act);
 }
 

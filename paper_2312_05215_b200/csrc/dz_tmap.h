@@ -45,17 +45,18 @@ inline int encode_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, u
 // drains; every kernel calls griddepcontrol.wait before touching the predecessor's output, so
 // both modes are correct). Off by default: on the 7B decode step it measured 0.4-0.8% slower
 // (two A/B pairs, profiles/r01_ab_pdl.txt). DZ_PDL=1 in the environment enables it.
-inline bool pdl_enabled() {
-  static int on = -1;
-  if (on < 0) {
+// DZ_PDL is a bit mask: 1 = the SBMM kernels (K2, K3), 2 = k_finalize.
+inline int pdl_mask() {
+  static int m = -1;
+  if (m < 0) {
     const char* e = std::getenv("DZ_PDL");
-    on = (e && e[0] == '1') ? 1 : 0;
+    m = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
   }
-  return on == 1;
+  return m;
 }
 
 template <typename Kern, typename... Args>
-inline int launch_pdl(Kern kernel, int grid, int threads, int smem, void* stream, Args... args) {
+inline int launch_pdl(int kind_bit, Kern kernel, int grid, int threads, int smem, void* stream, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads);
@@ -65,7 +66,7 @@ inline int launch_pdl(Kern kernel, int grid, int threads, int smem, void* stream
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = (pdl_mask() & kind_bit) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, args...) == cudaSuccess ? DZ_OK : DZ_E_CUDA;
 }
 
