@@ -13,7 +13,8 @@ one CUDA graph.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 N>1 (torchrun): Megatron tensor parallelism of the same stack (strong scaling) — q,k,v,gate,up
-column-parallel, o,down row-parallel + NCCL all-reduce; shared dimensions cut on 128-column
+column-parallel, o,down row-parallel, reduced by the finalize kernel over peer memory (CUDA IPC,
+NVLink; DZ_TP_FUSED=0 falls back to an NCCL all-reduce); shared dimensions cut on 128-column
 native-block edges (7B intermediate 11008 = 86 blocks, uneven at TP 4/8).
 
 --impl reference: the reference algorithm (oracle port of inference.sbmm, numpy f64) on the
@@ -276,6 +277,9 @@ def main():
 
     t_build = time.time()
     st = LlamaStack(MODEL, args.layers, D_DELTAS, BITS, device, rank=rank, world=world)
+    fused_tp = world > 1 and os.environ.get("DZ_TP_FUSED", "1") == "1"
+    if fused_tp:  # row-parallel outputs reduced over peer memory by the finalize kernel (no NCCL)
+        st.enable_fused_tp(T_TOKENS)
     t_build = time.time() - t_build
 
     ids = token_ids()
@@ -413,7 +417,9 @@ def main():
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random bf16 base, random reference-layout 4-bit 2:4 deltas uploaded via dz_repack_sparse)",
             "config": {"workload": WORKLOAD.format(layers=args.layers),
-                       "global_batch": T_TOKENS, "parallelism": f"tp{world}" if world > 1 else "single",
+                       "global_batch": T_TOKENS,
+                       "parallelism": (f"tp{world}" + ("+peer-memory reduce" if fused_tp else "+nccl all-reduce"))
+                       if world > 1 else "single",
                        "l2": "inputs > L2 (97.5 GB streamed per step at N=1)", "cuda_graph": graph is not None,
                        "step_bytes_rank0": step_bytes},
             "gpu_launches": 2 * len(order) * args.steps,  # k_sbmm + k_finalize per fused linear

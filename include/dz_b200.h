@@ -110,7 +110,32 @@ typedef struct dz_sbmm_args {
   int32_t base_splits;      /* K-splits of the base GEMM (1..4); 0 = chosen from (out, in) only,
                                so results never depend on the batch                     */
   int32_t _pad3;
+  const struct dz_tp_ctx* tp; /* host pointer or NULL: fused tensor-parallel reduction of a
+                               row-parallel linear (decode plans only, see dz_tp_ctx)    */
 } dz_sbmm_args;
+
+/* Fused tensor-parallel reduction over peer memory (NVLink / NVSwitch), replacing the
+ * reference's simulated all-reduce of row-parallel shards (inference.py:216-223) and a separate
+ * NCCL all-reduce. Every rank's k_sbmm leaves fp32 partial planes; the finalize kernel sums them
+ * into this rank's reduce buffer, publishes a ready flag to every peer, waits for all peers, and
+ * sums the peers' buffers in rank order (identical, deterministic Y on every rank). Buffers are
+ * double-buffered by a device-resident epoch, so the step stays CUDA-graph capturable. */
+typedef struct dz_tp_ctx {
+  float* const* peer_R;     /* device array [world]: rank p's two reduce buffers (fp32,
+                               2 x max_elems), peer-mapped (dz_ipc_open)                  */
+  int* const* peer_flags;   /* device array [world]: rank p's ready flags [world] (int)    */
+  unsigned int* sync;       /* this rank's device words: [0] epoch, [1] barrier count,
+                               [2] barrier generation (zeroed once)                        */
+  int64_t max_elems;        /* capacity of one reduce buffer: >= T * out                   */
+  int32_t rank, world;
+} dz_tp_ctx;
+/* Peer-shareable device memory (cudaMalloc, zeroed) and its IPC handle exchange (64-byte
+ * cudaIpcMemHandle_t): rank r allocates, all-gathers the handles, opens every peer's. */
+int dz_peer_alloc(size_t bytes, void** ptr);
+int dz_peer_free(void* ptr);
+int dz_ipc_handle(void* ptr, uint8_t* handle64);
+int dz_ipc_open(const uint8_t* handle64, void** ptr);
+int dz_ipc_close(void* ptr);
 
 const char* dz_version(void);
 const char* dz_strerror(int status);

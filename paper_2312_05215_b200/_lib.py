@@ -58,7 +58,13 @@ class DzSbmmArgs(C.Structure):
         ("n_pf_jobs", C.c_int32), ("t_pf", C.c_int32),
         ("ldxs", C.c_int64),
         ("base_splits", C.c_int32), ("_pad3", C.c_int32),
+        ("tp", C.c_void_p),
     ]
+
+
+class DzTpCtx(C.Structure):
+    _fields_ = [("peer_R", C.c_void_p), ("peer_flags", C.c_void_p), ("sync", C.c_void_p),
+                ("max_elems", C.c_int64), ("rank", C.c_int32), ("world", C.c_int32)]
 
 
 class DzDzdlInfo(C.Structure):
@@ -106,6 +112,11 @@ SIGNATURES = {
     "dz_dzdl_parse_layers": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_void_p,
                                        C.POINTER(C.c_int64)]),
     "dz_inflate": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]),
+    "dz_peer_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
+    "dz_peer_free": (C.c_int, [C.c_void_p]),
+    "dz_ipc_handle": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "dz_ipc_open": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "dz_ipc_close": (C.c_int, [C.c_void_p]),
 }
 
 _lib = None

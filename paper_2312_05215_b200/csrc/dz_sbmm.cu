@@ -960,6 +960,9 @@ extern "C" int dz_sbmm_ctas_per_sm(void) {
   return n;
 }
 
+extern "C" int dz_tp_finalize_launch(const float* part, int nsplit, int T, int out, const dz_tp_ctx* ctx, void* Y,
+                                     int64_t ldy, int y_dtype, int act, void* stream);
+
 static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
   dz_sbmm_args kargs = *a_in;
   const dz_sbmm_args* a = &kargs;
@@ -1003,12 +1006,17 @@ static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
   if (fgrid > 4 * 148) fgrid = 4 * 148;
   if (fgrid < 1) fgrid = 1;
   const float* part = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(a->workspace) + 256);
+  if (a->tp != nullptr && a->tp->world > 1)  // row-parallel shard: fused reduction over peer memory
+    return dz_tp_finalize_launch(part, a->base_splits, a->T, a->out, a->tp, a->Y, a->ldy, a->y_dtype, a->act,
+                                 stream);
   return launch_pdl(2, k_finalize, fgrid, 256, 0, stream, part, a->base_splits, t0, a->T, a->out, a->perm,
                     a->Y, a->ldy, a->y_dtype, a->act);
 }
 
 extern "C" int dz_sbmm(const dz_sbmm_args* a, void* stream) {
   if (!a || !a->X || !a->Y || !a->workspace) return DZ_E_VALUE;
+  if (a->tp != nullptr && a->tp->world > 1 && (a->perm != nullptr || a->base == nullptr))
+    return DZ_E_UNSUPPORTED;  // the fused reduction takes decode plans with a base
   if (a->T < 0 || a->out < 1 || a->in < 1) return DZ_E_SHAPE;
   if (a->T == 0 || a->n_jobs == 0) return DZ_OK;
   const int in_pad = ceil_div(a->in, kBlkCols) * kBlkCols;

@@ -135,9 +135,18 @@ class LlamaStack:
         assert b["v"].shape[1] == l0["o"].inp and b["up"].shape[1] == l0["down"].inp
         return b
 
+    def enable_fused_tp(self, max_tokens: int) -> None:
+        """Row-parallel outputs reduced by the finalize kernel over peer memory (dz_tp.cu) instead
+        of an NCCL all-reduce: every rank reads the peers' fp32 partial sums in rank order."""
+        from .peer import PeerGroup
+        out = max(lin[f].out for lin in self.stack[:1] for f in ROW_PARALLEL)
+        self.peers = PeerGroup(self.rank, self.world, max_tokens * out, self.device, self.group)
+
     def linear(self, lin: FusedLinear, plan: Plan, X: torch.Tensor, Y: torch.Tensor) -> None:
-        sbmm_forward(X, plan, lin.base, lin.table, Y=Y, workspace=self.ws)
-        if lin.row_parallel and self.world > 1:
+        fused = lin.row_parallel and self.world > 1 and getattr(self, "peers", None) is not None \
+            and plan.perm is None
+        sbmm_forward(X, plan, lin.base, lin.table, Y=Y, workspace=self.ws, tp=self.peers if fused else None)
+        if lin.row_parallel and self.world > 1 and not fused:
             import torch.distributed as dist
             dist.all_reduce(Y, op=dist.ReduceOp.SUM, group=self.group)
 
