@@ -32,6 +32,10 @@ extern "C" {
 #define DZ_E_UNSUPPORTED 7 /* layout the called kernel does not take (caller routes elsewhere) */
 #define DZ_E_CUDA 8        /* CUDA runtime error */
 
+/* ---- plan granularity ---------------------------------------------------------------- */
+#ifndef DZ_BASE_JOB_TOKENS
+#define DZ_BASE_JOB_TOKENS 128 /* tokens per base-GEMM job of the decode kernel (its UMMA N) */
+#endif
 /* ---- element types --------------------------------------------------------------- */
 #define DZ_F32 0
 #define DZ_BF16 1
@@ -75,7 +79,7 @@ typedef struct dz_native_delta {
 typedef struct dz_job {
   int32_t slot;             /* delta-table index; -1 = base GEMM over all tokens     */
   int32_t tok_begin;        /* first position in `order` (delta) or token (base)     */
-  int32_t tok_count;        /* <= 64 (base), <= 32 (dense delta), <= 8 (sparse), <= 256 (prefill) */
+  int32_t tok_count;        /* <= DZ_BASE_JOB_TOKENS (base), <= 32 (dense delta), <= 8 (sparse), <= 256 (prefill) */
   int32_t kind;             /* 0 = base, else DZ_KIND_* of the slot                  */
 } dz_job;
 

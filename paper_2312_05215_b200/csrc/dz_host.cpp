@@ -24,7 +24,7 @@ extern "C" const char* dz_strerror(int status) {
 extern "C" int32_t dz_plan_max_jobs(int32_t T) { return T < 0 ? 0 : 2 * T + 2; }  // >= base + delta + prefill jobs
 
 // Stable sort of token rows by slot (inference.py:106-123: `sorted` is stable), then cut into
-// jobs: base token chunks of 64, sparse delta chunks of 8, dense delta chunks of 32.
+// jobs: base token chunks of DZ_BASE_JOB_TOKENS, sparse delta chunks of 8, dense delta chunks of 32.
 extern "C" int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t n_slots,
                        int32_t with_base, int32_t* order_out, dz_job* jobs_out, int32_t max_jobs,
                        int32_t* n_jobs_out) {
@@ -44,8 +44,8 @@ extern "C" int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, in
     return true;
   };
   if (with_base)
-    for (int32_t b = 0; b < T; b += 64)
-      if (!push(-1, b, (T - b) < 64 ? (T - b) : 64, 0)) return DZ_E_VALUE;
+    for (int32_t b = 0; b < T; b += DZ_BASE_JOB_TOKENS)
+      if (!push(-1, b, (T - b) < DZ_BASE_JOB_TOKENS ? (T - b) : DZ_BASE_JOB_TOKENS, 0)) return DZ_E_VALUE;
   for (int32_t s = 0; s < n_slots; s++) {
     const int32_t c = count[s + 1] - count[s];
     if (c == 0) continue;
@@ -120,8 +120,8 @@ extern "C" int dz_plan_mixed(const int32_t* slots, int32_t T, const int32_t* kin
   std::vector<int32_t> dstart(dcount.begin(), dcount.end() - 1), dfill(dstart);
   for (int32_t i = 0; i < Td; i++) order_out[dfill[dslot[i]]++] = t_pf + i;
   if (with_base)
-    for (int32_t b = t_pf; b < T; b += 64)
-      if (!push(-1, b, (T - b) < 64 ? (T - b) : 64, 0)) return DZ_E_VALUE;
+    for (int32_t b = t_pf; b < T; b += DZ_BASE_JOB_TOKENS)
+      if (!push(-1, b, (T - b) < DZ_BASE_JOB_TOKENS ? (T - b) : DZ_BASE_JOB_TOKENS, 0)) return DZ_E_VALUE;
   for (int32_t s = 0; s < n_slots; s++) {
     const int32_t c = dcount[s + 1] - dcount[s];
     if (c == 0) continue;

@@ -2,7 +2,7 @@
 //
 // Replaces inference.sbmm (inference.py:126-154): y_t = W_base x_t + ΔW_{slot(t)} x_t.
 //
-// Work decomposition. An item is (row tile, job); a job is either the base GEMM for up to 64
+// Work decomposition. An item is (row tile, job); a job is either the base GEMM for up to 128
 // tokens (row tile = 128 rows, one UMMA M tile) or one delta group for up to 8 (2:4 sparse) / 32
 // (dense) of its tokens (row tile = 256 rows; dz_plan = group_by_delta, inference.py:106-123).
 // Base items come first, then delta items row-tile-major; one persistent CTA per SM pulls items
@@ -16,7 +16,7 @@
 //    and token ids are prefetched while the current item streams.
 //  * X producer (1 warp): one 1-D bulk copy per routed token row of a delta stage.
 //  * MMA issuer (1 warp, one elected thread): base stages become tcgen05.mma kind::f16 (M=128,
-//    N=64 tokens, K=16 x 8 per stage) into a double-buffered TMEM accumulator; tcgen05.commit
+//    N=128 tokens, K=16 x 8 per stage) into a double-buffered TMEM accumulator; tcgen05.commit
 //    frees the stage and, on the last chunk, signals the accumulator full.
 //  * consumers (8 warps, two 16-row groups each): 2:4 delta stages — decode codes in registers
 //    (LOP3 magic-number bf16 conversion; deferred per-(row,128-col) scaling) and mma.sp m16n8k32
@@ -92,7 +92,7 @@ constexpr int NB_SP = DZ_NB_SP;           // sparse chunk = 4 blocks = 512 colum
 constexpr int NT_SP = 1;                  // n-tiles per sparse job (8 tokens, dz_plan)
 constexpr int NT_DN = 4;                  // n-tiles per dense-delta job (32 tokens, dz_plan)
 constexpr int KC_DN = 64;                 // dense / base chunk = 64 columns
-constexpr int BASE_N = 64;                // tokens per base job == UMMA N
+constexpr int BASE_N = DZ_BASE_JOB_TOKENS; // tokens per base job == UMMA N (dz_plan)
 constexpr int XS_SP = NB_SP * kBlkCols * 2 + 16;  // smem bytes per staged token row; +16 B so the
 constexpr int XS_DN = KC_DN * 2 + 16;             //   8 rows of an ldmatrix hit distinct banks
 constexpr int A_SP = RG * NB_SP * sparse_block_bytes(4);  // 53248
@@ -100,13 +100,14 @@ constexpr int X_SP = NT_SP * 8 * XS_SP;                   // 8320
 constexpr int DN_HALF = kDenseBlockBytes / 2;             // 2048
 constexpr int A_DN = RG * DN_HALF;                        // 32768 == 256 rows x 128 B (base W tile)
 constexpr int X_DN = 64 * XS_DN;                          // 9216 (>= 64 x 128 B swizzled X tile)
-constexpr int STAGE_BYTES = ((A_SP + X_SP > A_DN + X_DN ? A_SP + X_SP : A_DN + X_DN) + 1023) / 1024 * 1024;
+constexpr int cmax(int x, int y) { return x > y ? x : y; }
 constexpr int NSTAGE = DZ_NSTAGE;
 constexpr int JOB_DN_TOK = BASE_N;        // largest token count of a job
 constexpr int BASE_RT = UMMA_M;           // rows per base item: one UMMA M tile (half a delta row tile)
 constexpr int BASE_CH = DZ_BASE_CH;             // 64-column K-chunks per base stage (32 KB of W in flight per stage)
-constexpr int TMEM_COLS = 2 * BASE_N;     // double-buffered fp32 accumulator, 128 lanes x 64 tokens
+constexpr int TMEM_COLS = 2 * BASE_N;     // double-buffered fp32 accumulator, 128 lanes x 128 tokens
 constexpr uint32_t IDESC_BASE = umma_idesc_bf16(UMMA_M, BASE_N);
+constexpr int STAGE_BYTES = (cmax(cmax(A_SP + X_SP, A_DN + X_DN), A_DN + BASE_CH * KC_DN * BASE_N * 2) + 1023) / 1024 * 1024;
 constexpr int PF_CHUNKS = 4;              // stages of the first item prefetched into L2 before the PDL wait
 
 struct StageHdr {

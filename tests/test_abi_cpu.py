@@ -188,5 +188,5 @@ def test_plan_mixed_prefill_decode_host_logic():
                 assert np.all(ids[rows] == slot) and c <= (32 if kind == 3 else 8)
                 covered += rows.tolist()
             else:
-                assert b >= p.t_pf and c <= 64
+                assert b >= p.t_pf and c <= 128
         assert sorted(covered) == list(range(T))
