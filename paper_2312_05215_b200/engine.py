@@ -149,7 +149,9 @@ class DeltaTable:
         return len(self.deltas)
 
 
-PF_MIN = int(os.environ.get("DZ_PF_MIN", "128"))  # tokens per delta group routed to the prefill kernel
+PF_MIN = int(os.environ.get("DZ_PF_MIN", "192"))  # tokens per delta group routed to the prefill kernel
+# (7B stacks: one 128-token group is faster on the decode kernel, one 256-token group on K3;
+#  profiles/r01_ab_pf_min.txt)
 
 
 class Plan:
