@@ -280,6 +280,10 @@ def main():
     fused_tp = world > 1 and os.environ.get("DZ_TP_FUSED", "1") == "1"
     if fused_tp:  # row-parallel outputs reduced over peer memory by the finalize kernel (no NCCL)
         st.enable_fused_tp(T_TOKENS)
+        flag = torch.tensor([0 if st.peers is None else 1], device=device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)  # every rank must take the same path
+        if int(flag.item()) == 0:
+            st.peers, fused_tp = None, False
     t_build = time.time() - t_build
 
     ids = token_ids()

@@ -138,9 +138,16 @@ class LlamaStack:
     def enable_fused_tp(self, max_tokens: int) -> None:
         """Row-parallel outputs reduced by the finalize kernel over peer memory (dz_tp.cu) instead
         of an NCCL all-reduce: every rank reads the peers' fp32 partial sums in rank order."""
+        import sys
+
+        from .errors import CudaError
         from .peer import PeerGroup
         out = max(lin[f].out for lin in self.stack[:1] for f in ROW_PARALLEL)
-        self.peers = PeerGroup(self.rank, self.world, max_tokens * out, self.device, self.group)
+        try:
+            self.peers = PeerGroup(self.rank, self.world, max_tokens * out, self.device, self.group)
+        except CudaError as e:  # e.g. no CUDA IPC between the ranks' devices: keep the NCCL all-reduce
+            self.peers = None
+            print(f"[dz] fused TP reduction unavailable ({e}); using the NCCL all-reduce", file=sys.stderr)
 
     def linear(self, lin: FusedLinear, plan: Plan, X: torch.Tensor, Y: torch.Tensor) -> None:
         fused = lin.row_parallel and self.world > 1 and getattr(self, "peers", None) is not None \
