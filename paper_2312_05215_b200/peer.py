@@ -13,6 +13,7 @@ import ctypes as C
 import torch
 
 from . import _lib as L
+from .errors import CudaError
 
 FLAG_BYTES = 256  # ready flags [world] (int32) at the head of every rank's buffer
 
@@ -37,15 +38,24 @@ class PeerGroup:
             dist.all_gather_object(handles, bytes(h), group=group)
             self.opened = []
             ptrs = []
+            ok = True
             for r in range(world):
                 if r == rank:
                     ptrs.append(self.local)
                     continue
                 hb = (C.c_uint8 * 64).from_buffer_copy(handles[r])
                 p = C.c_void_p()
-                L.check(lib.dz_ipc_open(hb, C.byref(p)), f"ipc open (rank {r})")
+                if lib.dz_ipc_open(hb, C.byref(p)) != L.DZ_OK:
+                    ok = False
+                    break
                 self.opened.append(p.value)
                 ptrs.append(p.value)
+            # every rank learns whether all ranks could map all peers before anyone proceeds
+            flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=device)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+            if int(flag.item()) == 0:
+                self.close()
+                raise CudaError("CUDA IPC: a rank could not map its peers' buffers")
         self.peer_R = torch.tensor([p + FLAG_BYTES for p in ptrs], dtype=torch.int64, device=device)
         self.peer_flags = torch.tensor(ptrs, dtype=torch.int64, device=device)
         self.sync = torch.zeros(4, dtype=torch.int32, device=device)  # epoch, barrier count, generation
