@@ -378,29 +378,29 @@ def main():
     e2e = None
     if not args.no_e2e:
         # Two pinned input/output sets used alternately, each with its own captured graph of
-        # [H2D plan, H2D X, the step, D2H Y], so the host can build and write step k+1's plan and
-        # tokens while step k runs without racing the in-flight copies.
+        # [H2D slots + X, on-device plan (dz_plan_device), the step, D2H Y], so the host can write
+        # step k+1's tokens and delta ids while step k runs without racing the in-flight copies.
+        from paper_2312_05215_b200.engine import DevicePlan
         hid = bufs["x"].shape[1]
+        dplan = DevicePlan(T_TOKENS, kinds, D_DELTAS, device=device)
+        slots_dev = torch.zeros(T_TOKENS, dtype=torch.int32, device=device)
         sets = []
         for _ in range(2):
             io = {"x": torch.randn(T_TOKENS, hid).to(torch.bfloat16).pin_memory(),
                   "y": torch.empty(T_TOKENS, hid, dtype=torch.bfloat16).pin_memory(),
-                  "order": torch.zeros(plan.order.numel(), dtype=torch.int32).pin_memory(),
-                  "jobs": torch.zeros(plan.jobs.numel(), dtype=torch.uint8).pin_memory(),
+                  "slots": torch.zeros(T_TOKENS, dtype=torch.int32).pin_memory(),
                   "done": torch.cuda.Event()}
             sets.append(io)
 
         def e2e_body(io):
-            plan.order.copy_(io["order"], non_blocking=True)
-            plan.jobs.copy_(io["jobs"], non_blocking=True)
+            slots_dev.copy_(io["slots"], non_blocking=True)
             bufs["x"].copy_(io["x"], non_blocking=True)
-            st.step(plan, bufs)
+            dplan.update(slots_dev)  # group_by_delta on the device
+            st.step(dplan, bufs)
             io["y"].copy_(bufs["down"], non_blocking=True)
 
         def host_plan(io):
-            hp = Plan(ids, kinds, D_DELTAS, upload=False)  # group_by_delta for this step, on the host
-            io["order"][: hp.T].copy_(torch.from_numpy(hp.order_host))
-            io["jobs"][: hp.jobs_bytes.size].copy_(torch.from_numpy(hp.jobs_bytes))
+            io["slots"].copy_(torch.from_numpy(ids))  # this step's token -> delta map
 
         graphs = []
         if graph is not None:
@@ -436,12 +436,14 @@ def main():
             t = torch.tensor([e2e_ms], device=device)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
+        dplan.check()
         io = sets[0]
-        h2d = io["x"].numel() * 2 + io["order"].numel() * 4 + io["jobs"].numel()
+        h2d = io["x"].numel() * 2 + io["slots"].numel() * 4
         d2h = io["y"].numel() * 2
         e2e = {"value": T_TOKENS / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
-               "path": "host dz_plan + pinned H2D (plan, X) + step + D2H (Y), one CUDA graph per step"}
+               "path": "pinned H2D (delta ids, X) + on-device group_by_delta (dz_plan_device) + step + D2H (Y), "
+                       "one CUDA graph per step"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick:

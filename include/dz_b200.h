@@ -116,6 +116,8 @@ typedef struct dz_sbmm_args {
   int32_t _pad3;
   const struct dz_tp_ctx* tp; /* host pointer or NULL: fused tensor-parallel reduction of a
                                row-parallel linear (decode plans only, see dz_tp_ctx)    */
+  const int32_t* n_jobs_dev; /* device job count written by dz_plan_device, or NULL; when set,
+                               n_jobs is only the capacity of `jobs` (grid sizing)       */
 } dz_sbmm_args;
 
 /* Fused tensor-parallel reduction over peer memory (NVLink / NVSwitch), replacing the
@@ -208,6 +210,14 @@ int dz_plan_mixed(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t
                   dz_job* jobs_out, int32_t max_jobs, int32_t* n_jobs_out, int32_t* n_pf_jobs_out,
                   int32_t* t_pf_out);
 
+/* On-device plan (decode plans): the same stable group_by_delta and job cut as dz_plan, computed
+ * by one CTA from device-resident slots, so a decode loop never round-trips to the host (SURVEY
+ * §8(f)-3). Writes order[T], jobs[<= max_jobs] and *n_jobs_dev; *err_dev = DZ_E_UNKNOWN when a
+ * slot is out of range (inference.py:135-137; *n_jobs_dev = 0 then), DZ_E_VALUE when max_jobs
+ * is too small. n_slots <= 4096. Stream-ordered, graph-capturable. */
+int dz_plan_device(const int32_t* slots_dev, int32_t T, const int32_t* kinds_dev, int32_t n_slots,
+                   int32_t with_base, int32_t* order_dev, dz_job* jobs_dev, int32_t max_jobs,
+                   int32_t* n_jobs_dev, int32_t* err_dev, void* stream);
 /* K2 — fused decode SBMM. Replaces inference.sbmm (inference.py:126-154):
  * Y[t] = W_base x_t + ΔW_{slot(t)} x_t for every token in ONE persistent launch:
  * TMA bulk copies stage native blocks and X through shared memory, warps decode

@@ -59,6 +59,7 @@ class DzSbmmArgs(C.Structure):
         ("ldxs", C.c_int64),
         ("base_splits", C.c_int32), ("_pad3", C.c_int32),
         ("tp", C.c_void_p),
+        ("n_jobs_dev", C.c_void_p),
     ]
 
 
@@ -112,6 +113,8 @@ SIGNATURES = {
     "dz_dzdl_parse_layers": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_void_p,
                                        C.POINTER(C.c_int64)]),
     "dz_inflate": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]),
+    "dz_plan_device": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                 C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "dz_peer_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
     "dz_peer_free": (C.c_int, [C.c_void_p]),
     "dz_ipc_handle": (C.c_int, [C.c_void_p, C.c_void_p]),

@@ -468,7 +468,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int n_base = a.base != nullptr ? ceil_div(a.T - a.t_pf, BASE_N) : 0;  // dz_plan: base jobs first
   const int nsplit = a.base_splits;  // resolved by the host (launch_decode)
   // debug bit 1: base items only (probe of the base stream)
-  const int n_items = nbt * nsplit * n_base + ((a.debug & 2) ? 0 : nrt * (a.n_jobs - n_base));
+  const int n_jobs = a.n_jobs_dev != nullptr ? *a.n_jobs_dev : a.n_jobs;  // dz_plan_device writes the count
+  const int n_items = n_jobs < n_base ? 0 : nbt * nsplit * n_base + ((a.debug & 2) ? 0 : nrt * (n_jobs - n_base));
 
   int* sched = reinterpret_cast<int*>(a.workspace);  // [0] item counter, [1] finished CTAs
   MergeCtx mctx;
@@ -519,7 +520,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // stream into L2: it depends only on resident weights, not on the predecessor's output.
     int item = blockIdx.x;
     int rt = 0, jj = 0, sp = 0;
-    if (item < n_items) item_coords(item, nrt, nbt, nsplit, a.n_jobs, n_base, rt, jj, sp);
+    if (item < n_items) item_coords(item, nrt, nbt, nsplit, n_jobs, n_base, rt, jj, sp);
     dz_job job = item < n_items ? a.jobs[jj] : dz_job{0, 0, 0, 0};
     if (item < n_items && lane == 0) {
       const bool dn = kind_dense(job.kind);
@@ -628,7 +629,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           item_nxt = __shfl_sync(0xffffffffu, id_nxt_raw, 0);
           if (item_nxt < n_items) {
             int j_n = 0;
-            item_coords(item_nxt, nrt, nbt, nsplit, a.n_jobs, n_base, rt_n, j_n, sp_n);
+            item_coords(item_nxt, nrt, nbt, nsplit, n_jobs, n_base, rt_n, j_n, sp_n);
             job_n = a.jobs[j_n];
             if (lane == 0) prefetch_tmap((job_n.kind == 0 ? a.base : a.table + job_n.slot)->tmap);
           }

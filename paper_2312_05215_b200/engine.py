@@ -196,6 +196,42 @@ class Plan:
                 self.perm = torch.from_numpy(perm).to(dev)
 
 
+class DevicePlan:
+    """On-device decode plan (dz_plan_device): the token -> slot map stays on the
+    GPU and each `update` enqueues one planner CTA that writes order / jobs / the job count, so a
+    decode loop (or a captured CUDA graph of it) needs no host round trip. Same stable
+    group_by_delta and job cut as `Plan` (decode plans: no prefill staging)."""
+
+    def __init__(self, T: int, kinds: np.ndarray, n_slots: int, with_base: bool = True, device=None):
+        dev = device or require_cuda()
+        lib = L.lib()
+        self.T, self.n_slots, self.with_base = int(T), int(n_slots), with_base
+        self.kinds_dev = torch.from_numpy(np.ascontiguousarray(kinds, dtype=np.int32)).to(dev)
+        self.max_jobs = int(lib.dz_plan_max_jobs(self.T))
+        self.n_jobs = self.max_jobs  # capacity: the kernel reads the device count
+        self.order = torch.zeros(max(self.T, 1), dtype=torch.int32, device=dev)
+        self.jobs = torch.zeros(max(self.max_jobs, 1) * C.sizeof(L.DzJob), dtype=torch.uint8, device=dev)
+        self.n_jobs_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.perm, self.t_pf, self.n_pf_jobs = None, 0, 0
+
+    def update(self, slots_dev: torch.Tensor) -> "DevicePlan":
+        if slots_dev.numel() != self.T or slots_dev.dtype != torch.int32 or not slots_dev.is_cuda:
+            raise ShapeError("slots must be an int32 CUDA tensor of T entries")
+        L.check(L.lib().dz_plan_device(slots_dev.data_ptr(), self.T, self.kinds_dev.data_ptr(), self.n_slots,
+                                       1 if self.with_base else 0, self.order.data_ptr(), self.jobs.data_ptr(),
+                                       self.max_jobs, self.n_jobs_dev.data_ptr(), self.err.data_ptr(),
+                                       stream_ptr()), "device plan")
+        return self
+
+    def check(self) -> None:
+        """Host sync: raise the reference's error for a slot outside the table (inference.py:135-137)."""
+        code = int(self.err.item())
+        if code == L.DZ_E_UNKNOWN:
+            raise UnknownDeltaError("a token references a slot outside the delta table")
+        L.check(code, "device plan")
+
+
 class Workspace:
     """Per-(T, out) scratch for the fused kernel: scheduler + tile counters (zeroed once; the
     kernel resets them itself) and the fp32 partial buffers."""
@@ -262,6 +298,8 @@ def sbmm_forward(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: De
     a.base_splits = base_splits  # 0 = by shape (batch-independent); 1..4 = explicit K-splits of the base
     if tp is not None:  # peer.PeerGroup: row-parallel shard, reduced over peer memory by the finalize
         a.tp = C.addressof(tp.ctx)
+    if isinstance(plan, DevicePlan):
+        a.n_jobs_dev = plan.n_jobs_dev.data_ptr()
     if plan.perm is not None:  # mixed plan: staged (permuted) copy of X, compact padded rows
         ldxs = _ceil(inp, BLK_COLS) * BLK_COLS
         xs = torch.empty(T, ldxs, dtype=torch.bfloat16, device=X.device)
