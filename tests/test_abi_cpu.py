@@ -190,3 +190,24 @@ def test_plan_mixed_prefill_decode_host_logic():
             else:
                 assert b >= p.t_pf and c <= 128
         assert sorted(covered) == list(range(T))
+
+
+def test_plain_c_host_links_the_abi(tmp_path):
+    """The C ABI is usable from a plain C host (no Python, no torch): compile tests/c_host/host_demo.c
+    against include/dz_b200.h, link _dz_b200.so, run the host-side entry points."""
+    import shutil
+    import subprocess
+    from paper_2312_05215_b200 import _lib
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no C compiler")
+    lib = _lib.LIB_PATH
+    exe = tmp_path / "host_demo"
+    src = os.path.join(ROOT, "tests", "c_host", "host_demo.c")
+    r = subprocess.run([gcc, "-O1", "-std=c11", f"-I{os.path.join(ROOT, 'include')}", src, "-o", str(exe), lib,
+                        f"-Wl,-rpath,{os.path.dirname(lib)}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    for case in ("dzdl_b4.dzdl", "dzdl_b4_deflate.dzdl"):
+        r = subprocess.run([str(exe), os.path.join(ROOT, "tests", "golden", case)], capture_output=True, text=True)
+        assert r.returncode == 0, r.stdout + r.stderr
+        assert "all ok" in r.stdout and "layer 1: 64x128" in r.stdout
