@@ -55,39 +55,45 @@ constexpr int XBOX = 64;                    // tokens per X TMA box
 constexpr int X_BYTES = NMAX * KC * 2;      // 32 KB
 constexpr int ACC_COLS = NMAX;
 constexpr int TMEM_COLS = 512;
+constexpr int E_COL0 = ACC_COLS;                 // SP: metadata columns (4 per stage) after the accumulator
+constexpr uint32_t kIdescSparse = 1u << 2;       // instruction descriptor: sparse A (2:4)
 
 // MT = UMMA M tiles per item (rows per item = 128·MT). MT = 1: 3 stages, double-buffered TMEM
 // accumulator (the epilogue overlaps the next item). MT = 2: the two M tiles share every X tile
 // (half the L2 traffic per flop), 2 stages, one accumulator pair (the epilogue is exposed).
 // Each output element sees the same MMA sequence either way (W k-steps then ΔW k-steps per
 // stage), so the choice never changes a result bit.
-template <int MT>
+// SP: the delta product runs as 2:4-sparse tcgen05 MMAs (tcgen05.mma.sp, K=32 logical per
+// instruction): the dequant warps write only the kept values (bf16, compressed K-major tile) and
+// the index nibbles go to TMEM as the sparse metadata. The TMEM then holds one 256-column
+// accumulator (single-buffered) plus the metadata columns.
+template <int MT, bool SP = false>
 struct Cfg {
   static constexpr int NSTAGE = MT == 1 ? 3 : 2;
   static constexpr int NDSLOT = MT == 1 ? 4 : 2;  // native-block ring: 128-column block columns in flight
-  static constexpr int NBUF = MT == 1 ? 2 : 1;
+  static constexpr int NBUF = (MT == 1 && !SP) ? 2 : 1;
   static constexpr int W_BYTES = MT * W_TILE;
-  static constexpr int DW_BYTES = MT * W_TILE;
+  static constexpr int DW_BYTES = SP ? MT * W_TILE / 2 : MT * W_TILE;
   static constexpr int STAGE = W_BYTES + DW_BYTES + X_BYTES;
   static constexpr int DSLOT = MT * RGS * sparse_block_bytes(4);  // one 128-column block column
   static constexpr int ROWS = MT * M;
 };
 
-template <int MT>
+template <int MT, bool SP = false>
 struct Smem {
-  uint64_t full[Cfg<MT>::NSTAGE];    // TMA: W + X of the stage landed
-  uint64_t empty[Cfg<MT>::NSTAGE];   // MMA: the stage (W, ΔW, X) was consumed
-  uint64_t dq[Cfg<MT>::NSTAGE];      // dequant warps: ΔW tiles of the stage written
-  uint64_t dfull[Cfg<MT>::NDSLOT];   // TMA: native blocks of a 128-column block column landed
-  uint64_t dempty[Cfg<MT>::NDSLOT];  // dequant warps: done with the block column
+  uint64_t full[Cfg<MT, SP>::NSTAGE];    // TMA: W + X of the stage landed
+  uint64_t empty[Cfg<MT, SP>::NSTAGE];   // MMA: the stage (W, ΔW, X) was consumed
+  uint64_t dq[Cfg<MT, SP>::NSTAGE];      // dequant warps: ΔW tiles of the stage written
+  uint64_t dfull[Cfg<MT, SP>::NDSLOT];   // TMA: native blocks of a 128-column block column landed
+  uint64_t dempty[Cfg<MT, SP>::NDSLOT];  // dequant warps: done with the block column
   uint64_t tfull[2];                 // MMA: accumulator complete
   uint64_t tempty[2];                // epilogue: accumulator drained
   uint32_t tmem_base;
 };
-template <int MT>
+template <int MT, bool SP = false>
 constexpr int smem_bytes() {
-  return 1024 + Cfg<MT>::NSTAGE * Cfg<MT>::STAGE + Cfg<MT>::NDSLOT * Cfg<MT>::DSLOT +
-         static_cast<int>(sizeof(Smem<MT>));
+  return 1024 + Cfg<MT, SP>::NSTAGE * Cfg<MT, SP>::STAGE + Cfg<MT, SP>::NDSLOT * Cfg<MT, SP>::DSLOT +
+         static_cast<int>(sizeof(Smem<MT, SP>));
 }
 
 __device__ __forceinline__ void sts64(uint32_t addr, uint32_t lo, uint32_t hi) {
@@ -216,17 +222,66 @@ __device__ __forceinline__ void dequant_half(uint32_t dw, uint32_t dslot, int rg
   }
 }
 
-template <int MT>
+// SP: kept values only. Row group rg (16 rows) of the 64-column half `h` of the block column into the
+// compressed K-major tile (32 bf16 per row; element (r, c) at (r/8)*512 + (c/8)*128 + (r%8)*16 +
+// (c%8)*2). Group j of a row keeps (first, second) at compressed columns (2j, 2j+1), the order of
+// the index nibble (p0 < p1), which the metadata in TMEM describes.
+template <int FB>
+__device__ __forceinline__ void dequant_half_sp(uint32_t dw, uint32_t dslot, int rg, int n_valid, int h, int qmax,
+                                                int lane) {
+  constexpr int BB = sparse_block_bytes(FB);
+  constexpr int CODE = sparse_code_bytes(FB);
+  const int g = lane >> 2, t = lane & 3;
+  const bool valid = rg < n_valid;  // warp-uniform
+  const uint32_t blk = dslot + rg * BB;
+  float sA = 0.f, sB = 0.f;
+  if (valid) {
+    const uint2 sv = lds64(blk + CODE + kMetaBytes + g * 8);
+    sA = __uint_as_float(sv.x);
+    sB = __uint_as_float(sv.y);
+  }
+#pragma unroll
+  for (int ii = 0; ii < 2; ii++) {
+    const int i = 2 * h + ii;
+    uint32_t u[8];
+    if (FB == 4) {
+      const uint32_t w = valid ? lds32(blk + lane * 16 + i * 4) : 0x77777777u;
+#pragma unroll
+      for (int k = 0; k < 8; k++) u[k] = (w >> (4 * k)) & 0xFu;
+    } else {
+      const uint32_t w = valid ? lds32(blk + lane * 8 + h * 4) : 0x55555555u;
+      const int o = 4 * ii;
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        u[k] = (w >> (2 * (o + k))) & 3u;
+        u[k + 4] = (w >> (2 * (o + k + 8))) & 3u;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int row = kBlkRows * rg + g + ((k & 1) ? 8 : 0);
+      const int slot = t + ((k & 2) ? 4 : 0);
+      const float sc = (k & 1) ? sB : sA;
+      const float v0 = static_cast<float>(static_cast<int>(u[k]) - qmax) * sc;
+      const float v1 = static_cast<float>(static_cast<int>(u[k + 4]) - qmax) * sc;
+      const int c = 16 * ii + 2 * slot;  // compressed column
+      const uint32_t addr = dw + (row >> 3) * 512 + (c >> 3) * 128 + (row & 7) * 16 + (c & 7) * 2;
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(pack_bf16(v0, v1)) : "memory");
+    }
+  }
+}
+
+template <int MT, bool SP>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_prefill(const __grid_constant__ dz_sbmm_args a, const __grid_constant__ CUtensorMap xmap) {
-  using C = Cfg<MT>;
+  using C = Cfg<MT, SP>;
   constexpr int NSTAGE = C::NSTAGE, STAGE = C::STAGE, DSLOT = C::DSLOT, W_BYTES = C::W_BYTES;
   constexpr int DW_BYTES = C::DW_BYTES, NBUF = C::NBUF, IRG = MT * RGS;  // row groups per item
   constexpr int NDSLOT = C::NDSLOT;
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* stages = smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);
   uint8_t* dslots = stages + NSTAGE * STAGE;
-  Smem<MT>* sm = reinterpret_cast<Smem<MT>*>(dslots + NDSLOT * DSLOT);
+  Smem<MT, SP>* sm = reinterpret_cast<Smem<MT, SP>*>(dslots + NDSLOT * DSLOT);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   const int n_jobs = a.n_pf_jobs;
@@ -345,13 +400,26 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 umma_bf16(tmem_d, wdesc + 2 * k, xdesc + 2 * k, idesc, (ch | k) ? 1u : 0u);
             }
           }
+          if constexpr (SP) {
+            // compressed ΔW tile (no swizzle, [8-row group][16-B chunk][8 x 16 B]: SBO 512, LBO 128)
+            // x X: 2 sparse MMAs of K=32 logical; metadata column per MMA (E_COL0 + 4 s + ii)
+            const uint32_t tmem_d = tmem_base;
 #pragma unroll
-          for (int h = 0; h < MT; h++) {
-            const uint64_t ddesc = umma_desc_sw128(sb + W_BYTES + h * W_TILE);
-            const uint32_t tmem_d = tmem_base + (buf * MT + h) * ACC_COLS;
+            for (int ii = 0; ii < KC / 32; ii++)
+              // metadata address: the even column of the stage; sparse_id2 (idesc bits 0-1) = ii selects
+              // the column of this MMA (CUTLASS mma_traits_sm100: id2 = tmem_e & 1)
+              umma_sp_bf16(tmem_d, umma_desc_interleave(sb + W_BYTES + ii * 256, 128, 512), xdesc + 4 * ii,
+                           tmem_base + E_COL0 + 4 * s, idesc | kIdescSparse | static_cast<uint32_t>(ii),
+                           (has_base || (ch | ii)) ? 1u : 0u);
+          } else {
 #pragma unroll
-            for (int k = 0; k < KC / 16; k++)
-              umma_bf16(tmem_d, ddesc + 2 * k, xdesc + 2 * k, idesc, (has_base || (ch | k)) ? 1u : 0u);
+            for (int h = 0; h < MT; h++) {
+              const uint64_t ddesc = umma_desc_sw128(sb + W_BYTES + h * W_TILE);
+              const uint32_t tmem_d = tmem_base + (buf * MT + h) * ACC_COLS;
+#pragma unroll
+              for (int k = 0; k < KC / 16; k++)
+                umma_bf16(tmem_d, ddesc + 2 * k, xdesc + 2 * k, idesc, (has_base || (ch | k)) ? 1u : 0u);
+            }
           }
           umma_commit(&sm->empty[s]);
           if (ch == nch - 1) umma_commit(&sm->tfull[buf]);
@@ -375,15 +443,38 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int ch = 0; ch < nch; ch++) {
         if ((ch & 1) == 0) mbar_wait(&sm->dfull[ds], dph);
         mbar_wait(&sm->empty[s], ph ^ 1);  // the MMAs that last read these ΔW tiles are done
-        // warp w covers RPW consecutive row groups of the item (within one M tile)
-        constexpr int RPW = IRG / NDQ;
-        const int rg = RPW * warp, tile = rg / RGS;
-        const uint32_t dw = smem_u32(stages + s * STAGE + W_BYTES + tile * W_TILE);
-        const uint32_t dsl = smem_u32(dslots + ds * DSLOT) + tile * RGS * bb;
-        if (two_bit)
-          dequant_half<2, RPW>(dw, dsl, rg - tile * RGS, nrg - tile * RGS, ch & 1, qmax, lane);
-        else
-          dequant_half<4, RPW>(dw, dsl, rg - tile * RGS, nrg - tile * RGS, ch & 1, qmax, lane);
+        if constexpr (SP) {
+          // kept values of row group `warp` -> compressed tile; warps 0-3 also write the metadata of
+          // row groups 2q, 2q+1 into their TMEM lane quarter (lane = g + 8 h + 16 rg, column = MMA)
+          const uint32_t dw = smem_u32(stages + s * STAGE + W_BYTES);
+          const uint32_t dsl = smem_u32(dslots + ds * DSLOT);
+          if (two_bit)
+            dequant_half_sp<2>(dw, dsl, warp, nrg, ch & 1, qmax, lane);
+          else
+            dequant_half_sp<4>(dw, dsl, warp, nrg, ch & 1, qmax, lane);
+          if (warp < 4) {
+            const int rgm = 2 * warp + (lane >> 4), g = lane & 7, hh = (lane >> 3) & 1, h = ch & 1;
+            uint32_t e0 = 0x44444444u, e1 = 0x44444444u;
+            if (rgm < nrg) {
+              const uint32_t mb = dsl + rgm * bb + (two_bit ? sparse_code_bytes(2) : sparse_code_bytes(4));
+              e0 = lds32(mb + (4 * g + 0 + hh) * 8 + h * 4);  // MMA i = 2h     (i & 1 = 0)
+              e1 = lds32(mb + (4 * g + 2 + hh) * 8 + h * 4);  // MMA i = 2h + 1 (i & 1 = 1)
+            }
+            tmem_st2(tmem_base + (static_cast<uint32_t>(32 * warp) << 16) + E_COL0 + 4 * s, e0, e1);
+            tmem_st_wait();
+          }
+          tc_fence_before();
+        } else {
+          // warp w covers RPW consecutive row groups of the item (within one M tile)
+          constexpr int RPW = IRG / NDQ;
+          const int rg = RPW * warp, tile = rg / RGS;
+          const uint32_t dw = smem_u32(stages + s * STAGE + W_BYTES + tile * W_TILE);
+          const uint32_t dsl = smem_u32(dslots + ds * DSLOT) + tile * RGS * bb;
+          if (two_bit)
+            dequant_half<2, RPW>(dw, dsl, rg - tile * RGS, nrg - tile * RGS, ch & 1, qmax, lane);
+          else
+            dequant_half<4, RPW>(dw, dsl, rg - tile * RGS, nrg - tile * RGS, ch & 1, qmax, lane);
+        }
         fence_proxy_async();  // generic-proxy st.shared -> visible to the tensor core (async proxy)
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm->dq[s]);
@@ -461,7 +552,8 @@ __global__ void k_gather_rows(const uint16_t* __restrict__ X, int64_t ldx, const
 
 using namespace dz;
 
-static_assert(pf::smem_bytes<1>() <= 232448 && pf::smem_bytes<2>() <= 232448, "prefill kernel shared memory");
+static_assert(pf::smem_bytes<1>() <= 232448 && pf::smem_bytes<2>() <= 232448 && pf::smem_bytes<1, true>() <= 232448,
+              "prefill kernel shared memory");
 static_assert(pf::Cfg<1>::STAGE % 1024 == 0 && pf::Cfg<2>::STAGE % 1024 == 0 && pf::W_TILE % 1024 == 0,
               "SW128 tile alignment");
 
@@ -480,16 +572,16 @@ extern "C" int dz_gather_rows(const uint16_t* X, int64_t ldx, const int32_t* per
   return cudaGetLastError() == cudaSuccess ? DZ_OK : DZ_E_CUDA;
 }
 
-template <int MT>
+template <int MT, bool SP>
 static int launch_prefill(const dz_sbmm_args& k, const CUtensorMap& xmap, int grid, void* stream) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(pf::k_prefill<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    pf::smem_bytes<MT>());
+    attr_err = cudaFuncSetAttribute(pf::k_prefill<MT, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    pf::smem_bytes<MT, SP>());
   });
   if (attr_err != cudaSuccess) return DZ_E_CUDA;
-  return launch_pdl(1, pf::k_prefill<MT>, grid, pf::NTHREADS, pf::smem_bytes<MT>(), stream, k, xmap);
+  return launch_pdl(1, pf::k_prefill<MT, SP>, grid, pf::NTHREADS, pf::smem_bytes<MT, SP>(), stream, k, xmap);
 }
 
 // Launch K3 over jobs[0:n_pf_jobs]; X is the staged buffer (dz_sbmm passes it as X).
@@ -522,5 +614,9 @@ extern "C" int dz_sbmm_prefill(const dz_sbmm_args* a, void* stream) {
   if (e && (e[0] == '1' || e[0] == '2')) mt = e[0] - '0';
   const int n_items = mt == 2 ? items2 : items1;
   const int grid = g > n_items ? n_items : g;
-  return mt == 2 ? launch_prefill<2>(*a, xmap, grid, stream) : launch_prefill<1>(*a, xmap, grid, stream);
+  // 2:4-sparse tcgen05 delta product by default (8-23% faster than the dense-dequantised one at the
+  // 13B shapes, profiles/r01_pf_sparse.txt); DZ_PF_SPARSE=0 selects the dense variant (A/B)
+  const char* sp = std::getenv("DZ_PF_SPARSE");
+  if (!(sp && sp[0] == '0') && mt == 1) return launch_prefill<1, true>(*a, xmap, grid, stream);
+  return mt == 2 ? launch_prefill<2, false>(*a, xmap, grid, stream) : launch_prefill<1, false>(*a, xmap, grid, stream);
 }

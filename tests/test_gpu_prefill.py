@@ -180,9 +180,29 @@ def test_prefill_item_height_does_not_change_results(E, rows, cols, bits, monkey
     Xd = torch.from_numpy(X.astype(np.float32)).cuda().to(torch.bfloat16)
     plan = E.Plan(ids, table.kinds, 3, pf_min=64)
     ys = []
+    monkeypatch.setenv("DZ_PF_SPARSE", "0")  # both heights on the dense-dequantised delta product
     for mt in ("1", "2"):
         monkeypatch.setenv("DZ_PF_MT", mt)
         ys.append(E.sbmm_forward(Xd, plan, base, table, y_dtype=torch.float32))
     assert torch.equal(ys[0], ys[1])
     R = O.sbmm_matrix(W, dict(enumerate(ods)), ids, X)
     assert rel_err_rows(ys[1].cpu().double().numpy(), R).max() <= REL_TOL
+
+
+@pytest.mark.parametrize("rows,cols,bits", [(640, 512, 4), (300, 448, 2), (136, 520, 3)])
+def test_prefill_sparse_tcgen05_vs_dense(E, rows, cols, bits, monkeypatch):
+    """The default 2:4-sparse tcgen05 delta product (compressed kept values in shared memory, index
+    nibbles as TMEM metadata) against the dense-dequantised variant and the oracle."""
+    rng = np.random.default_rng(rows + 3 * bits)
+    W, ods, table, base = _setup(E, rng, rows, cols, [bits] * 3)
+    ids = _ids(rng, [256, 200, 9])
+    X = bf16_round(rng.normal(0, 1, (ids.size, cols)))
+    Xd = torch.from_numpy(X.astype(np.float32)).cuda().to(torch.bfloat16)
+    plan = E.Plan(ids, table.kinds, 3, pf_min=64)
+    ys = {}
+    for sp in ("1", "0"):
+        monkeypatch.setenv("DZ_PF_SPARSE", sp)
+        ys[sp] = E.sbmm_forward(Xd, plan, base, table, y_dtype=torch.float32).cpu().double().numpy()
+    R = O.sbmm_matrix(W, dict(enumerate(ods)), ids, X)
+    assert rel_err_rows(ys["1"], R).max() <= REL_TOL
+    assert rel_err_rows(ys["1"], ys["0"]).max() <= 1e-4  # same bf16 ΔW values, fp32 sums in another order
