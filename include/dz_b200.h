@@ -36,6 +36,12 @@ extern "C" {
 #ifndef DZ_BASE_JOB_TOKENS
 #define DZ_BASE_JOB_TOKENS 128 /* tokens per base-GEMM job of the decode kernel (its UMMA N) */
 #endif
+#ifndef DZ_PREFILL_REM_MIN
+#define DZ_PREFILL_REM_MIN 32      /* smallest remainder of a large group kept on the prefill path */
+#endif
+#ifndef DZ_PREFILL_JOB_TOKENS
+#define DZ_PREFILL_JOB_TOKENS 240 /* tokens per prefill job of K3 (its UMMA N), multiple of 16 */
+#endif
 /* ---- element types --------------------------------------------------------------- */
 #define DZ_F32 0
 #define DZ_BF16 1

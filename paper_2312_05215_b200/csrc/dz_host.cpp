@@ -61,7 +61,7 @@ extern "C" int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, in
 }
 
 // Mixed plan (prefill + decode). A group of c >= pf_min tokens with a 2:4 sparse kind sends its
-// first 256*floor(c/256) tokens (in original order) to prefill jobs of 256, plus the remainder as
+// first J*floor(c/J) tokens (in original order) to prefill jobs of J = DZ_PREFILL_JOB_TOKENS, plus the remainder as
 // one more prefill job when it still has >= pf_min tokens; prefill tokens are staged first
 // (grouped by slot in slot order). Every other token follows in its original order and is planned
 // exactly like dz_plan over the staged rows.
@@ -82,8 +82,13 @@ extern "C" int dz_plan_mixed(const int32_t* slots, int32_t T, const int32_t* kin
   std::vector<int32_t> npf(static_cast<size_t>(n_slots), 0);  // prefill tokens per slot
   for (int32_t s = 0; s < n_slots; s++) {
     if (pf_min <= 0 || count[s] < pf_min || kinds[s] == DZ_KIND_DENSE) continue;
-    const int32_t rem = count[s] % 256;
-    npf[s] = count[s] - rem + (rem >= pf_min ? rem : 0);
+    const int32_t rem = count[s] % DZ_PREFILL_JOB_TOKENS;
+    // the remainder of a group that already has full prefill jobs becomes one more (narrower)
+    // prefill job when it has >= DZ_PREFILL_REM_MIN tokens (cheaper than rem/8 decode jobs each
+    // re-streaming the delta); a group below one full job keeps the pf_min rule
+    const int32_t rmin = count[s] >= DZ_PREFILL_JOB_TOKENS ? (pf_min < DZ_PREFILL_REM_MIN ? pf_min : DZ_PREFILL_REM_MIN)
+                                                           : pf_min;
+    npf[s] = count[s] - rem + (rem >= rmin ? rem : 0);
   }
   // staged order: prefill groups by slot, then the decode tokens in original order
   std::vector<int32_t> pstart(static_cast<size_t>(n_slots) + 1, 0);
@@ -109,8 +114,10 @@ extern "C" int dz_plan_mixed(const int32_t* slots, int32_t T, const int32_t* kin
     return true;
   };
   for (int32_t s = 0; s < n_slots; s++)
-    for (int32_t off = 0; off < npf[s]; off += 256)
-      if (!push(s, pstart[s] + off, (npf[s] - off) < 256 ? (npf[s] - off) : 256, kinds[s])) return DZ_E_VALUE;
+    for (int32_t off = 0; off < npf[s]; off += DZ_PREFILL_JOB_TOKENS)
+      if (!push(s, pstart[s] + off, (npf[s] - off) < DZ_PREFILL_JOB_TOKENS ? (npf[s] - off) : DZ_PREFILL_JOB_TOKENS,
+                kinds[s]))
+        return DZ_E_VALUE;
   const int32_t n_pf = nj;
   // decode part over staged rows [t_pf, T): base jobs, then delta jobs (dz_plan's rules)
   const int32_t Td = T - t_pf;

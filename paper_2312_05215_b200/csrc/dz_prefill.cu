@@ -41,7 +41,8 @@ namespace dz {
 namespace pf {
 
 constexpr int M = 128;                      // rows per UMMA M tile
-constexpr int NMAX = 256;                   // tokens per job (UMMA N <= 256)
+constexpr int NMAX = 256;                   // X tile rows per stage (4 TMA boxes of 64 tokens)
+constexpr int NJOB = DZ_PREFILL_JOB_TOKENS; // tokens per job (UMMA N <= 256; dz_plan_mixed)
 constexpr int KC = 64;                      // columns per stage (one 128-B swizzle row)
 constexpr int NDQ = 8;                      // dequant warps
 constexpr int NEPI = 4;                     // epilogue warps
@@ -53,9 +54,12 @@ constexpr int RGS = M / kBlkRows;           // 8 row groups (native block rows) 
 constexpr int W_TILE = M * KC * 2;          // 16 KB: one W (or ΔW) tile of a stage
 constexpr int XBOX = 64;                    // tokens per X TMA box
 constexpr int X_BYTES = NMAX * KC * 2;      // 32 KB
-constexpr int ACC_COLS = NMAX;
+constexpr int ACC_COLS = NJOB;
 constexpr int TMEM_COLS = 512;
-constexpr int E_COL0 = ACC_COLS;                 // SP: metadata columns (4 per stage) after the accumulator
+// SP: the metadata columns (4 per stage) follow the accumulator(s); with jobs of <= 240 tokens two
+// accumulators still fit next to them (double-buffered), with 256-token jobs only one does.
+constexpr bool SP_DOUBLE = 2 * ACC_COLS + 32 <= TMEM_COLS;
+constexpr int E_COL0 = SP_DOUBLE ? 2 * ACC_COLS : ACC_COLS;
 constexpr uint32_t kIdescSparse = 1u << 2;       // instruction descriptor: sparse A (2:4)
 
 // MT = UMMA M tiles per item (rows per item = 128·MT). MT = 1: 3 stages, double-buffered TMEM
@@ -71,7 +75,7 @@ template <int MT, bool SP = false>
 struct Cfg {
   static constexpr int NSTAGE = MT == 1 ? 3 : 2;
   static constexpr int NDSLOT = MT == 1 ? 4 : 2;  // native-block ring: 128-column block columns in flight
-  static constexpr int NBUF = (MT == 1 && !SP) ? 2 : 1;
+  static constexpr int NBUF = MT == 1 && (!SP || SP_DOUBLE) ? 2 : 1;
   static constexpr int W_BYTES = MT * W_TILE;
   static constexpr int DW_BYTES = SP ? MT * W_TILE / 2 : MT * W_TILE;
   static constexpr int STAGE = W_BYTES + DW_BYTES + X_BYTES;
@@ -403,7 +407,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if constexpr (SP) {
             // compressed ΔW tile (no swizzle, [8-row group][16-B chunk][8 x 16 B]: SBO 512, LBO 128)
             // x X: 2 sparse MMAs of K=32 logical; metadata column per MMA (E_COL0 + 4 s + ii)
-            const uint32_t tmem_d = tmem_base;
+            const uint32_t tmem_d = tmem_base + buf * ACC_COLS;
 #pragma unroll
             for (int ii = 0; ii < KC / 32; ii++)
               // metadata address: the even column of the stage; sparse_id2 (idesc bits 0-1) = ii selects

@@ -15,6 +15,11 @@ from conftest import ROOT
 HEADER = os.path.join(ROOT, "include", "dz_b200.h")
 
 
+def _header_define(name):
+    m = re.search(rf"#define {name} (\d+)", open(HEADER).read())
+    return int(m.group(1))
+
+
 def declared_symbols():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
@@ -168,8 +173,14 @@ def test_plan_mixed_prefill_decode_host_logic():
         p = Plan(ids, kinds, D, upload=False, pf_min=64)
         T = ids.size
         cnt = np.bincount(ids, minlength=D)
-        npf = np.array([0 if (cnt[s] < 64 or kinds[s] == 3) else cnt[s] - cnt[s] % 256 + (cnt[s] % 256 if cnt[s] % 256 >= 64 else 0)
-                        for s in range(D)])
+        J, RM = _header_define("DZ_PREFILL_JOB_TOKENS"), _header_define("DZ_PREFILL_REM_MIN")
+
+        def n_prefill(c):  # dz_plan_mixed's rule (pf_min = 64)
+            if c < 64:
+                return 0
+            rmin = min(64, RM) if c >= J else 64
+            return c - c % J + (c % J if c % J >= rmin else 0)
+        npf = np.array([0 if kinds[s] == 3 else n_prefill(cnt[s]) for s in range(D)])
         assert p.t_pf == npf.sum()
         perm = p.perm_host if p.t_pf else np.arange(T)
         assert sorted(perm.tolist()) == list(range(T))
@@ -179,7 +190,7 @@ def test_plan_mixed_prefill_decode_host_logic():
         covered = []
         for k, (slot, b, c, kind) in enumerate(jobs):
             if k < p.n_pf_jobs:
-                assert 0 < c <= 256 and kind == kinds[slot] and kind != 3
+                assert 0 < c <= J and kind == kinds[slot] and kind != 3
                 rows = perm[b:b + c]
                 assert np.all(ids[rows] == slot)
                 covered += rows.tolist()

@@ -54,7 +54,7 @@ def test_prefill_vs_oracle(E, rows, cols, bits):
     X = bf16_round(rng.normal(0, 1, (ids.size, cols)))
     Xd = torch.from_numpy(X.astype(np.float32)).cuda().to(torch.bfloat16)
     plan = E.Plan(ids, table.kinds, len(counts), pf_min=64)
-    assert plan.n_pf_jobs == 2 and plan.t_pf == 406  # 300 -> 256 prefill + 44 decode; 150 -> prefill
+    assert plan.n_pf_jobs == 3 and plan.t_pf == 450  # 300 -> 240 + 60-token remainder job; 150 -> one job
     Y = E.sbmm_forward(Xd, plan, base, table, y_dtype=torch.float32)
     R = O.sbmm_matrix(W, dict(enumerate(ods)), ids, X)
     err = rel_err_rows(Y.cpu().double().numpy(), R)
