@@ -152,7 +152,8 @@ class LlamaStack:
     def linear(self, lin: FusedLinear, plan: Plan, X: torch.Tensor, Y: torch.Tensor) -> None:
         fused = lin.row_parallel and self.world > 1 and getattr(self, "peers", None) is not None \
             and plan.perm is None
-        sbmm_forward(X, plan, lin.base, lin.table, Y=Y, workspace=self.ws, tp=self.peers if fused else None)
+        sbmm_forward(X, plan, lin.base, lin.table, Y=Y, workspace=self.ws, tp=self.peers if fused else None,
+                     base_splits=getattr(self, "base_splits", 0))
         if lin.row_parallel and self.world > 1 and not fused:
             import torch.distributed as dist
             dist.all_reduce(Y, op=dist.ReduceOp.SUM, group=self.group)

@@ -56,6 +56,8 @@ def main():
     ap.add_argument("--pf-min", type=int, default=None)
     ap.add_argument("--seed", type=int, default=13)
     ap.add_argument("--sweep", action="store_true", help="cfg5: D in 1..128 x batch in 1..256, Zipf ids")
+    ap.add_argument("--base-splits", type=int, default=0, help="K-splits of the decode base GEMM (0 = by shape)")
+    ap.add_argument("--max-batch", type=int, default=256, help="sweep: largest batch")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -71,13 +73,15 @@ def main():
 
     st = LlamaStack(args.model, args.layers, args.deltas, args.bits, dev, rank=args.rank, world=args.world)
     st.world = 1  # one rank's shard timed alone: no collective in this process
+    st.base_splits = args.base_splits
     if args.sweep:
         Ds = [d for d in (1, 2, 4, 8, 16, 32, 64, 128) if d <= args.deltas]
-        Bs = (1, 2, 4, 8, 16, 32, 64, 128, 256)
+        Bs = tuple(b for b in (1, 2, 4, 8, 16, 32, 64, 128, 256) if b <= args.max_batch)
         for D in Ds:
             for B in Bs:
                 sid = zipf_ids(B, D, args.zipf or 1.5, args.seed + 1000 * D + B)
-                print(json.dumps(run(args, st, sid, dev, extra={"sweep_D": D, "batch": B})), flush=True)
+                print(json.dumps(run(args, st, sid, dev, extra={"sweep_D": D, "batch": B,
+                                                                "base_splits": args.base_splits})), flush=True)
         return
     print(json.dumps(run(args, st, ids, dev)), flush=True)
 
