@@ -119,7 +119,7 @@ typedef struct dz_sbmm_args {
   int64_t ldxs;             /* row stride of xs (elements, >= ceil128(in), % 8 == 0)  */
   int32_t base_splits;      /* K-splits of the base GEMM (1..4); 0 = chosen from (out, in) only,
                                so results never depend on the batch                     */
-  int32_t _pad3;
+  int32_t delta_splits;     /* K-splits of each decode delta job (1..2); 0 = from (out, in) only */
   const struct dz_tp_ctx* tp; /* host pointer or NULL: fused tensor-parallel reduction of a
                                row-parallel linear (decode plans only, see dz_tp_ctx)    */
   const int32_t* n_jobs_dev; /* device job count written by dz_plan_device, or NULL; when set,

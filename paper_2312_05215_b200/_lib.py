@@ -57,7 +57,7 @@ class DzSbmmArgs(C.Structure):
         ("perm", C.c_void_p), ("xs", C.c_void_p),
         ("n_pf_jobs", C.c_int32), ("t_pf", C.c_int32),
         ("ldxs", C.c_int64),
-        ("base_splits", C.c_int32), ("_pad3", C.c_int32),
+        ("base_splits", C.c_int32), ("delta_splits", C.c_int32),
         ("tp", C.c_void_p),
         ("n_jobs_dev", C.c_void_p),
     ]

@@ -141,8 +141,8 @@ __device__ __forceinline__ bool kind_dense(int kind) { return kind == 0 || kind 
 // cover BASE_RT = 128 rows (nbt tiles), delta items RT = 256 rows (nrt tiles): a base item streams
 // 2 bytes per weight against a 4-bit delta's ~0.8, so halving it keeps the long base items off the
 // launch's critical path. Each output element still gets exactly one base and one delta partial.
-__device__ __forceinline__ void item_coords(int item, int nrt, int nbt, int nsplit, int n_jobs, int n_base, int& rt,
-                                            int& j, int& sp) {
+__device__ __forceinline__ void item_coords(int item, int nrt, int nbt, int nsplit, int dsplit, int n_jobs, int n_base,
+                                            int& rt, int& j, int& sp) {
   const int nb_items = nbt * nsplit * n_base;
   if (item < nb_items) {
     j = item / (nbt * nsplit);
@@ -150,10 +150,11 @@ __device__ __forceinline__ void item_coords(int item, int nrt, int nbt, int nspl
     sp = r / nbt;
     rt = r - sp * nbt;
   } else {
-    const int k = item - nb_items, nd = n_jobs - n_base;
-    rt = k / nd;
-    j = n_base + (k - rt * nd);
-    sp = 0;
+    const int k = item - nb_items, per = (n_jobs - n_base) * dsplit;
+    rt = k / per;
+    const int r = k - rt * per;
+    j = n_base + r / dsplit;
+    sp = r - (r / dsplit) * dsplit;
   }
 }
 
@@ -163,6 +164,10 @@ __device__ __forceinline__ void item_coords(int item, int nrt, int nbt, int nspl
 // dz_sbmm_args.base_splits. The split count is never derived from the batch, so a token's
 // result does not depend on the other tokens of the call.
 __host__ __device__ inline int base_splits(int /*out*/, int /*in*/) { return 1; }
+// Default K-splits of each decode delta job: 1. Splitting the delta items of the out <= 4096 layers
+// in two measured neutral at the BASELINE batch and mixed at low batch (profiles/r01_ab_dsplit.txt),
+// so it stays an explicit knob (dz_sbmm_args.delta_splits). Never derived from the batch.
+__host__ __device__ inline int delta_splits(int /*out*/, int /*in*/) { return 1; }
 
 __device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
   int old;
@@ -430,7 +435,7 @@ __device__ __forceinline__ void drain_base_accumulator(uint32_t tmem_acc, int wa
 
 // Dense-delta job partial (mma.sync fragments) -> merge.
 __device__ __forceinline__ void merge_fragments(const float (&acc)[MR][NT_DN][4], int nt, const MergeCtx& m,
-                                                int rg0, int tcount, const int* tok_ids, int lane) {
+                                                int plane, int rg0, int tcount, const int* tok_ids, int lane) {
   const int g = lane >> 2, t = lane & 3;
 #pragma unroll
   for (int r = 0; r < MR; r++) {
@@ -442,7 +447,7 @@ __device__ __forceinline__ void merge_fragments(const float (&acc)[MR][NT_DN][4]
         for (int v = 0; v < 4; v++) {
           const int tk = n * 8 + 2 * t + (v & 1);
           const int row = row0 + g + ((v & 2) ? 8 : 0);
-          if (tk < tcount && row < m.out) merge_contribution(m, m.nsplit, tok_ids[tk], row, acc[r][n][v]);
+          if (tk < tcount && row < m.out) merge_contribution(m, plane, tok_ids[tk], row, acc[r][n][v]);
         }
       }
     }
@@ -467,9 +472,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int nbt = ceil_div(a.out, BASE_RT);
   const int n_base = a.base != nullptr ? ceil_div(a.T - a.t_pf, BASE_N) : 0;  // dz_plan: base jobs first
   const int nsplit = a.base_splits;  // resolved by the host (launch_decode)
+  const int dsplit = a.delta_splits;  // resolved by the host (launch_decode)
   // debug bit 1: base items only (probe of the base stream)
   const int n_jobs = a.n_jobs_dev != nullptr ? *a.n_jobs_dev : a.n_jobs;  // dz_plan_device writes the count
-  const int n_items = n_jobs < n_base ? 0 : nbt * nsplit * n_base + ((a.debug & 2) ? 0 : nrt * (n_jobs - n_base));
+  const int n_items =
+      n_jobs < n_base ? 0 : nbt * nsplit * n_base + ((a.debug & 2) ? 0 : nrt * (n_jobs - n_base) * dsplit);
 
   int* sched = reinterpret_cast<int*>(a.workspace);  // [0] item counter, [1] finished CTAs
   MergeCtx mctx;
@@ -520,7 +527,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // stream into L2: it depends only on resident weights, not on the predecessor's output.
     int item = blockIdx.x;
     int rt = 0, jj = 0, sp = 0;
-    if (item < n_items) item_coords(item, nrt, nbt, nsplit, n_jobs, n_base, rt, jj, sp);
+    if (item < n_items) item_coords(item, nrt, nbt, nsplit, dsplit, n_jobs, n_base, rt, jj, sp);
     dz_job job = item < n_items ? a.jobs[jj] : dz_job{0, 0, 0, 0};
     if (item < n_items && lane == 0) {
       const bool dn = kind_dense(job.kind);
@@ -531,9 +538,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int c = 0; c < PF_CHUNKS * BASE_CH && k0 + c * KC_DN < a.in; c++)
           tma_prefetch_2d(m0, k0 + c * KC_DN, rt * BASE_RT);
       } else if (dn) {
-        for (int c = 0; c < PF_CHUNKS && c < 2 * nkb; c++) tma_prefetch_2d(m0, c * (DN_HALF / 8), rt * RG);
+        const int d0 = sp * (2 * nkb) / dsplit;
+        for (int c = d0; c < d0 + PF_CHUNKS && c < 2 * nkb; c++) tma_prefetch_2d(m0, c * (DN_HALF / 8), rt * RG);
       } else {
-        for (int c = 0; c < PF_CHUNKS && c * NB_SP < nkb; c++) tma_prefetch_3d(m0, 0, c * NB_SP, rt * RG);
+        const int d0 = sp * ceil_div(nkb, NB_SP) / dsplit;
+        for (int c = d0; c < d0 + PF_CHUNKS && c * NB_SP < nkb; c++) tma_prefetch_3d(m0, 0, c * NB_SP, rt * RG);
       }
     }
     griddep_wait();
@@ -551,8 +560,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const void* amap = ent->tmap;  // address only: the descriptor stays in global memory
       const int bb = dense ? kDenseBlockBytes : sparse_block_bytes(kind_fbits(job.kind));
       // base items stream K-chunks [c0, c0 + nch) of split sp; delta items all of K
-      const int c0 = is_base ? sp * nch_base / nsplit : 0;
-      const int nch = is_base ? (sp + 1) * nch_base / nsplit - c0 : dense ? 2 * nkb : ceil_div(nkb, NB_SP);
+      const int nch_all = is_base ? nch_base : dense ? 2 * nkb : ceil_div(nkb, NB_SP);
+      const int ns = is_base ? nsplit : dsplit;
+      const int c0 = sp * nch_all / ns;
+      const int nch = (sp + 1) * nch_all / ns - c0;
       const uint32_t abytes = is_base ? static_cast<uint32_t>(BASE_RT * KC_DN * 2)
                               : dense ? static_cast<uint32_t>(A_DN) : static_cast<uint32_t>(RG * NB_SP * bb);
       // Next item: its id is fetched after chunk 0 goes out (one item of lookahead per CTA keeps
@@ -577,12 +588,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           ay = rt * BASE_RT;
         } else if (dense) {
           nb = 1;
-          col0 = ch * KC_DN;
+          col0 = (c0 + ch) * KC_DN;
           xbytes = KC_DN * 2;
-          ax = ch * (DN_HALF / 8);
+          ax = (c0 + ch) * (DN_HALF / 8);
           ay = rt * RG;
         } else {
-          const int kb0 = ch * NB_SP;
+          const int kb0 = (c0 + ch) * NB_SP;
           nb = (nkb - kb0) < NB_SP ? (nkb - kb0) : NB_SP;
           col0 = kb0 * kBlkCols;
           xbytes = nb * kBlkCols * 2;
@@ -599,8 +610,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           StageHdr h;
           h.item = item; h.rt = rt; h.kind = job.kind;
           h.tok_begin = job.tok_begin; h.tok_count = job.tok_count; h.nb = nb;
-          h.flags = (ch == 0 ? 1 : 0) | (last ? 2 : 0) | (ch << 8);  // chunk index for the X producer
-          h.pad = sp;  // base K-split: the partial slot the drain writes
+          h.flags = (ch == 0 ? 1 : 0) | (last ? 2 : 0) | ((c0 + ch) << 8);  // absolute chunk (X producer)
+          h.pad = sp;  // K-split of the item: selects the partial plane its epilogue writes
           sm->hdr[stage] = h;
           const uint32_t xb = is_base ? static_cast<uint32_t>(nb * KC_DN * BASE_N * 2)
                                       : static_cast<uint32_t>(job.tok_count * xbytes);
@@ -629,7 +640,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           item_nxt = __shfl_sync(0xffffffffu, id_nxt_raw, 0);
           if (item_nxt < n_items) {
             int j_n = 0;
-            item_coords(item_nxt, nrt, nbt, nsplit, n_jobs, n_base, rt_n, j_n, sp_n);
+            item_coords(item_nxt, nrt, nbt, nsplit, dsplit, n_jobs, n_base, rt_n, j_n, sp_n);
             job_n = a.jobs[j_n];
             if (lane == 0) prefetch_tmap((job_n.kind == 0 ? a.base : a.table + job_n.slot)->tmap);
           }
@@ -769,7 +780,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (t2 + 1 < h.tok_count) tk1 = sm->tok_ids[stage][t2 + 1];
       }
       if ((h.flags & 2) && h.kind == DZ_KIND_DENSE && nrv > 0)  // rare path: needs the stage's token list
-        merge_fragments(acc, nt, mctx, rg0, h.tok_count, sm->tok_ids[stage], lane);
+        merge_fragments(acc, nt, mctx, nsplit + h.pad, rg0, h.tok_count, sm->tok_ids[stage], lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm->empty[stage]);  // the stage is free before the epilogue
       if (lane == 0 && warp == 0) TRACE(4, h.item, stage);
@@ -804,7 +815,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               ok[i] = r < nrv && t2 + (v & 1) < h.tok_count && rw[i] < a.out;
             }
           }
-          merge_batch<4 * MR>(mctx, nsplit, tk, rw, x, ok);
+          merge_batch<4 * MR>(mctx, nsplit + h.pad, tk, rw, x, ok);
         }
         if (lane == 0 && warp == 0) TRACE(5, h.item, 0);
         if (lane == 0 && warp == 0) ITEM_TRACE(1, h.item, globaltimer());
@@ -934,7 +945,7 @@ extern "C" int dz_base_init(dz_native_delta* e, const uint16_t* W, int64_t ldw, 
 
 extern "C" size_t dz_sbmm_workspace_bytes(int32_t T, int32_t out) {
   if (T < 0 || out < 1) return 0;
-  return 256 + static_cast<size_t>(T) * out * sizeof(float) * 5;  // <= 4 base K-splits + the delta partial
+  return 256 + static_cast<size_t>(T) * out * sizeof(float) * 6;  // <= 4 base + 2 delta K-split planes
 }
 
 static int g_ctas_per_sm = 0;
@@ -974,6 +985,13 @@ static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
     if (e && e[0] >= '1' && e[0] <= '4') kargs.base_splits = e[0] - '0';
   }
   if (kargs.base_splits > 4) kargs.base_splits = 4;
+  if (kargs.delta_splits <= 0) {
+    kargs.delta_splits = delta_splits(kargs.out, kargs.in);
+    const char* e = std::getenv("DZ_DELTA_SPLITS");  // experiment override (A/B)
+    if (e && (e[0] == '1' || e[0] == '2')) kargs.delta_splits = e[0] - '0';
+  }
+  if (kargs.delta_splits > 2) kargs.delta_splits = 2;
+  if (kargs.base == nullptr) kargs.delta_splits = 1;  // single contributor: the delta writes Y directly
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   static int ctas_per_sm = 1;
@@ -996,7 +1014,7 @@ static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return DZ_E_CUDA;
     grid = sms * ctas_per_sm;
   }
-  const int n_items = ceil_div(a->out, RT) * a->n_jobs +
+  const int n_items = ceil_div(a->out, RT) * a->n_jobs * a->delta_splits +
                       ceil_div(a->out, BASE_RT) * a->base_splits * ceil_div(a->T, BASE_N);
   if (grid > n_items) grid = n_items;
   st = launch_pdl(1, k_sbmm, grid, NTHREADS, SMEM_BYTES, stream, *a, xmap);
@@ -1009,9 +1027,11 @@ static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
   if (fgrid < 1) fgrid = 1;
   const float* part = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(a->workspace) + 256);
   if (a->tp != nullptr && a->tp->world > 1)  // row-parallel shard: fused reduction over peer memory
-    return dz_tp_finalize_launch(part, a->base_splits, a->T, a->out, a->tp, a->Y, a->ldy, a->y_dtype, a->act,
+    return dz_tp_finalize_launch(part, a->base_splits + a->delta_splits - 1, a->T, a->out, a->tp, a->Y, a->ldy,
+                                 a->y_dtype, a->act,
                                  stream);
-  return launch_pdl(2, k_finalize, fgrid, 256, 0, stream, part, a->base_splits, t0, a->T, a->out, a->perm,
+  return launch_pdl(2, k_finalize, fgrid, 256, 0, stream, part, a->base_splits + a->delta_splits - 1, t0, a->T,
+                    a->out, a->perm,
                     a->Y, a->ldy, a->y_dtype, a->act);
 }
 
