@@ -268,7 +268,7 @@ def prepare_x(X: torch.Tensor) -> torch.Tensor:
 def sbmm_forward(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: DeltaTable,
                  y_dtype: torch.dtype = torch.bfloat16, act: int = L.DZ_ACT_NONE, Y: torch.Tensor | None = None,
                  workspace: Workspace | None = None, grid: int = 0, debug: int = 0,
-                 base_splits: int = 0, tp=None) -> torch.Tensor:
+                 base_splits: int = 0, tp=None, delta_splits: int = 0) -> torch.Tensor:
     """Y[T, out] = X W_base^T + ΔW_{slot(t)} x_t for all t, one fused launch (inference.py:126-154)."""
     T, inp = int(X.shape[0]), int(X.shape[1])
     out = table.out if base is None else base.out
@@ -296,6 +296,7 @@ def sbmm_forward(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: De
     a.grid = grid
     a.debug = debug
     a.base_splits = base_splits  # 0 = by shape (batch-independent); 1..4 = explicit K-splits of the base
+    a.delta_splits = delta_splits  # 0 = by shape; 1..2 = explicit K-splits of each decode delta job
     if tp is not None:  # peer.PeerGroup: row-parallel shard, reduced over peer memory by the finalize
         a.tp = C.addressof(tp.ctx)
     if isinstance(plan, DevicePlan):

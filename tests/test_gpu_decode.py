@@ -47,3 +47,24 @@ def test_base_splits_agree_and_batch_invariant(E, rows, cols):
     R = O.sbmm_matrix(W.float().double().cpu().numpy(), dict(enumerate(ods)), ids, X.float().double().cpu().numpy())
     err = np.linalg.norm(ys[4].double().cpu().numpy() - R, axis=1) / np.linalg.norm(R, axis=1)
     assert err.max() <= 1e-2
+
+
+@pytest.mark.parametrize("bits", [4, 2])
+def test_delta_splits_agree_and_batch_invariant(E, bits):
+    rng = np.random.default_rng(77 + bits)
+    rows, cols, D, T = 384, 2048, 6, 33
+    ods = [O.random_packed_delta(rng, rows, cols, bits) for _ in range(D)]
+    table = E.DeltaTable([E.NativeDelta.from_layer_delta(o) for o in ods], rows, cols)
+    base = E.NativeBase((torch.randn(rows, cols, device="cuda") / np.sqrt(cols)).to(torch.bfloat16))
+    ids = rng.integers(0, D, T).astype(np.int32)
+    X = torch.randn(T, cols, device="cuda").to(torch.bfloat16)
+    plan = E.Plan(ids, table.kinds, D)
+    y1 = E.sbmm_forward(X, plan, base, table, y_dtype=torch.float32, delta_splits=1)
+    y2 = E.sbmm_forward(X, plan, base, table, y_dtype=torch.float32, delta_splits=2, base_splits=2)
+    assert torch.equal(y2, E.sbmm_forward(X, plan, base, table, y_dtype=torch.float32, delta_splits=2, base_splits=2))
+    sel = np.array([1, 5, 30])
+    ysub = E.sbmm_forward(X[torch.from_numpy(sel).cuda()].contiguous(), E.Plan(ids[sel], table.kinds, D), base, table,
+                          y_dtype=torch.float32, delta_splits=2, base_splits=2)
+    assert torch.equal(ysub, y2[torch.from_numpy(sel).cuda()])
+    rel = (torch.linalg.norm(y2 - y1, dim=1) / torch.linalg.norm(y1, dim=1)).max().item()
+    assert rel < 1e-5, rel
