@@ -124,6 +124,8 @@ typedef struct dz_sbmm_args {
                                row-parallel linear (decode plans only, see dz_tp_ctx)    */
   const int32_t* n_jobs_dev; /* device job count written by dz_plan_device, or NULL; when set,
                                n_jobs is only the capacity of `jobs` (grid sizing)       */
+  int32_t fin_inline;       /* set by dz_sbmm (callers leave 0): finalize inside the kernel */
+  int32_t _pad4;
 } dz_sbmm_args;
 
 /* Fused tensor-parallel reduction over peer memory (NVLink / NVSwitch), replacing the

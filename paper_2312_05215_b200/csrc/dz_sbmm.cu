@@ -454,6 +454,89 @@ __device__ __forceinline__ void merge_fragments(const float (&acc)[MR][NT_DN][4]
   }
 }
 
+__device__ __forceinline__ void finalize_rows(const float* __restrict__ part, int nsplit, int t0, int T, int out,
+                                              const int32_t* __restrict__ perm, void* __restrict__ Y, int64_t ldy,
+                                              int y_dtype, int act, int64_t first, int64_t stride) {
+  const int64_t plane = static_cast<int64_t>(T) * out;
+  const bool vec = (out % 4) == 0 && (ldy % 4) == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
+  if (vec) {
+    const int o4 = out / 4;
+    const int64_t n = static_cast<int64_t>(T - t0) * o4;
+    for (int64_t i = first; i < n; i += stride) {
+      const int t = t0 + static_cast<int>(i / o4), r = 4 * static_cast<int>(i % o4);
+      const float* p = part + static_cast<int64_t>(t) * out + r;
+      float4 v = __ldcg(reinterpret_cast<const float4*>(p));
+      for (int sp = 1; sp <= nsplit; sp++) {
+        const float4 w = __ldcg(reinterpret_cast<const float4*>(p + sp * plane));
+        v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+      }
+      if (act == DZ_ACT_TANH) { v.x = tanhf(v.x); v.y = tanhf(v.y); v.z = tanhf(v.z); v.w = tanhf(v.w); }
+      const int yr = perm != nullptr ? __ldg(perm + t) : t;
+      const int64_t yo = static_cast<int64_t>(yr) * ldy + r;
+      if (y_dtype == DZ_F32) {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(Y) + yo) = v;
+      } else {
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+        uint2 w;
+        w.x = *reinterpret_cast<const uint32_t*>(&lo);
+        w.y = *reinterpret_cast<const uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(Y) + yo) = w;
+      }
+    }
+  } else {
+    const int64_t n = static_cast<int64_t>(T - t0) * out;
+    for (int64_t i = first; i < n; i += stride) {
+      const int t = t0 + static_cast<int>(i / out), r = static_cast<int>(i % out);
+      const float* p = part + static_cast<int64_t>(t) * out + r;
+      float v = __ldcg(p);
+      for (int sp = 1; sp <= nsplit; sp++) v += __ldcg(p + sp * plane);
+      if (act == DZ_ACT_TANH) v = tanhf(v);
+      const int yr = perm != nullptr ? __ldg(perm + t) : t;
+      const int64_t yo = static_cast<int64_t>(yr) * ldy + r;
+      if (y_dtype == DZ_F32)
+        reinterpret_cast<float*>(Y)[yo] = v;
+      else
+        reinterpret_cast<__nv_bfloat16*>(Y)[yo] = __float2bfloat16_rn(v);
+    }
+  }
+}
+
+// Finalize the merged decode rows [t0, T): Y[perm[t]][r] = act(((P_0 + P_1) + ... + P_{S-1}) + P_S)
+// with P_s the base K-split partials and the delta partials after them — a fixed summation order,
+// so the result is deterministic and independent of the batch. With DZ_FIN_INLINE=1, k_sbmm runs
+// the same code itself after a grid barrier instead.
+__global__ void __launch_bounds__(256) k_finalize(const float* __restrict__ part, int nsplit, int t0, int T, int out,
+                                                  const int32_t* __restrict__ perm, void* __restrict__ Y, int64_t ldy,
+                                                  int y_dtype, int act) {
+  griddep_wait();
+  griddep_launch_dependents();
+  finalize_rows(part, nsplit, t0, T, out, perm, Y, ldy, y_dtype, act,
+                blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x, static_cast<int64_t>(gridDim.x) * blockDim.x);
+}
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Sense-reversal grid barrier over co-resident CTAs (count + generation words in the workspace).
+__device__ __forceinline__ void grid_sync(unsigned* count, unsigned* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = ld_acquire_u32(gen);
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *count = 0;
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(g + 1) : "memory");
+    } else {
+      while (ld_acquire_u32(gen) == g) __nanosleep(32);
+    }
+  }
+  __syncthreads();
+}
+
 // ------------------------------------------------------------------------------------------
 // The persistent kernel
 // ------------------------------------------------------------------------------------------
@@ -828,62 +911,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, TMEM_COLS);
   }
+  if (a.fin_inline && a.base != nullptr && !(a.debug & 4)) {
+    // every partial plane of every CTA written -> finalize here (no separate launch)
+    unsigned* sync = reinterpret_cast<unsigned*>(a.workspace) + 2;
+    grid_sync(sync, sync + 1);
+    finalize_rows(mctx.part, nsplit + dsplit - 1, a.t_pf, a.T, a.out, a.perm, a.Y, a.ldy, a.y_dtype, a.act,
+                  blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x,
+                  static_cast<int64_t>(gridDim.x) * blockDim.x);
+  }
 }
 
 // Finalize the merged decode rows [t0, T): Y[perm[t]][r] = act(((P_0 + P_1) + ... + P_{S-1}) + P_S)
 // with P_s the base K-split partials and P_S the delta partial — a fixed summation order, so the
 // result is deterministic and independent of the batch. Runs after k_sbmm in the same stream
 // (programmatic dependent launch).
-__global__ void __launch_bounds__(256) k_finalize(const float* __restrict__ part, int nsplit, int t0, int T, int out,
-                                                  const int32_t* __restrict__ perm, void* __restrict__ Y, int64_t ldy,
-                                                  int y_dtype, int act) {
-  griddep_wait();
-  griddep_launch_dependents();
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  const int64_t plane = static_cast<int64_t>(T) * out;
-  const bool vec = (out % 4) == 0 && (ldy % 4) == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
-  if (vec) {
-    const int o4 = out / 4;
-    const int64_t n = static_cast<int64_t>(T - t0) * o4;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
-      const int t = t0 + static_cast<int>(i / o4), r = 4 * static_cast<int>(i % o4);
-      const float* p = part + static_cast<int64_t>(t) * out + r;
-      float4 v = __ldcs(reinterpret_cast<const float4*>(p));
-      for (int sp = 1; sp <= nsplit; sp++) {
-        const float4 w = __ldcs(reinterpret_cast<const float4*>(p + sp * plane));
-        v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
-      }
-      if (act == DZ_ACT_TANH) { v.x = tanhf(v.x); v.y = tanhf(v.y); v.z = tanhf(v.z); v.w = tanhf(v.w); }
-      const int yr = perm != nullptr ? __ldg(perm + t) : t;
-      const int64_t yo = static_cast<int64_t>(yr) * ldy + r;
-      if (y_dtype == DZ_F32) {
-        *reinterpret_cast<float4*>(reinterpret_cast<float*>(Y) + yo) = v;
-      } else {
-        const __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
-        uint2 w;
-        w.x = *reinterpret_cast<const uint32_t*>(&lo);
-        w.y = *reinterpret_cast<const uint32_t*>(&hi);
-        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(Y) + yo) = w;
-      }
-    }
-  } else {
-    const int64_t n = static_cast<int64_t>(T - t0) * out;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
-      const int t = t0 + static_cast<int>(i / out), r = static_cast<int>(i % out);
-      const float* p = part + static_cast<int64_t>(t) * out + r;
-      float v = p[0];
-      for (int sp = 1; sp <= nsplit; sp++) v += p[sp * plane];
-      if (act == DZ_ACT_TANH) v = tanhf(v);
-      const int yr = perm != nullptr ? __ldg(perm + t) : t;
-      const int64_t yo = static_cast<int64_t>(yr) * ldy + r;
-      if (y_dtype == DZ_F32)
-        reinterpret_cast<float*>(Y)[yo] = v;
-      else
-        reinterpret_cast<__nv_bfloat16*>(Y)[yo] = __float2bfloat16_rn(v);
-    }
-  }
-}
-
 }  // namespace dz
 
 using namespace dz;
@@ -976,6 +1017,16 @@ extern "C" int dz_sbmm_ctas_per_sm(void) {
 extern "C" int dz_tp_finalize_launch(const float* part, int nsplit, int T, int out, const dz_tp_ctx* ctx, void* Y,
                                      int64_t ldy, int y_dtype, int act, void* stream);
 
+static int sms_count() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
 static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
   dz_sbmm_args kargs = *a_in;
   const dz_sbmm_args* a = &kargs;
@@ -1017,8 +1068,13 @@ static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
   const int n_items = ceil_div(a->out, RT) * a->n_jobs * a->delta_splits +
                       ceil_div(a->out, BASE_RT) * a->base_splits * ceil_div(a->T, BASE_N);
   if (grid > n_items) grid = n_items;
+  // DZ_FIN_INLINE=1: finalize inside k_sbmm after a grid barrier (every CTA is resident: grid <=
+  // SMs x 1) instead of a separate k_finalize launch. Off by default: inside a CUDA graph the
+  // separate launch measured 0.7-1.7% faster (profiles/r01_ab_fin_inline.txt).
+  const char* fe = std::getenv("DZ_FIN_INLINE");
+  kargs.fin_inline = (a->tp == nullptr || a->tp->world <= 1) && (fe && fe[0] == '1') && grid <= sms_count() ? 1 : 0;
   st = launch_pdl(1, k_sbmm, grid, NTHREADS, SMEM_BYTES, stream, *a, xmap);
-  if (st || a->base == nullptr || (a->debug & 4)) return st;
+  if (st || a->base == nullptr || (a->debug & 4) || kargs.fin_inline) return st;
   // merged rows -> Y (+ activation), accumulator re-zeroed
   const int t0 = a->t_pf;
   const int64_t work = static_cast<int64_t>(a->T - t0) * a->out / 4;
