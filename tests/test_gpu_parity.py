@@ -307,3 +307,17 @@ def test_full_size_llama_linear(P, out_f, in_f, bits):
     Wh = Wt.float().double().cpu().numpy()
     Ro = O.sbmm_matrix(Wh, dict(enumerate(ods)), ids[:2], Xh)
     assert rel_err_rows(Y[:2].double().cpu().numpy(), Ro).max() <= REL_TOL
+
+
+def test_sbmm_api_large_group_takes_prefill_path(P):
+    """The drop-in `sbmm` (inference.py:126-154) on a batch whose main group is above the prefill
+    threshold: the mixed plan (K3 tcgen05 prefill + K2 decode) matches the reference oracle."""
+    from paper_2312_05215_b200.engine import PF_MIN
+    rng = np.random.default_rng(31)
+    W, ods, pds, X, _ = _random_case(P, rng, 192, 384, 4, 3, 8)
+    ids = np.concatenate([np.zeros(PF_MIN + 50, np.int64), rng.integers(1, 3, 20)])
+    X = bf16_round(rng.normal(0, 1, size=(ids.size, 384)))
+    out = P.sbmm(W, pds, P.BatchInput([(i, int(d), X[i]) for i, d in enumerate(ids)]))
+    Y = np.stack([out[i] for i in range(ids.size)])
+    R = O.sbmm_matrix(W, ods, ids, X)
+    assert rel_err_rows(Y, R).max() <= REL_TOL
