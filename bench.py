@@ -291,6 +291,9 @@ def main():
     plan = Plan(ids, kinds, D_DELTAS, device=device)
     assert plan.t_pf == 0  # 2 tokens per delta: pure decode plan
     bufs = st.buffers(T_TOKENS)
+    tail_pf = world == 1 and os.environ.get("DZ_TAIL_PREFETCH", "1") != "0"
+    if tail_pf:  # each launch warms L2 with the next launch's first weight stages at its tail
+        st.prepare_chain(plan, bufs)
     stream = torch.cuda.current_stream()
 
     st.step(plan, bufs)  # eager warm-up (sets kernel attributes, NCCL communicators)
@@ -384,6 +387,8 @@ def main():
         hid = bufs["x"].shape[1]
         dplan = DevicePlan(T_TOKENS, kinds, D_DELTAS, device=device)
         slots_dev = torch.zeros(T_TOKENS, dtype=torch.int32, device=device)
+        if tail_pf:
+            st.prepare_chain(dplan, bufs)
         sets = []
         for _ in range(2):
             io = {"x": torch.randn(T_TOKENS, hid).to(torch.bfloat16).pin_memory(),

@@ -126,6 +126,9 @@ typedef struct dz_sbmm_args {
                                n_jobs is only the capacity of `jobs` (grid sizing)       */
   int32_t fin_inline;       /* set by dz_sbmm (callers leave 0): finalize inside the kernel */
   int32_t _pad4;
+  const struct dz_sbmm_args* next; /* device copy of the NEXT linear's args in the step, or NULL:
+                               CTAs that run out of items warm L2 with the first weight stages
+                               their blockIdx gets in that launch (decode plans only)      */
 } dz_sbmm_args;
 
 /* Fused tensor-parallel reduction over peer memory (NVLink / NVSwitch), replacing the

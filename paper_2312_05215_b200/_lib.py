@@ -61,6 +61,7 @@ class DzSbmmArgs(C.Structure):
         ("tp", C.c_void_p),
         ("n_jobs_dev", C.c_void_p),
         ("fin_inline", C.c_int32), ("_pad4", C.c_int32),
+        ("next", C.c_void_p),
     ]
 
 

@@ -537,6 +537,39 @@ __device__ __forceinline__ void grid_sync(unsigned* count, unsigned* gen) {
   __syncthreads();
 }
 
+// Tail prefetch: a CTA with no more items warms L2 with the first weight stages of the item its
+// blockIdx takes first in the next linear of the step (items [0, grid) are static there), so the
+// launch boundary keeps HBM busy with bytes the next launch reads anyway.
+constexpr int TAIL_PF_CHUNKS = 6;
+__device__ __forceinline__ void tail_prefetch(const dz_sbmm_args& nx) {
+  if (nx.perm != nullptr || nx.T <= 0) return;  // decode plans only
+  const int nrt = ceil_div(nx.out, RT), nbt = ceil_div(nx.out, BASE_RT), nkb = ceil_div(nx.in, kBlkCols);
+  const int nch_base = ceil_div(nx.in, BASE_CH * KC_DN);
+  const int n_base = nx.base != nullptr ? ceil_div(nx.T, BASE_N) : 0;
+  const int n_jobs = nx.n_jobs_dev != nullptr ? *nx.n_jobs_dev : nx.n_jobs;
+  const int nsplit = nx.base_splits > 0 ? nx.base_splits : base_splits(nx.out, nx.in);
+  const int dsplit = nx.base == nullptr ? 1 : nx.delta_splits > 0 ? nx.delta_splits : delta_splits(nx.out, nx.in);
+  const int n_items = n_jobs < n_base ? 0 : nbt * nsplit * n_base + nrt * (n_jobs - n_base) * dsplit;
+  const int item = blockIdx.x;
+  if (item >= n_items) return;
+  int rt = 0, jj = 0, sp = 0;
+  item_coords(item, nrt, nbt, nsplit, dsplit, n_jobs, n_base, rt, jj, sp);
+  const dz_job job = nx.jobs[jj];
+  const dz_native_delta* e = job.kind == 0 ? nx.base : nx.table + job.slot;
+  const void* m = e->tmap;
+  if (job.kind == 0) {
+    const int k0 = (sp * nch_base / nsplit) * BASE_CH * KC_DN;
+    for (int c = 0; c < TAIL_PF_CHUNKS * BASE_CH && k0 + c * KC_DN < nx.in; c++)
+      tma_prefetch_2d(m, k0 + c * KC_DN, rt * BASE_RT);
+  } else if (kind_dense(job.kind)) {
+    const int d0 = sp * (2 * nkb) / dsplit;
+    for (int c = d0; c < d0 + TAIL_PF_CHUNKS && c < 2 * nkb; c++) tma_prefetch_2d(m, c * (DN_HALF / 8), rt * RG);
+  } else {
+    const int d0 = sp * ceil_div(nkb, NB_SP) / dsplit;
+    for (int c = d0; c < d0 + TAIL_PF_CHUNKS && c * NB_SP < nkb; c++) tma_prefetch_3d(m, 0, c * NB_SP, rt * RG);
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // The persistent kernel
 // ------------------------------------------------------------------------------------------
@@ -742,6 +775,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tok = tok_n;
       tok2 = tok2_n;
     }
+    if (a.next != nullptr && lane == 0) tail_prefetch(*a.next);
     mbar_wait(&sm->empty[stage], phase ^ 1);
     if (lane == 0) {
       sm->hdr[stage].item = -1;

@@ -52,7 +52,11 @@ __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
       *count = 0;
       st_release_gpu(gen, g + 1);
     } else {
-      while (ld_acquire_gpu(gen) == g) __nanosleep(64);
+      long long spins = 0;
+      while (ld_acquire_gpu(gen) == g) {
+        __nanosleep(64);
+        if (++spins > (1ll << 27)) __trap();
+      }
     }
   }
   __syncthreads();
@@ -84,10 +88,15 @@ __global__ void __launch_bounds__(256) k_tp_finalize(const float* __restrict__ p
     for (int p = 0; p < tp.world; p++) st_release_sys(tp.peer_flags[p] + tp.rank, e);
     tp.sync[0] = static_cast<unsigned>(e);
   }
-  // 3. wait for every peer's buffer of this epoch
+  // 3. wait for every peer's buffer of this epoch (bounded: a peer that never arrives aborts the
+  //    kernel after ~10 s instead of hanging the GPU)
   if (threadIdx.x < tp.world) {
     const int* f = tp.peer_flags[tp.rank] + threadIdx.x;
-    while (ld_acquire_sys(f) < e) __nanosleep(128);
+    long long spins = 0;
+    while (ld_acquire_sys(f) < e) {
+      __nanosleep(128);
+      if (++spins > (1ll << 26)) __trap();
+    }
   }
   __syncthreads();
   // 4. rank-order sum over peer memory -> Y

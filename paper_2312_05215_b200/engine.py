@@ -268,8 +268,23 @@ def prepare_x(X: torch.Tensor) -> torch.Tensor:
 def sbmm_forward(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: DeltaTable,
                  y_dtype: torch.dtype = torch.bfloat16, act: int = L.DZ_ACT_NONE, Y: torch.Tensor | None = None,
                  workspace: Workspace | None = None, grid: int = 0, debug: int = 0,
-                 base_splits: int = 0, tp=None, delta_splits: int = 0) -> torch.Tensor:
-    """Y[T, out] = X W_base^T + ΔW_{slot(t)} x_t for all t, one fused launch (inference.py:126-154)."""
+                 base_splits: int = 0, tp=None, delta_splits: int = 0, next_args: int = 0) -> torch.Tensor:
+    """Y[T, out] = X W_base^T + ΔW_{slot(t)} x_t for all t, one fused launch (inference.py:126-154).
+
+    next_args: device address of the next linear's dz_sbmm_args (see `sbmm_args`), or 0; CTAs that
+    run out of work then warm L2 with that launch's first weight stages."""
+    a, Y, keep = sbmm_args(X, plan, base, table, y_dtype, act, Y, workspace, grid, debug, base_splits, tp,
+                           delta_splits)
+    a.next = next_args or None
+    L.check(L.lib().dz_sbmm(C.byref(a), stream_ptr()), "sbmm")
+    return Y
+
+
+def sbmm_args(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: DeltaTable,
+              y_dtype: torch.dtype = torch.bfloat16, act: int = L.DZ_ACT_NONE, Y: torch.Tensor | None = None,
+              workspace: Workspace | None = None, grid: int = 0, debug: int = 0,
+              base_splits: int = 0, tp=None, delta_splits: int = 0):
+    """The dz_sbmm_args of one launch (plus Y and the tensors the args point to)."""
     T, inp = int(X.shape[0]), int(X.shape[1])
     out = table.out if base is None else base.out
     if base is not None and (base.out, base.inp) != (table.out, table.inp):
@@ -301,13 +316,19 @@ def sbmm_forward(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: De
         a.tp = C.addressof(tp.ctx)
     if isinstance(plan, DevicePlan):
         a.n_jobs_dev = plan.n_jobs_dev.data_ptr()
+    xs = None
     if plan.perm is not None:  # mixed plan: staged (permuted) copy of X, compact padded rows
         ldxs = _ceil(inp, BLK_COLS) * BLK_COLS
         xs = torch.empty(T, ldxs, dtype=torch.bfloat16, device=X.device)
         a.perm, a.xs, a.ldxs = plan.perm.data_ptr(), xs.data_ptr(), ldxs
         a.n_pf_jobs, a.t_pf = plan.n_pf_jobs, plan.t_pf
-    L.check(L.lib().dz_sbmm(C.byref(a), stream_ptr()), "sbmm")
-    return Y
+    return a, Y, (Xp, xs, ws)
+
+
+def args_to_device(args: list, device) -> torch.Tensor:
+    """Device copy of a list of dz_sbmm_args (for `next_args` chains)."""
+    raw = b"".join(C.string_at(C.addressof(a), C.sizeof(a)) for a in args)
+    return torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(device)
 
 
 def concat_rows(parts: list[NativeDelta]) -> NativeDelta:

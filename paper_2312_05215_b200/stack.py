@@ -28,6 +28,7 @@ from .engine import DeltaTable, NativeBase, NativeDelta, Plan, Workspace, concat
 from .synth import delta_algorithmic_bytes, llama_linears, random_base, random_native_delta
 
 FUSED = {"qkv": ("q", "k", "v"), "o": ("o",), "gate_up": ("gate", "up"), "down": ("down",)}
+C_SIZEOF_ARGS = __import__("ctypes").sizeof(L.DzSbmmArgs)
 STEP_ORDER = (("qkv", "h"), ("o", "v"), ("gate_up", "h"), ("down", "up"))
 ROW_PARALLEL = ("o", "down")
 
@@ -149,26 +150,47 @@ class LlamaStack:
             self.peers = None
             print(f"[dz] fused TP reduction unavailable ({e}); using the NCCL all-reduce", file=sys.stderr)
 
-    def linear(self, lin: FusedLinear, plan: Plan, X: torch.Tensor, Y: torch.Tensor) -> None:
+    def linear(self, lin: FusedLinear, plan: Plan, X: torch.Tensor, Y: torch.Tensor, next_args: int = 0) -> None:
         fused = lin.row_parallel and self.world > 1 and getattr(self, "peers", None) is not None \
             and plan.perm is None
         sbmm_forward(X, plan, lin.base, lin.table, Y=Y, workspace=self.ws, tp=self.peers if fused else None,
-                     base_splits=getattr(self, "base_splits", 0))
+                     base_splits=getattr(self, "base_splits", 0), next_args=next_args)
         if lin.row_parallel and self.world > 1 and not fused:
             import torch.distributed as dist
             dist.all_reduce(Y, op=dist.ReduceOp.SUM, group=self.group)
 
+    def prepare_chain(self, plan: Plan, bufs: dict[str, torch.Tensor]) -> None:
+        """Device copies of every launch's args in step order, so each launch can point its tail
+        prefetch at the next one (`sbmm_forward(next_args=...)`). Single GPU, decode plans."""
+        from .engine import args_to_device, sbmm_args
+        args, h = [], bufs["x"]
+        for lin in self.stack:
+            src = {"h": h, "v": bufs["v"], "up": bufs["up"]}
+            for f, s_ in STEP_ORDER:
+                a, _, _ = sbmm_args(src[s_], plan, lin[f].base, lin[f].table, Y=bufs[f], workspace=self.ws,
+                                    base_splits=getattr(self, "base_splits", 0))
+                args.append(a)
+            h = bufs["down"]
+        if not hasattr(self, "chains"):
+            self.chains = {}
+        self.chains[(id(plan), bufs["x"].data_ptr())] = (plan, args_to_device(args, self.device))
+
     def step(self, plan: Plan, bufs: dict[str, torch.Tensor], record=None) -> torch.Tensor:
         """One decode step through every layer; returns the last layer's output buffer."""
-        h = bufs["x"]
+        chain = getattr(self, "chains", {}).get((id(plan), bufs["x"].data_ptr()))
+        use_chain = chain is not None and chain[0] is plan and self.world == 1
+        n_lin = len(self.stack) * len(STEP_ORDER)
+        h, k = bufs["x"], 0
         for lin in self.stack:
             src = {"h": h, "v": bufs["v"], "up": bufs["up"]}
             for f, s_ in STEP_ORDER:
                 if record is not None:
                     record(f, "begin")
-                self.linear(lin[f], plan, src[s_], bufs[f])
+                nxt = chain[1].data_ptr() + (k + 1) * C_SIZEOF_ARGS if use_chain and k + 1 < n_lin else 0
+                self.linear(lin[f], plan, src[s_], bufs[f], next_args=nxt)
                 if record is not None:
                     record(f, "end")
+                k += 1
             h = bufs["down"]
         return h
 
