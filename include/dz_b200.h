@@ -276,6 +276,28 @@ int dz_dzdl_parse_layers(const uint8_t* buf, int64_t len, int64_t layers_off, in
  * *out_len = inflated bytes; DZ_E_FORMAT = corrupt stream; DZ_E_ENCODING = dst too small
  * (*out_len = the size needed; call again). dst may be NULL to size the output. */
 int dz_inflate(const uint8_t* src, int64_t n, uint8_t* dst, int64_t cap, int64_t* out_len);
+/* ---- GPU ΔCompress ---------------------------------------------------
+ * obs_compress_layer (compress.py:348-464): greedy OBS column solver over a layer delta with
+ * 2:4 keep masks (_keep_mask_groups compress.py:204-215) and per-(row, group) symmetric RTN.
+ * W     [rows, cols] f64 device, the delta; overwritten with the quantized delta (the solver's
+ *       final `w`, i.e. dequantize_layer of the result) — the caller's propagation input.
+ * U     [cols, cols] f64 device, upper Cholesky factor of H^-1 (_inverse_cholesky_factor,
+ *       compress.py:321-336; computed by the caller, e.g. cuSOLVER).
+ * packed  n_words u32 (bits < 16: ceil(n / (32/bits)), n = rows*cols/2 under 2:4 else rows*cols;
+ *         bits 16: 2 words per stored f64 value)
+ * index   rows*cols/8 bytes (2:4 only), scales rows*ceil(cols/gs) f32 (bits < 16 only),
+ * proxy_loss one f64. Stream-ordered; workspace from dz_obs_workspace_bytes. */
+typedef struct dz_obs_cfg {
+  int32_t bits;       /* 2, 3, 4, 8, or 16 (identity quantizer: values stored raw) */
+  int32_t sparse;     /* 1 = two_of_four */
+  int32_t group_size;
+  int32_t block_size; /* <= 256; multiple of 4 under 2:4 */
+} dz_obs_cfg;
+size_t dz_obs_workspace_bytes(int32_t rows, int32_t cols, const dz_obs_cfg* cfg);
+int dz_obs_compress(double* W, const double* U, int32_t rows, int32_t cols, const dz_obs_cfg* cfg,
+                    uint32_t* packed, uint8_t* index, float* scales, double* proxy_loss, void* ws,
+                    size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -354,3 +354,97 @@ def random_packed_delta(rng: np.random.Generator, rows: int, cols: int, bits: in
     return OracleDelta(rows=rows, cols=cols, packed_values=words, index_stream=index,
                        scales=scales, bits=bits,
                        sparsity=SPARSITY_2_4 if sparse else SPARSITY_NONE, group_size=group_size)
+
+
+# --------------------------------------------------------------------------- ΔCompress solver
+# (the offline producer of packed deltas, restated for the GPU solver's tests)
+
+
+def compute_hessian(samples: np.ndarray, damping: float) -> np.ndarray:
+    """H = X X^T + damping * mean(diag(X X^T)) * I  (compress.py:178-186)."""
+    x = np.asarray(samples, dtype=np.float64)
+    h = x @ x.T
+    h[np.diag_indices_from(h)] += damping * float(np.mean(np.diag(h)))
+    return h
+
+
+def inverse_cholesky_factor(hessian: np.ndarray) -> np.ndarray:
+    """Upper U with H^-1 = U^T U (compress.py:321-336), via LAPACK like the reference."""
+    import scipy.linalg as sla
+    try:
+        cf = sla.cho_factor(hessian, lower=True, check_finite=False)
+        hinv = sla.cho_solve(cf, np.eye(hessian.shape[0]), check_finite=False)
+        return sla.cholesky(hinv, lower=False, check_finite=False)
+    except (np.linalg.LinAlgError, sla.LinAlgError, ValueError) as exc:
+        raise OracleError("NumericDomainError", f"hessian is not positive definite: {exc}") from exc
+
+
+def keep_mask_groups(w4: np.ndarray, hd: np.ndarray) -> np.ndarray:
+    """2:4 keep-mask per row of 4 (compress.py:204-215): prune the two smallest saliencies
+    w^2 / hd, ties to the lower index (stable order)."""
+    sal = w4 * w4 / hd
+    rank = np.argsort(np.argsort(sal, axis=1, kind="stable"), axis=1, kind="stable")
+    return rank >= 2
+
+
+def obs_compress_layer(delta, hessian, bits: int, sparsity: str, group_size: int, block_size: int,
+                       u: np.ndarray | None = None):
+    """Greedy OBS column solver (compress.py:348-464). Returns (OracleDelta, proxy_loss,
+    quantized dense f64 delta). `u` overrides the inverse-Hessian factor (the GPU tests pass
+    the same factor to both sides)."""
+    w = np.array(delta, dtype=np.float64)
+    r, c = w.shape
+    sparse = sparsity == SPARSITY_2_4
+    passthrough = bits == 16
+    if passthrough and not sparse:  # compress.py:372-385
+        return (OracleDelta(rows=r, cols=c, packed_values=float64_payload(w), index_stream=b"",
+                            scales=np.zeros(0, "<f4"), bits=bits, sparsity=sparsity,
+                            group_size=group_size), 0.0, w.copy())
+    if u is None:
+        u = inverse_cholesky_factor(np.asarray(hessian, dtype=np.float64))
+    ud = np.diag(u)
+    q = _qmax(bits)
+    ng = -(-c // group_size)
+    keep = np.ones((r, c), dtype=bool)
+    codes = np.zeros((r, c), dtype=np.int64)
+    quant = np.zeros((r, c))
+    scales = np.zeros((r, ng))
+    loss = 0.0
+    for b0 in range(0, c, block_size):
+        b1 = min(b0 + block_size, c)
+        blk = w[:, b0:b1].copy()            # the in-block working copy (`w1`)
+        errs = np.zeros_like(blk)
+        for j in range(b1 - b0):
+            col = b0 + j
+            if not passthrough and col % group_size == 0:   # scale from the block-start `w`
+                mx = np.max(np.abs(w[:, col:min(col + group_size, c)]), axis=1)
+                scales[:, col // group_size] = np.float64(np.float32(mx / q))
+            if sparse and col % 4 == 0:
+                keep[:, col:col + 4] = keep_mask_groups(blk[:, j:j + 4], ud[col:col + 4] ** 2)
+            wc, kc = blk[:, j], keep[:, col]
+            if passthrough:
+                qc = np.where(kc, wc, 0.0)
+            else:
+                s = scales[:, col // group_size]
+                m = kc & (s > 0)
+                cc = np.zeros(r, dtype=np.int64)
+                cc[m] = np.clip(np.rint(wc[m] / s[m]), -q, q).astype(np.int64)
+                codes[:, col] = cc
+                qc = cc.astype(np.float64) * s
+            quant[:, col] = qc
+            e = (wc - qc) / ud[col]
+            loss += float(np.sum((wc - qc) ** 2) / (ud[col] * ud[col]))
+            blk[:, j + 1:] -= np.outer(e, u[col, col + 1:b1])
+            errs[:, j] = e
+        w[:, b0:b1] = quant[:, b0:b1]
+        if b1 < c:
+            w[:, b1:] -= errs @ u[b0:b1, b1:]
+    if sparse:
+        index = encode_mask_indices(keep)
+        packed = float64_payload(quant[keep]) if passthrough else pack_codes(codes[keep], bits)
+    else:
+        index, packed = b"", pack_codes(codes.reshape(-1), bits)
+    sc = np.zeros(0, "<f4") if passthrough else scales.astype("<f4").reshape(-1)
+    od = OracleDelta(rows=r, cols=c, packed_values=packed, index_stream=index, scales=sc, bits=bits,
+                     sparsity=sparsity, group_size=group_size)
+    return od, loss, quant

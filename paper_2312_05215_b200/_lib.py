@@ -37,6 +37,10 @@ class DzNativeDelta(C.Structure):
                 ("tmap", C.c_uint64 * 16)]
 
 
+class DzObsCfg(C.Structure):
+    _fields_ = [("bits", C.c_int32), ("sparse", C.c_int32), ("group_size", C.c_int32), ("block_size", C.c_int32)]
+
+
 class DzJob(C.Structure):
     _fields_ = [("slot", C.c_int32), ("tok_begin", C.c_int32), ("tok_count", C.c_int32),
                 ("kind", C.c_int32)]
@@ -117,6 +121,9 @@ SIGNATURES = {
     "dz_inflate": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]),
     "dz_plan_device": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                  C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "dz_obs_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int32, C.POINTER(DzObsCfg)]),
+    "dz_obs_compress": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.POINTER(DzObsCfg), C.c_void_p,
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "dz_peer_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
     "dz_peer_free": (C.c_int, [C.c_void_p]),
     "dz_ipc_handle": (C.c_int, [C.c_void_p, C.c_void_p]),

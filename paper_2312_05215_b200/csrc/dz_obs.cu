@@ -1,0 +1,338 @@
+// GPU ΔCompress: the OBS column solver that produces a packed layer delta.
+//
+// Reference: obs_compress_layer (compress.py:348-464) with _keep_mask_groups (compress.py:204-215)
+// and the symmetric per-(row, group) RTN grid (compress.py:403-428). The solver is sequential
+// over columns but independent over rows given the shared inverse-Hessian Cholesky factor U:
+//
+//   for each block [i1, i2) of `block_size` columns:
+//     k_obs_block   one thread per row walks the block's columns in order: group scale at
+//                   col % gs == 0 (from the block-start W, as the reference reads `w`, not `w1`),
+//                   2:4 keep mask at col % 4 == 0 (stable argsort of w^2 / u_ii^2), RTN code,
+//                   err = (w - q) / u_col,col, and the in-block update w1[:, j] -= err * u[col, j]
+//                   held in shared memory; writes the quantized block back into W and err into E;
+//     k_obs_update  W[:, i2:] -= E @ U[i1:i2, i2:] (rank-block_size update, f64 tiles).
+//   k_obs_loss / k_obs_pack_* then reduce the proxy loss and emit the reference's packed layout
+//   (pack_codes compress.py:243-262, encode_mask_indices compress.py:280-292).
+//
+// Floating-point order follows the reference: the in-block update is a rounded product then a
+// rounded subtraction (numpy's `w1 -= np.outer(err, u)`), so it uses __dmul_rn / __dsub_rn
+// (never contracted to FMA); the trailing product accumulates k in order with FMA from zero,
+// the order OpenBLAS's dgemm kernels use for `err1 @ u`, and is subtracted after rounding.
+// Codes, masks and scales are therefore bit-identical to the reference on the same U whenever
+// the reference's BLAS follows that order (tests/test_gpu_obs.py).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "dz_b200.h"
+
+namespace dz {
+namespace obs {
+
+constexpr int ROWS_PER_CTA = 32;  // one warp: one row per lane (the loss reduction is a shuffle)
+constexpr int MAX_BLOCK = 256;    // block_size limit (w1 row segment in shared memory)
+
+struct Cfg {
+  int bits, sparse, gs, bs, qmax, passthrough, n_groups;
+};
+
+// One block of columns [i1, i2) for all rows. Shared memory: w1[B][32] f64 (column-major by
+// lane: a column step touches 32 consecutive doubles).
+__global__ void __launch_bounds__(ROWS_PER_CTA) k_obs_block(double* __restrict__ W, const double* __restrict__ U,
+                                                            int rows, int cols, int i1, int i2, Cfg cfg,
+                                                            int32_t* __restrict__ codes, uint8_t* __restrict__ nib,
+                                                            double* __restrict__ kept_vals, float* __restrict__ scales,
+                                                            double* __restrict__ E, double* __restrict__ loss_part) {
+  extern __shared__ double w1[];  // [B][32]
+  const int lane = threadIdx.x;
+  const int row = blockIdx.x * ROWS_PER_CTA + lane;
+  const bool live = row < rows;
+  const int B = i2 - i1;
+  const double* wrow = W + static_cast<int64_t>(row) * cols;
+  for (int j = 0; j < B; j++) w1[j * ROWS_PER_CTA + lane] = live ? wrow[i1 + j] : 0.0;
+
+  // the scale of a group that started in an earlier block (stored f32 = the snapped value)
+  double scale = (!cfg.passthrough && live && i1 % cfg.gs != 0)
+                     ? static_cast<double>(scales[static_cast<int64_t>(row) * cfg.n_groups + i1 / cfg.gs])
+                     : 0.0;
+  unsigned keep4 = 0xF;  // blocks start at multiples of 4 under 2:4: the mask is set at i = 0
+  for (int i = 0; i < B; i++) {
+    const int col = i1 + i;
+    const double d = __ldg(U + static_cast<int64_t>(col) * cols + col);
+    if (!cfg.passthrough && col % cfg.gs == 0) {
+      // scales[:, g] = f32(max|w[:, col:col+gs]| / qmax), w = the block-start matrix
+      const int end = min(col + cfg.gs, cols);
+      double mx = 0.0;
+      if (live)
+        for (int j = col; j < end; j++) mx = fmax(mx, fabs(wrow[j]));
+      scale = static_cast<double>(__double2float_rn(__ddiv_rn(mx, static_cast<double>(cfg.qmax))));
+      if (live) scales[static_cast<int64_t>(row) * cfg.n_groups + col / cfg.gs] = static_cast<float>(scale);
+    }
+    if (cfg.sparse && (col & 3) == 0) {
+      // saliency w^2 / hd over the 4-group, stable argsort: prune the two smallest
+      double s[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const double uk = __ldg(U + static_cast<int64_t>(col + k) * cols + col + k);
+        const double w = w1[(i + k) * ROWS_PER_CTA + lane];
+        s[k] = __ddiv_rn(__dmul_rn(w, w), __dmul_rn(uk, uk));
+      }
+      keep4 = 0;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        int rank = 0;
+#pragma unroll
+        for (int k = 0; k < 4; k++) rank += (s[k] < s[j]) || (s[k] == s[j] && k < j);
+        if (rank >= 2) keep4 |= 1u << j;
+      }
+      if (live) {
+        const int p0 = __ffs(keep4) - 1, p1 = 31 - __clz(keep4);
+        nib[(static_cast<int64_t>(row) * cols + col) >> 2] = static_cast<uint8_t>(p0 | (p1 << 2));
+      }
+    }
+    const bool kc = !cfg.sparse || ((keep4 >> (col & 3)) & 1u);
+    const double wc = w1[i * ROWS_PER_CTA + lane];
+    double qc;
+    int32_t code = 0;
+    if (cfg.passthrough) {
+      qc = kc ? wc : 0.0;
+    } else {
+      if (scale > 0.0 && kc) {
+        double r = rint(__ddiv_rn(wc, scale));
+        r = fmin(fmax(r, -static_cast<double>(cfg.qmax)), static_cast<double>(cfg.qmax));
+        code = static_cast<int32_t>(r);
+      }
+      qc = __dmul_rn(static_cast<double>(code), scale);
+    }
+    const double diff = __dsub_rn(wc, qc);
+    const double err = __ddiv_rn(diff, d);
+    if (live) {
+      if (cfg.sparse) {
+        if (kc) {
+          // kept index: two per 4-group, row-major, in column order (codes[keep])
+          const int slot = __popc(keep4 & ((1u << (col & 3)) - 1u));
+          const int64_t kk = (static_cast<int64_t>(row) * cols + (col & ~3)) / 2 + slot;
+          if (cfg.passthrough) kept_vals[kk] = qc;
+          else codes[kk] = code;
+        }
+      } else if (!cfg.passthrough) {
+        codes[static_cast<int64_t>(row) * cols + col] = code;
+      }
+      E[static_cast<int64_t>(row) * cfg.bs + i] = err;
+    }
+    // proxy loss: sum over rows of (w - q)^2 for this column (fixed shuffle order)
+    double sq = live ? __dmul_rn(diff, diff) : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq = __dadd_rn(sq, __shfl_down_sync(0xffffffffu, sq, o));
+    if (lane == 0) loss_part[static_cast<int64_t>(blockIdx.x) * cols + col] = sq;
+    // w1[:, j] -= err * u[col, j] for the rest of the block (rounded product, rounded difference)
+    const double* urow = U + static_cast<int64_t>(col) * cols + i1;
+    for (int j = i + 1; j < B; j++)
+      w1[j * ROWS_PER_CTA + lane] = __dsub_rn(w1[j * ROWS_PER_CTA + lane], __dmul_rn(err, __ldg(urow + j)));
+    w1[i * ROWS_PER_CTA + lane] = qc;  // w[:, i1:i2] = quantized[:, i1:i2] after the block
+  }
+  __syncwarp();
+  if (live)
+    for (int j = 0; j < B; j++) const_cast<double*>(wrow)[i1 + j] = w1[j * ROWS_PER_CTA + lane];
+}
+
+// W[:, i2:] -= E[:, :B] @ U[i1:i2, i2:]. 64x64 output tile per CTA, 256 threads, 4x4 per thread;
+// k accumulates in order with FMA from zero, then one rounded subtraction.
+constexpr int UT = 64, UK = 32;
+__global__ void __launch_bounds__(256) k_obs_update(double* __restrict__ W, const double* __restrict__ E,
+                                                    const double* __restrict__ U, int rows, int cols, int i1, int i2,
+                                                    int ldE) {
+  __shared__ double sE[UK][UT + 1];  // [k][row]
+  __shared__ double sU[UK][UT];      // [k][col]
+  const int B = i2 - i1;
+  const int c0 = i2 + blockIdx.x * UT, r0 = blockIdx.y * UT;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; a++)
+#pragma unroll
+    for (int b = 0; b < 4; b++) acc[a][b] = 0.0;
+  for (int k0 = 0; k0 < B; k0 += UK) {
+    const int kn = min(UK, B - k0);
+    for (int e = threadIdx.x; e < UK * UT; e += 256) {
+      const int kr = e % UK, rr = e / UK;  // E row-major: consecutive threads walk k
+      const int r = r0 + rr;
+      sE[kr][rr] = (kr < kn && r < rows) ? E[static_cast<int64_t>(r) * ldE + k0 + kr] : 0.0;
+      const int kc = e / UT, cc = e % UT;
+      const int c = c0 + cc;
+      sU[kc][cc] = (kc < kn && c < cols) ? U[static_cast<int64_t>(i1 + k0 + kc) * cols + c] : 0.0;
+    }
+    __syncthreads();
+    for (int k = 0; k < kn; k++) {
+      double a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        a[q] = sE[k][ty + 16 * q];
+        b[q] = sU[k][tx + 16 * q];
+      }
+#pragma unroll
+      for (int p = 0; p < 4; p++)
+#pragma unroll
+        for (int q = 0; q < 4; q++) acc[p][q] = fma(a[p], b[q], acc[p][q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int p = 0; p < 4; p++) {
+    const int r = r0 + ty + 16 * p;
+    if (r >= rows) continue;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int c = c0 + tx + 16 * q;
+      if (c < cols) {
+        double* w = W + static_cast<int64_t>(r) * cols + c;
+        *w = __dsub_rn(*w, acc[p][q]);
+      }
+    }
+  }
+}
+
+// proxy_loss = sum_col (sum_rows sq) / u_col,col^2, accumulated in column order (one CTA).
+__global__ void __launch_bounds__(256) k_obs_loss(const double* __restrict__ part, int n_cta, int cols,
+                                                  const double* __restrict__ U, double* __restrict__ loss) {
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (int c = threadIdx.x; c < cols; c += 256) {
+    double s = 0.0;
+    for (int b = 0; b < n_cta; b++) s = __dadd_rn(s, part[static_cast<int64_t>(b) * cols + c]);
+    const double d = U[static_cast<int64_t>(c) * cols + c];
+    acc = __dadd_rn(acc, __ddiv_rn(s, __dmul_rn(d, d)));
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *loss = red[0];
+}
+
+// pack_codes: word w holds codes [w*per, w*per+per) as (code + qmax) << (bits * j)
+__global__ void k_obs_pack_codes(const int32_t* __restrict__ codes, int64_t n, int bits, int qmax,
+                                 uint32_t* __restrict__ words, int64_t n_words) {
+  const int per = 32 / bits;
+  for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < n_words;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint32_t v = 0;
+    for (int j = 0; j < per; j++) {
+      const int64_t k = w * per + j;
+      if (k < n) v |= static_cast<uint32_t>(codes[k] + qmax) << (bits * j);
+    }
+    words[w] = v;
+  }
+}
+
+// encode_mask_indices: byte b = nib[2b] | nib[2b+1] << 4 (zero nibble pads an odd count)
+__global__ void k_obs_pack_index(const uint8_t* __restrict__ nib, int64_t n_groups, uint8_t* __restrict__ index,
+                                 int64_t n_bytes) {
+  for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b < n_bytes;
+       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint8_t lo = nib[2 * b];
+    const uint8_t hi = (2 * b + 1 < n_groups) ? nib[2 * b + 1] : 0;
+    index[b] = static_cast<uint8_t>(lo | (hi << 4));
+  }
+}
+
+struct WsLayout {
+  size_t E, codes, nib, part, total;
+};
+
+static WsLayout ws_layout(int rows, int cols, const dz_obs_cfg& c) {
+  auto al = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
+  const int n_cta = (rows + ROWS_PER_CTA - 1) / ROWS_PER_CTA;
+  const int64_t rc = static_cast<int64_t>(rows) * cols;
+  WsLayout L{};
+  size_t off = 0;
+  L.E = off;
+  off += al(static_cast<size_t>(rows) * c.block_size * 8);
+  L.codes = off;
+  off += al(static_cast<size_t>(c.sparse ? rc / 2 : rc) * 4);
+  L.nib = off;
+  off += al(static_cast<size_t>(c.sparse ? rc / 4 : 1));
+  L.part = off;
+  off += al(static_cast<size_t>(n_cta) * cols * 8);
+  L.total = off;
+  return L;
+}
+
+static int check_cfg(int rows, int cols, const dz_obs_cfg* c) {
+  if (!c || rows < 1 || cols < 1) return DZ_E_VALUE;
+  if (!(c->bits == 2 || c->bits == 3 || c->bits == 4 || c->bits == 8 || c->bits == 16)) return DZ_E_VALUE;
+  if (c->group_size < 1 || c->block_size < 1 || c->block_size > MAX_BLOCK) return DZ_E_VALUE;
+  if (c->sparse && (c->block_size % 4 != 0)) return DZ_E_VALUE;
+  if (c->sparse && (cols % 4 != 0)) return DZ_E_SHAPE;
+  return DZ_OK;
+}
+
+}  // namespace obs
+}  // namespace dz
+
+using namespace dz;
+
+extern "C" size_t dz_obs_workspace_bytes(int32_t rows, int32_t cols, const dz_obs_cfg* cfg) {
+  if (obs::check_cfg(rows, cols, cfg) != DZ_OK) return 0;
+  return obs::ws_layout(rows, cols, *cfg).total;
+}
+
+extern "C" int dz_obs_compress(double* W, const double* U, int32_t rows, int32_t cols, const dz_obs_cfg* cfg,
+                               uint32_t* packed, uint8_t* index, float* scales, double* proxy_loss, void* ws,
+                               size_t ws_bytes, void* stream) {
+  const int st = obs::check_cfg(rows, cols, cfg);
+  if (st != DZ_OK) return st;
+  if (!W || !U || !packed || !proxy_loss) return DZ_E_VALUE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t rc = static_cast<int64_t>(rows) * cols;
+  const bool passthrough = cfg->bits == 16;
+  if (passthrough && !cfg->sparse) {
+    // identity quantizer, no pruning: the raw f64 values are the payload (compress.py:372-385)
+    if (cudaMemcpyAsync(packed, W, rc * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return DZ_E_CUDA;
+    return cudaMemsetAsync(proxy_loss, 0, 8, s) == cudaSuccess ? DZ_OK : DZ_E_CUDA;
+  }
+  if (cfg->sparse && !index) return DZ_E_VALUE;
+  if (!passthrough && !scales) return DZ_E_VALUE;
+  const obs::WsLayout L = obs::ws_layout(rows, cols, *cfg);
+  if (!ws || ws_bytes < L.total) return DZ_E_VALUE;
+  char* base = static_cast<char*>(ws);
+  double* E = reinterpret_cast<double*>(base + L.E);
+  int32_t* codes = reinterpret_cast<int32_t*>(base + L.codes);
+  uint8_t* nib = reinterpret_cast<uint8_t*>(base + L.nib);
+  double* part = reinterpret_cast<double*>(base + L.part);
+
+  obs::Cfg c{cfg->bits, cfg->sparse, cfg->group_size, cfg->block_size, (1 << (cfg->bits - 1)) - 1,
+             passthrough ? 1 : 0, (cols + cfg->group_size - 1) / cfg->group_size};
+  const int n_cta = (rows + obs::ROWS_PER_CTA - 1) / obs::ROWS_PER_CTA;
+  const size_t smem = static_cast<size_t>(cfg->block_size) * obs::ROWS_PER_CTA * 8;
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(obs::k_obs_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem)) != cudaSuccess)
+    return DZ_E_CUDA;
+  double* kept_vals = reinterpret_cast<double*>(packed);  // passthrough 2:4: f64 payload of kept values
+  for (int i1 = 0; i1 < cols; i1 += cfg->block_size) {
+    const int i2 = i1 + cfg->block_size < cols ? i1 + cfg->block_size : cols;
+    obs::k_obs_block<<<n_cta, obs::ROWS_PER_CTA, smem, s>>>(W, U, rows, cols, i1, i2, c, codes, nib, kept_vals,
+                                                             scales, E, part);
+    if (i2 < cols) {
+      dim3 grid((cols - i2 + obs::UT - 1) / obs::UT, (rows + obs::UT - 1) / obs::UT);
+      obs::k_obs_update<<<grid, 256, 0, s>>>(W, E, U, rows, cols, i1, i2, cfg->block_size);
+    }
+  }
+  obs::k_obs_loss<<<1, 256, 0, s>>>(part, n_cta, cols, U, proxy_loss);
+  if (cfg->sparse) {
+    const int64_t n_groups = rc / 4, n_bytes = (n_groups + 1) / 2;
+    obs::k_obs_pack_index<<<static_cast<int>((n_bytes + 255) / 256 < 4096 ? (n_bytes + 255) / 256 : 4096), 256, 0,
+                            s>>>(nib, n_groups, index, n_bytes);
+  }
+  if (!passthrough) {
+    const int64_t n = cfg->sparse ? rc / 2 : rc;
+    const int per = 32 / cfg->bits;
+    const int64_t n_words = (n + per - 1) / per;
+    obs::k_obs_pack_codes<<<static_cast<int>((n_words + 255) / 256 < 4096 ? (n_words + 255) / 256 : 4096), 256, 0,
+                            s>>>(codes, n, cfg->bits, c.qmax, packed, n_words);
+  }
+  return cudaGetLastError() == cudaSuccess ? DZ_OK : DZ_E_CUDA;
+}

@@ -42,6 +42,29 @@ class CompressConfig:
     damping: float = 0.01
     block_size: int = 32
     lossless: str = LOSSLESS_OFF
+    solver: str = "obs"
+
+    def __post_init__(self):  # reference compress.py:52-69
+        if self.solver != "obs":
+            raise ValueError(f"solver {self.solver!r} is not implemented")
+        if self.bits not in (2, 3, 4, 8, 16):
+            raise ValueError(f"bits must be one of (2, 3, 4, 8, 16), got {self.bits}")
+        if self.sparsity not in ("none", SPARSITY_2_4):
+            raise ValueError(f"unknown sparsity {self.sparsity!r}")
+        if self.group_size < 1:
+            raise ValueError("group_size must be >= 1")
+        if self.block_size < 1:
+            raise ValueError("block_size must be >= 1")
+        if self.sparsity == SPARSITY_2_4 and self.block_size % 4 != 0:
+            raise ValueError("block_size must be a multiple of 4 for 2:4 sparsity")
+        if self.damping < 0:
+            raise ValueError("damping must be nonnegative")
+        if self.lossless not in (LOSSLESS_OFF, LOSSLESS_DEFLATE):
+            raise ValueError(f"unknown lossless codec {self.lossless!r}")
+
+    @property
+    def is_passthrough(self) -> bool:
+        return self.bits == 16
 
 
 @dataclass

@@ -109,3 +109,35 @@ def test_rtn_producer_round_trip():
     assert (((dq != 0).reshape(8, 64, 4).sum(-1)) <= 2).all()
     kept = dq != 0
     assert np.abs(dq - d)[kept].max() <= np.abs(d).max() / 7 / 2 + 1e-9
+
+
+OBS_FILES = sorted(f for f in os.listdir(os.path.join(os.path.dirname(__file__), "golden"))
+                   if f.startswith("obs_b") and f.endswith(".npz"))
+
+
+@pytest.mark.parametrize("name", OBS_FILES)
+def test_obs_solver_matches_reference(name):
+    """The oracle's ΔCompress solver reproduces the reference's obs_compress_layer
+    (compress.py:348-464) on its fixtures: same factor U, same packed bytes."""
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", name))
+    bits, sp, gs, bs = (int(v) for v in z["cfg"])
+    if not (bits == 16 and not sp):
+        assert np.array_equal(O.inverse_cholesky_factor(z["hessian"]), z["u"])
+    od, loss, quant = O.obs_compress_layer(z["delta"], z["hessian"], bits,
+                                           O.SPARSITY_2_4 if sp else O.SPARSITY_NONE, gs, bs)
+    assert np.array_equal(od.packed_values, z["packed"])
+    assert od.index_stream == z["index"].tobytes()
+    assert np.array_equal(od.scales, z["scales"])
+    assert loss == pytest.approx(float(z["proxy_loss"]), rel=1e-12, abs=1e-300)
+    assert np.array_equal(O.dequantize_layer(od), z["dequant"])
+    assert np.array_equal(quant, z["dequant"])
+
+
+def test_obs_model_hessian_matches_reference():
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "obs_model_2layer.npz"))
+    h = O.compute_hessian(z["calib"], 0.01)
+    u = O.inverse_cholesky_factor(h)
+    d0 = z["wf0"] - z["wb0"]
+    od, loss, _ = O.obs_compress_layer(d0, h, 4, O.SPARSITY_2_4, 32, 16, u=u)
+    assert np.array_equal(od.packed_values, z["packed0"])
+    assert loss == pytest.approx(float(z["loss0"]), rel=1e-12)
