@@ -36,35 +36,60 @@ struct Cfg {
   int bits, sparse, gs, bs, qmax, passthrough, n_groups;
 };
 
-// One block of columns [i1, i2) for all rows. Shared memory: w1[B][32] f64 (column-major by
-// lane: a column step touches 32 consecutive doubles).
+// One block of columns [i1, i2) for all rows, one warp per 32 rows. Shared memory: the rows'
+// block segments w1[B][32] (a column step touches 32 consecutive doubles), their squared
+// residuals sq[B][32], and, when it fits (B <= 128), U's diagonal block su[B][B] (uniform
+// broadcast reads). The column loop is not
+// unrolled: a fully unrolled block thrashes the instruction cache (ncu: no_instructions stalls).
 __global__ void __launch_bounds__(ROWS_PER_CTA) k_obs_block(double* __restrict__ W, const double* __restrict__ U,
                                                             int rows, int cols, int i1, int i2, Cfg cfg,
                                                             int32_t* __restrict__ codes, uint8_t* __restrict__ nib,
                                                             double* __restrict__ kept_vals, float* __restrict__ scales,
-                                                            double* __restrict__ E, double* __restrict__ loss_part) {
-  extern __shared__ double w1[];  // [B][32]
+                                                            double* __restrict__ E, double* __restrict__ loss_part,
+                                                            int stage_u) {
+  extern __shared__ double smem[];
+  const int nb = i2 - i1;
+  double* w1s = smem;                               // [nb][32]
+  double* sq = smem + nb * ROWS_PER_CTA;            // [nb][32] squared residuals
+  double* su = smem + 2 * nb * ROWS_PER_CTA;        // [nb][nb] when stage_u
   const int lane = threadIdx.x;
   const int row = blockIdx.x * ROWS_PER_CTA + lane;
   const bool live = row < rows;
-  const int B = i2 - i1;
-  const double* wrow = W + static_cast<int64_t>(row) * cols;
-  for (int j = 0; j < B; j++) w1[j * ROWS_PER_CTA + lane] = live ? wrow[i1 + j] : 0.0;
+  double* wrow = W + static_cast<int64_t>(row) * cols;
+  auto w1 = [&](int j) -> double& { return w1s[j * ROWS_PER_CTA + lane]; };
+  auto ublk = [&](int i, int j) -> double {
+    return stage_u ? su[i * nb + j] : __ldg(U + static_cast<int64_t>(i1 + i) * cols + i1 + j);
+  };
+  if (stage_u)
+    for (int e = lane; e < nb * nb; e += ROWS_PER_CTA)
+      su[e] = U[static_cast<int64_t>(i1 + e / nb) * cols + i1 + e % nb];
+  for (int j = 0; j < nb; j++) w1(j) = live ? wrow[i1 + j] : 0.0;
+  __syncwarp();
 
   // the scale of a group that started in an earlier block (stored f32 = the snapped value)
   double scale = (!cfg.passthrough && live && i1 % cfg.gs != 0)
                      ? static_cast<double>(scales[static_cast<int64_t>(row) * cfg.n_groups + i1 / cfg.gs])
                      : 0.0;
   unsigned keep4 = 0xF;  // blocks start at multiples of 4 under 2:4: the mask is set at i = 0
-  for (int i = 0; i < B; i++) {
+#pragma unroll 1
+  for (int i = 0; i < nb; i++) {
     const int col = i1 + i;
-    const double d = __ldg(U + static_cast<int64_t>(col) * cols + col);
+    const double d = ublk(i, i);
     if (!cfg.passthrough && col % cfg.gs == 0) {
       // scales[:, g] = f32(max|w[:, col:col+gs]| / qmax), w = the block-start matrix
       const int end = min(col + cfg.gs, cols);
-      double mx = 0.0;
-      if (live)
-        for (int j = col; j < end; j++) mx = fmax(mx, fabs(wrow[j]));
+      double m0 = 0.0, m1 = 0.0, m2 = 0.0, m3 = 0.0;  // max is order-free: 4 chains for MLP
+      if (live) {
+        int j = col;
+        for (; j + 4 <= end; j += 4) {
+          m0 = fmax(m0, fabs(wrow[j]));
+          m1 = fmax(m1, fabs(wrow[j + 1]));
+          m2 = fmax(m2, fabs(wrow[j + 2]));
+          m3 = fmax(m3, fabs(wrow[j + 3]));
+        }
+        for (; j < end; j++) m0 = fmax(m0, fabs(wrow[j]));
+      }
+      const double mx = fmax(fmax(m0, m1), fmax(m2, m3));
       scale = static_cast<double>(__double2float_rn(__ddiv_rn(mx, static_cast<double>(cfg.qmax))));
       if (live) scales[static_cast<int64_t>(row) * cfg.n_groups + col / cfg.gs] = static_cast<float>(scale);
     }
@@ -73,8 +98,8 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_obs_block(double* __restrict__
       double s[4];
 #pragma unroll
       for (int k = 0; k < 4; k++) {
-        const double uk = __ldg(U + static_cast<int64_t>(col + k) * cols + col + k);
-        const double w = w1[(i + k) * ROWS_PER_CTA + lane];
+        const double uk = ublk(i + k, i + k);
+        const double w = w1(i + k);
         s[k] = __ddiv_rn(__dmul_rn(w, w), __dmul_rn(uk, uk));
       }
       keep4 = 0;
@@ -91,7 +116,7 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_obs_block(double* __restrict__
       }
     }
     const bool kc = !cfg.sparse || ((keep4 >> (col & 3)) & 1u);
-    const double wc = w1[i * ROWS_PER_CTA + lane];
+    const double wc = w1(i);
     double qc;
     int32_t code = 0;
     if (cfg.passthrough) {
@@ -106,6 +131,10 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_obs_block(double* __restrict__
     }
     const double diff = __dsub_rn(wc, qc);
     const double err = __ddiv_rn(diff, d);
+    // w1[:, j] -= err * u[col, j] for the rest of the block (rounded product, rounded difference)
+#pragma unroll 4
+    for (int j = i + 1; j < nb; j++) w1(j) = __dsub_rn(w1(j), __dmul_rn(err, ublk(i, j)));
+    w1(i) = qc;  // w[:, i1:i2] = quantized[:, i1:i2] after the block
     if (live) {
       if (cfg.sparse) {
         if (kc) {
@@ -120,89 +149,122 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_obs_block(double* __restrict__
       }
       E[static_cast<int64_t>(row) * cfg.bs + i] = err;
     }
-    // proxy loss: sum over rows of (w - q)^2 for this column (fixed shuffle order)
-    double sq = live ? __dmul_rn(diff, diff) : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sq = __dadd_rn(sq, __shfl_down_sync(0xffffffffu, sq, o));
-    if (lane == 0) loss_part[static_cast<int64_t>(blockIdx.x) * cols + col] = sq;
-    // w1[:, j] -= err * u[col, j] for the rest of the block (rounded product, rounded difference)
-    const double* urow = U + static_cast<int64_t>(col) * cols + i1;
-    for (int j = i + 1; j < B; j++)
-      w1[j * ROWS_PER_CTA + lane] = __dsub_rn(w1[j * ROWS_PER_CTA + lane], __dmul_rn(err, __ldg(urow + j)));
-    w1[i * ROWS_PER_CTA + lane] = qc;  // w[:, i1:i2] = quantized[:, i1:i2] after the block
+    sq[i * ROWS_PER_CTA + lane] = live ? __dmul_rn(diff, diff) : 0.0;
   }
+  // proxy loss partials: per column, the sum over this CTA's rows in row order (off the
+  // column loop's critical path)
   __syncwarp();
+  for (int j = lane; j < nb; j += ROWS_PER_CTA) {
+    double t = 0.0;
+    for (int k = 0; k < ROWS_PER_CTA; k++) t = __dadd_rn(t, sq[j * ROWS_PER_CTA + k]);
+    loss_part[static_cast<int64_t>(blockIdx.x) * cols + i1 + j] = t;
+  }
   if (live)
-    for (int j = 0; j < B; j++) const_cast<double*>(wrow)[i1 + j] = w1[j * ROWS_PER_CTA + lane];
+    for (int j = 0; j < nb; j++) wrow[i1 + j] = w1(j);
 }
 
-// W[:, i2:] -= E[:, :B] @ U[i1:i2, i2:]. 64x64 output tile per CTA, 256 threads, 4x4 per thread;
-// k accumulates in order with FMA from zero, then one rounded subtraction.
-constexpr int UT = 64, UK = 32;
+// W[:, i2:] -= E[:, :B] @ U[i1:i2, i2:] on the FP64 tensor cores (mma.sync m8n8k4 f64, DMMA).
+// DMMA is bit-identical to the k-ordered FMA chain fma(a3,b3, fma(a2,b2, fma(a1,b1, fma(a0,b0,c))))
+// (tools/dmma_probe.cu, 2.56M cases), so chaining k-steps from a zero accumulator reproduces the
+// in-order FMA accumulation of the reference's BLAS exactly; one rounded subtraction per element.
+// 128x128 output tile per CTA, 8 warps as 4 (rows) x 2 (cols), 32x64 per warp = 4x8 DMMA tiles.
+// Shared tiles are [k][128 + 4]: the +4 pad spreads a half-warp's 4 k-rows over all 32 banks.
+constexpr int UT = 128, UK = 32, UPAD = UT + 4;
+constexpr size_t UPD_SMEM = 2ull * UK * UPAD * 8;
 __global__ void __launch_bounds__(256) k_obs_update(double* __restrict__ W, const double* __restrict__ E,
                                                     const double* __restrict__ U, int rows, int cols, int i1, int i2,
                                                     int ldE) {
-  __shared__ double sE[UK][UT + 1];  // [k][row]
-  __shared__ double sU[UK][UT];      // [k][col]
+  extern __shared__ double sm[];
+  double* sE = sm;              // [UK][UPAD]: E[r0 + row][k0 + k]
+  double* sU = sm + UK * UPAD;  // [UK][UPAD]: U[i1 + k0 + k][c0 + col]
   const int B = i2 - i1;
   const int c0 = i2 + blockIdx.x * UT, r0 = blockIdx.y * UT;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  double acc[4][4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 64;
+  const int fr = lane >> 2, fk = lane & 3;
+  double acc[4][8][2];
 #pragma unroll
   for (int a = 0; a < 4; a++)
 #pragma unroll
-    for (int b = 0; b < 4; b++) acc[a][b] = 0.0;
+    for (int b = 0; b < 8; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
   for (int k0 = 0; k0 < B; k0 += UK) {
     const int kn = min(UK, B - k0);
-    for (int e = threadIdx.x; e < UK * UT; e += 256) {
-      const int kr = e % UK, rr = e / UK;  // E row-major: consecutive threads walk k
-      const int r = r0 + rr;
-      sE[kr][rr] = (kr < kn && r < rows) ? E[static_cast<int64_t>(r) * ldE + k0 + kr] : 0.0;
-      const int kc = e / UT, cc = e % UT;
-      const int c = c0 + cc;
-      sU[kc][cc] = (kc < kn && c < cols) ? U[static_cast<int64_t>(i1 + k0 + kc) * cols + c] : 0.0;
+    // all global loads of the tile in flight before any shared store (one latency, not 16)
+    constexpr int PER = UK * UT / 256;
+    double ve[PER], vu[PER];
+#pragma unroll
+    for (int t = 0; t < PER; t++) {
+      const int e = threadIdx.x + 256 * t;
+      const int kr = e % UK, r = r0 + e / UK;
+      ve[t] = (kr < kn && r < rows) ? E[static_cast<int64_t>(r) * ldE + k0 + kr] : 0.0;
+      const int kc = e / UT, c = c0 + e % UT;
+      vu[t] = (kc < kn && c < cols) ? U[static_cast<int64_t>(i1 + k0 + kc) * cols + c] : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < PER; t++) {
+      const int e = threadIdx.x + 256 * t;
+      sE[(e % UK) * UPAD + e / UK] = ve[t];
+      sU[(e / UT) * UPAD + e % UT] = vu[t];
     }
     __syncthreads();
-    for (int k = 0; k < kn; k++) {
-      double a[4], b[4];
+    const int ksteps = (kn + 3) >> 2;
+    for (int ks = 0; ks < ksteps; ks++) {
+      const int kk = ks * 4 + fk;
+      double a[4], b[8];
 #pragma unroll
-      for (int q = 0; q < 4; q++) {
-        a[q] = sE[k][ty + 16 * q];
-        b[q] = sU[k][tx + 16 * q];
-      }
+      for (int m = 0; m < 4; m++) a[m] = sE[kk * UPAD + wm + m * 8 + fr];
 #pragma unroll
-      for (int p = 0; p < 4; p++)
+      for (int n = 0; n < 8; n++) b[n] = sU[kk * UPAD + wn + n * 8 + fr];
 #pragma unroll
-        for (int q = 0; q < 4; q++) acc[p][q] = fma(a[p], b[q], acc[p][q]);
+      for (int m = 0; m < 4; m++)
+#pragma unroll
+        for (int n = 0; n < 8; n++)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[m][n][0]), "+d"(acc[m][n][1])
+                       : "d"(a[m]), "d"(b[n]));
     }
     __syncthreads();
   }
+  // W -= acc: per row group, all 16 loads in flight before the stores (W loads and stores may
+  // alias as far as the compiler knows, so interleaving them would serialise 64 round trips)
 #pragma unroll
-  for (int p = 0; p < 4; p++) {
-    const int r = r0 + ty + 16 * p;
+  for (int m = 0; m < 4; m++) {
+    const int r = r0 + wm + m * 8 + fr;
     if (r >= rows) continue;
+    double* wr = W + static_cast<int64_t>(r) * cols;
+    double v[8][2];
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
-      const int c = c0 + tx + 16 * q;
-      if (c < cols) {
-        double* w = W + static_cast<int64_t>(r) * cols + c;
-        *w = __dsub_rn(*w, acc[p][q]);
-      }
+    for (int n = 0; n < 8; n++) {
+      const int c = c0 + wn + n * 8 + 2 * fk;
+      v[n][0] = c < cols ? wr[c] : 0.0;
+      v[n][1] = c + 1 < cols ? wr[c + 1] : 0.0;
+    }
+#pragma unroll
+    for (int n = 0; n < 8; n++) {
+      const int c = c0 + wn + n * 8 + 2 * fk;
+      if (c < cols) wr[c] = __dsub_rn(v[n][0], acc[m][n][0]);
+      if (c + 1 < cols) wr[c + 1] = __dsub_rn(v[n][1], acc[m][n][1]);
     }
   }
 }
 
-// proxy_loss = sum_col (sum_rows sq) / u_col,col^2, accumulated in column order (one CTA).
-__global__ void __launch_bounds__(256) k_obs_loss(const double* __restrict__ part, int n_cta, int cols,
-                                                  const double* __restrict__ U, double* __restrict__ loss) {
+// proxy_loss = sum_col (sum_rows sq) / u_col,col^2: one thread per column folds the per-CTA
+// partials in CTA order into part[0][col], then one CTA sums the columns (fixed order).
+__global__ void __launch_bounds__(256) k_obs_loss_cols(double* __restrict__ part, int n_cta, int cols,
+                                                       const double* __restrict__ U) {
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c >= cols) return;
+  double s = 0.0;
+  for (int b = 0; b < n_cta; b++) s = __dadd_rn(s, part[static_cast<int64_t>(b) * cols + c]);
+  const double d = U[static_cast<int64_t>(c) * cols + c];
+  part[c] = __ddiv_rn(s, __dmul_rn(d, d));
+}
+
+__global__ void __launch_bounds__(256) k_obs_loss(const double* __restrict__ part, int cols,
+                                                  double* __restrict__ loss) {
   __shared__ double red[256];
   double acc = 0.0;
-  for (int c = threadIdx.x; c < cols; c += 256) {
-    double s = 0.0;
-    for (int b = 0; b < n_cta; b++) s = __dadd_rn(s, part[static_cast<int64_t>(b) * cols + c]);
-    const double d = U[static_cast<int64_t>(c) * cols + c];
-    acc = __dadd_rn(acc, __ddiv_rn(s, __dmul_rn(d, d)));
-  }
+  for (int c = threadIdx.x; c < cols; c += 256) acc = __dadd_rn(acc, part[c]);
   red[threadIdx.x] = acc;
   __syncthreads();
   for (int o = 128; o > 0; o >>= 1) {
@@ -306,22 +368,27 @@ extern "C" int dz_obs_compress(double* W, const double* U, int32_t rows, int32_t
   obs::Cfg c{cfg->bits, cfg->sparse, cfg->group_size, cfg->block_size, (1 << (cfg->bits - 1)) - 1,
              passthrough ? 1 : 0, (cols + cfg->group_size - 1) / cfg->group_size};
   const int n_cta = (rows + obs::ROWS_PER_CTA - 1) / obs::ROWS_PER_CTA;
-  const size_t smem = static_cast<size_t>(cfg->block_size) * obs::ROWS_PER_CTA * 8;
-  if (smem > 48 * 1024 &&
-      cudaFuncSetAttribute(obs::k_obs_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem)) != cudaSuccess)
+  const int bs = cfg->block_size;
+  const int stage_u = bs <= 128;
+  const size_t smem = 2 * static_cast<size_t>(bs) * obs::ROWS_PER_CTA * 8 + (stage_u ? static_cast<size_t>(bs) * bs * 8 : 0);
+  if (smem > 48 * 1024 && cudaFuncSetAttribute(obs::k_obs_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem)) != cudaSuccess)
+    return DZ_E_CUDA;
+  if (cudaFuncSetAttribute(obs::k_obs_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(obs::UPD_SMEM)) != cudaSuccess)
     return DZ_E_CUDA;
   double* kept_vals = reinterpret_cast<double*>(packed);  // passthrough 2:4: f64 payload of kept values
-  for (int i1 = 0; i1 < cols; i1 += cfg->block_size) {
-    const int i2 = i1 + cfg->block_size < cols ? i1 + cfg->block_size : cols;
+  for (int i1 = 0; i1 < cols; i1 += bs) {
+    const int i2 = i1 + bs < cols ? i1 + bs : cols;
     obs::k_obs_block<<<n_cta, obs::ROWS_PER_CTA, smem, s>>>(W, U, rows, cols, i1, i2, c, codes, nib, kept_vals,
-                                                             scales, E, part);
+                                                             scales, E, part, stage_u);
     if (i2 < cols) {
       dim3 grid((cols - i2 + obs::UT - 1) / obs::UT, (rows + obs::UT - 1) / obs::UT);
-      obs::k_obs_update<<<grid, 256, 0, s>>>(W, E, U, rows, cols, i1, i2, cfg->block_size);
+      obs::k_obs_update<<<grid, 256, obs::UPD_SMEM, s>>>(W, E, U, rows, cols, i1, i2, cfg->block_size);
     }
   }
-  obs::k_obs_loss<<<1, 256, 0, s>>>(part, n_cta, cols, U, proxy_loss);
+  obs::k_obs_loss_cols<<<(cols + 255) / 256, 256, 0, s>>>(part, n_cta, cols, U);
+  obs::k_obs_loss<<<1, 256, 0, s>>>(part, cols, proxy_loss);
   if (cfg->sparse) {
     const int64_t n_groups = rc / 4, n_bytes = (n_groups + 1) / 2;
     obs::k_obs_pack_index<<<static_cast<int>((n_bytes + 255) / 256 < 4096 ? (n_bytes + 255) / 256 : 4096), 256, 0,
