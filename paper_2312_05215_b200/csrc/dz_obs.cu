@@ -5,7 +5,7 @@
 // over columns but independent over rows given the shared inverse-Hessian Cholesky factor U:
 //
 //   for each block [i1, i2) of `block_size` columns:
-//     k_obs_block   one thread per row walks the block's columns in order: group scale at
+//     k_obs_block   each row walks the block's columns in order (4 lanes per row): group scale at
 //                   col % gs == 0 (from the block-start W, as the reference reads `w`, not `w1`),
 //                   2:4 keep mask at col % 4 == 0 (stable argsort of w^2 / u_ii^2), RTN code,
 //                   err = (w - q) / u_col,col, and the in-block update w1[:, j] -= err * u[col, j]
@@ -29,42 +29,50 @@
 namespace dz {
 namespace obs {
 
-constexpr int ROWS_PER_CTA = 32;  // one warp: one row per lane (the loss reduction is a shuffle)
-constexpr int MAX_BLOCK = 256;    // block_size limit (w1 row segment in shared memory)
+#ifndef DZ_OBS_LPR
+#define DZ_OBS_LPR 8
+#endif
+constexpr int ROWS_PER_CTA = 32;  // rows per CTA
+constexpr int LPR = DZ_OBS_LPR;   // lanes per row: a row's in-block update is split LPR ways
+constexpr int OBS_THREADS = ROWS_PER_CTA * LPR;
+constexpr int RS = ROWS_PER_CTA + 1;  // shared row stride of the [column][row] tiles
+constexpr int MAX_BLOCK = 256;    // block_size limit (row segments in shared memory)
 
 struct Cfg {
   int bits, sparse, gs, bs, qmax, passthrough, n_groups;
 };
 
-// One block of columns [i1, i2) for all rows, one warp per 32 rows. Shared memory: the rows'
-// block segments w1[B][32] (a column step touches 32 consecutive doubles), their squared
-// residuals sq[B][32], and, when it fits (B <= 128), U's diagonal block su[B][B] (uniform
-// broadcast reads). The column loop is not
-// unrolled: a fully unrolled block thrashes the instruction cache (ncu: no_instructions stalls).
-__global__ void __launch_bounds__(ROWS_PER_CTA) k_obs_block(double* __restrict__ W, const double* __restrict__ U,
-                                                            int rows, int cols, int i1, int i2, Cfg cfg,
-                                                            int32_t* __restrict__ codes, uint8_t* __restrict__ nib,
-                                                            double* __restrict__ kept_vals, float* __restrict__ scales,
-                                                            double* __restrict__ E, double* __restrict__ loss_part,
-                                                            int stage_u) {
+// One block of columns [i1, i2) for all rows: 32 rows per CTA, 4 lanes per row (8 rows per warp).
+// Column i is quantised by its owner lane (i % 4) of each row; err is broadcast to the row's 4
+// lanes by a shuffle, and lane q applies the update to the block columns j > i with j % 4 == q.
+// That cuts the serial update per column 4x and puts 4 warps on each SM instead of 1 (the walk
+// is latency-bound). Shared memory: row segments w1[B][33], squared residuals sq[B][33], and,
+// when it fits (B <= 128), U's diagonal block su[B][B] (broadcast reads). The column loop is
+// not unrolled: a fully unrolled block thrashes the instruction cache (ncu: no_instructions).
+__global__ void __launch_bounds__(OBS_THREADS) k_obs_block(double* __restrict__ W, const double* __restrict__ U,
+                                                           int rows, int cols, int i1, int i2, Cfg cfg,
+                                                           int32_t* __restrict__ codes, uint8_t* __restrict__ nib,
+                                                           double* __restrict__ kept_vals, float* __restrict__ scales,
+                                                           double* __restrict__ E, double* __restrict__ loss_part,
+                                                           int stage_u) {
   extern __shared__ double smem[];
   const int nb = i2 - i1;
-  double* w1s = smem;                               // [nb][32]
-  double* sq = smem + nb * ROWS_PER_CTA;            // [nb][32] squared residuals
-  double* su = smem + 2 * nb * ROWS_PER_CTA;        // [nb][nb] when stage_u
-  const int lane = threadIdx.x;
-  const int row = blockIdx.x * ROWS_PER_CTA + lane;
+  double* w1s = smem;                 // [nb][RS]
+  double* sq = smem + nb * RS;        // [nb][RS]
+  double* su = smem + 2 * nb * RS;    // [nb][nb] when stage_u
+  const int tid = threadIdx.x, q = tid & (LPR - 1), rl = tid / LPR;
+  const int gbase = (tid & 31) & ~(LPR - 1);  // this row's lane 0 within the warp
+  const int row = blockIdx.x * ROWS_PER_CTA + rl;
   const bool live = row < rows;
   double* wrow = W + static_cast<int64_t>(row) * cols;
-  auto w1 = [&](int j) -> double& { return w1s[j * ROWS_PER_CTA + lane]; };
+  auto w1 = [&](int j) -> double& { return w1s[j * RS + rl]; };
   auto ublk = [&](int i, int j) -> double {
     return stage_u ? su[i * nb + j] : __ldg(U + static_cast<int64_t>(i1 + i) * cols + i1 + j);
   };
   if (stage_u)
-    for (int e = lane; e < nb * nb; e += ROWS_PER_CTA)
-      su[e] = U[static_cast<int64_t>(i1 + e / nb) * cols + i1 + e % nb];
-  for (int j = 0; j < nb; j++) w1(j) = live ? wrow[i1 + j] : 0.0;
-  __syncwarp();
+    for (int e = tid; e < nb * nb; e += OBS_THREADS) su[e] = U[static_cast<int64_t>(i1 + e / nb) * cols + i1 + e % nb];
+  for (int j = q; j < nb; j += LPR) w1(j) = live ? wrow[i1 + j] : 0.0;
+  __syncthreads();
 
   // the scale of a group that started in an earlier block (stored f32 = the snapped value)
   double scale = (!cfg.passthrough && live && i1 % cfg.gs != 0)
@@ -74,173 +82,182 @@ __global__ void __launch_bounds__(ROWS_PER_CTA) k_obs_block(double* __restrict__
 #pragma unroll 1
   for (int i = 0; i < nb; i++) {
     const int col = i1 + i;
-    const double d = ublk(i, i);
+    const int own = i & (LPR - 1);
     if (!cfg.passthrough && col % cfg.gs == 0) {
-      // scales[:, g] = f32(max|w[:, col:col+gs]| / qmax), w = the block-start matrix
+      // scales[:, g] = f32(max|w[:, col:col+gs]| / qmax), w = the block-start matrix; the row's
+      // 4 lanes take every 4th column and combine (max is order-free, so this is exact)
       const int end = min(col + cfg.gs, cols);
-      double m0 = 0.0, m1 = 0.0, m2 = 0.0, m3 = 0.0;  // max is order-free: 4 chains for MLP
-      if (live) {
-        int j = col;
-        for (; j + 4 <= end; j += 4) {
-          m0 = fmax(m0, fabs(wrow[j]));
-          m1 = fmax(m1, fabs(wrow[j + 1]));
-          m2 = fmax(m2, fabs(wrow[j + 2]));
-          m3 = fmax(m3, fabs(wrow[j + 3]));
-        }
-        for (; j < end; j++) m0 = fmax(m0, fabs(wrow[j]));
-      }
-      const double mx = fmax(fmax(m0, m1), fmax(m2, m3));
-      scale = static_cast<double>(__double2float_rn(__ddiv_rn(mx, static_cast<double>(cfg.qmax))));
-      if (live) scales[static_cast<int64_t>(row) * cfg.n_groups + col / cfg.gs] = static_cast<float>(scale);
+      double m = 0.0;
+      if (live)
+        for (int j = col + q; j < end; j += LPR) m = fmax(m, fabs(wrow[j]));
+#pragma unroll
+      for (int o = 1; o < LPR; o <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      scale = static_cast<double>(__double2float_rn(__ddiv_rn(m, static_cast<double>(cfg.qmax))));
+      if (live && q == 0) scales[static_cast<int64_t>(row) * cfg.n_groups + col / cfg.gs] = static_cast<float>(scale);
     }
     if (cfg.sparse && (col & 3) == 0) {
-      // saliency w^2 / hd over the 4-group, stable argsort: prune the two smallest
-      double s[4];
+      // saliency w^2 / hd over the 4-group, stable argsort: prune the two smallest (every lane
+      // of the row computes the same mask)
+      double s4[4];
 #pragma unroll
       for (int k = 0; k < 4; k++) {
         const double uk = ublk(i + k, i + k);
         const double w = w1(i + k);
-        s[k] = __ddiv_rn(__dmul_rn(w, w), __dmul_rn(uk, uk));
+        s4[k] = __ddiv_rn(__dmul_rn(w, w), __dmul_rn(uk, uk));
       }
       keep4 = 0;
 #pragma unroll
       for (int j = 0; j < 4; j++) {
         int rank = 0;
 #pragma unroll
-        for (int k = 0; k < 4; k++) rank += (s[k] < s[j]) || (s[k] == s[j] && k < j);
+        for (int k = 0; k < 4; k++) rank += (s4[k] < s4[j]) || (s4[k] == s4[j] && k < j);
         if (rank >= 2) keep4 |= 1u << j;
       }
-      if (live) {
+      if (live && q == 0) {
         const int p0 = __ffs(keep4) - 1, p1 = 31 - __clz(keep4);
         nib[(static_cast<int64_t>(row) * cols + col) >> 2] = static_cast<uint8_t>(p0 | (p1 << 2));
       }
     }
-    const bool kc = !cfg.sparse || ((keep4 >> (col & 3)) & 1u);
-    const double wc = w1(i);
-    double qc;
-    int32_t code = 0;
-    if (cfg.passthrough) {
-      qc = kc ? wc : 0.0;
-    } else {
-      if (scale > 0.0 && kc) {
-        double r = rint(__ddiv_rn(wc, scale));
-        r = fmin(fmax(r, -static_cast<double>(cfg.qmax)), static_cast<double>(cfg.qmax));
-        code = static_cast<int32_t>(r);
-      }
-      qc = __dmul_rn(static_cast<double>(code), scale);
-    }
-    const double diff = __dsub_rn(wc, qc);
-    const double err = __ddiv_rn(diff, d);
-    // w1[:, j] -= err * u[col, j] for the rest of the block (rounded product, rounded difference)
-#pragma unroll 4
-    for (int j = i + 1; j < nb; j++) w1(j) = __dsub_rn(w1(j), __dmul_rn(err, ublk(i, j)));
-    w1(i) = qc;  // w[:, i1:i2] = quantized[:, i1:i2] after the block
-    if (live) {
-      if (cfg.sparse) {
-        if (kc) {
-          // kept index: two per 4-group, row-major, in column order (codes[keep])
-          const int slot = __popc(keep4 & ((1u << (col & 3)) - 1u));
-          const int64_t kk = (static_cast<int64_t>(row) * cols + (col & ~3)) / 2 + slot;
-          if (cfg.passthrough) kept_vals[kk] = qc;
-          else codes[kk] = code;
+    double err = 0.0;
+    if (q == own) {
+      const bool kc = !cfg.sparse || ((keep4 >> (col & 3)) & 1u);
+      const double wc = w1(i);
+      double qc;
+      int32_t code = 0;
+      if (cfg.passthrough) {
+        qc = kc ? wc : 0.0;
+      } else {
+        if (scale > 0.0 && kc) {
+          double r = rint(__ddiv_rn(wc, scale));
+          r = fmin(fmax(r, -static_cast<double>(cfg.qmax)), static_cast<double>(cfg.qmax));
+          code = static_cast<int32_t>(r);
         }
-      } else if (!cfg.passthrough) {
-        codes[static_cast<int64_t>(row) * cols + col] = code;
+        qc = __dmul_rn(static_cast<double>(code), scale);
       }
-      E[static_cast<int64_t>(row) * cfg.bs + i] = err;
+      const double diff = __dsub_rn(wc, qc);
+      err = __ddiv_rn(diff, ublk(i, i));
+      w1(i) = qc;  // w[:, i1:i2] = quantized[:, i1:i2] after the block
+      sq[i * RS + rl] = live ? __dmul_rn(diff, diff) : 0.0;
+      if (live) {
+        if (cfg.sparse) {
+          if (kc) {
+            // kept index: two per 4-group, row-major, in column order (codes[keep])
+            const int slot = __popc(keep4 & ((1u << (col & 3)) - 1u));
+            const int64_t kk = (static_cast<int64_t>(row) * cols + (col & ~3)) / 2 + slot;
+            if (cfg.passthrough) kept_vals[kk] = qc;
+            else codes[kk] = code;
+          }
+        } else if (!cfg.passthrough) {
+          codes[static_cast<int64_t>(row) * cols + col] = code;
+        }
+        E[static_cast<int64_t>(row) * cfg.bs + i] = err;
+      }
     }
-    sq[i * ROWS_PER_CTA + lane] = live ? __dmul_rn(diff, diff) : 0.0;
+    err = __shfl_sync(0xffffffffu, err, gbase + own);
+    // w1[:, j] -= err * u[col, j] for this lane's columns of the rest of the block (rounded
+    // product, rounded difference)
+    for (int j = i + 1 + ((q - i - 1) & (LPR - 1)); j < nb; j += LPR)
+      w1(j) = __dsub_rn(w1(j), __dmul_rn(err, ublk(i, j)));
+    __syncwarp();
   }
-  // proxy loss partials: per column, the sum over this CTA's rows in row order (off the
-  // column loop's critical path)
-  __syncwarp();
-  for (int j = lane; j < nb; j += ROWS_PER_CTA) {
+  __syncthreads();
+  // proxy loss partials: per column, the sum over this CTA's rows in row order
+  for (int j = tid; j < nb; j += OBS_THREADS) {
     double t = 0.0;
-    for (int k = 0; k < ROWS_PER_CTA; k++) t = __dadd_rn(t, sq[j * ROWS_PER_CTA + k]);
+    for (int k = 0; k < ROWS_PER_CTA; k++) t = __dadd_rn(t, sq[j * RS + k]);
     loss_part[static_cast<int64_t>(blockIdx.x) * cols + i1 + j] = t;
   }
   if (live)
-    for (int j = 0; j < nb; j++) wrow[i1 + j] = w1(j);
+    for (int j = q; j < nb; j += LPR) wrow[i1 + j] = w1(j);
 }
 
 // W[:, i2:] -= E[:, :B] @ U[i1:i2, i2:] on the FP64 tensor cores (mma.sync m8n8k4 f64, DMMA).
 // DMMA is bit-identical to the k-ordered FMA chain fma(a3,b3, fma(a2,b2, fma(a1,b1, fma(a0,b0,c))))
 // (tools/dmma_probe.cu, 2.56M cases), so chaining k-steps from a zero accumulator reproduces the
 // in-order FMA accumulation of the reference's BLAS exactly; one rounded subtraction per element.
-// 128x128 output tile per CTA, 8 warps as 4 (rows) x 2 (cols), 32x64 per warp = 4x8 DMMA tiles.
-// Shared tiles are [k][128 + 4]: the +4 pad spreads a half-warp's 4 k-rows over all 32 banks.
-constexpr int UT = 128, UK = 32, UPAD = UT + 4;
-constexpr size_t UPD_SMEM = 2ull * UK * UPAD * 8;
-__global__ void __launch_bounds__(256) k_obs_update(double* __restrict__ W, const double* __restrict__ E,
-                                                    const double* __restrict__ U, int rows, int cols, int i1, int i2,
-                                                    int ldE) {
+// 64x128 output tile per CTA, 8 warps as 2 (rows) x 4 (cols), 32x32 per warp = 4x4 DMMA tiles;
+// ~120 registers, so two CTAs share an SM and one's loads overlap the other's DMMAs.
+// Shared tiles are [k][cols + 4]: the +4 pad spreads a half-warp's 4 k-rows over all 32 banks.
+constexpr int UTM = 64, UTN = 128, UK = 32, EPAD = UTM + 4, UPAD = UTN + 4;
+constexpr size_t UPD_SMEM = static_cast<size_t>(UK) * (EPAD + UPAD) * 8;
+__global__ void __launch_bounds__(256, 2) k_obs_update(double* __restrict__ W, const double* __restrict__ E,
+                                                       const double* __restrict__ U, int rows, int cols, int i1, int i2,
+                                                       int ldE) {
   extern __shared__ double sm[];
-  double* sE = sm;              // [UK][UPAD]: E[r0 + row][k0 + k]
-  double* sU = sm + UK * UPAD;  // [UK][UPAD]: U[i1 + k0 + k][c0 + col]
+  double* sE = sm;              // [UK][EPAD]: E[r0 + row][k0 + k]
+  double* sU = sm + UK * EPAD;  // [UK][UPAD]: U[i1 + k0 + k][c0 + col]
   const int B = i2 - i1;
-  const int c0 = i2 + blockIdx.x * UT, r0 = blockIdx.y * UT;
+  const int c0 = i2 + blockIdx.x * UTN, r0 = blockIdx.y * UTM;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 64;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
   const int fr = lane >> 2, fk = lane & 3;
-  double acc[4][8][2];
+  double acc[4][4][2];
 #pragma unroll
   for (int a = 0; a < 4; a++)
 #pragma unroll
-    for (int b = 0; b < 8; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
   for (int k0 = 0; k0 < B; k0 += UK) {
     const int kn = min(UK, B - k0);
-    // all global loads of the tile in flight before any shared store (one latency, not 16)
-    constexpr int PER = UK * UT / 256;
-    double ve[PER], vu[PER];
+    // all global loads of the tile in flight before any shared store (one latency, not many)
+    constexpr int PE = UK * UTM / 256, PU = UK * UTN / 256;
+    double ve[PE], vu[PU];
 #pragma unroll
-    for (int t = 0; t < PER; t++) {
+    for (int t = 0; t < PE; t++) {
       const int e = threadIdx.x + 256 * t;
       const int kr = e % UK, r = r0 + e / UK;
       ve[t] = (kr < kn && r < rows) ? E[static_cast<int64_t>(r) * ldE + k0 + kr] : 0.0;
-      const int kc = e / UT, c = c0 + e % UT;
+    }
+#pragma unroll
+    for (int t = 0; t < PU; t++) {
+      const int e = threadIdx.x + 256 * t;
+      const int kc = e / UTN, c = c0 + e % UTN;
       vu[t] = (kc < kn && c < cols) ? U[static_cast<int64_t>(i1 + k0 + kc) * cols + c] : 0.0;
     }
 #pragma unroll
-    for (int t = 0; t < PER; t++) {
+    for (int t = 0; t < PE; t++) {
       const int e = threadIdx.x + 256 * t;
-      sE[(e % UK) * UPAD + e / UK] = ve[t];
-      sU[(e / UT) * UPAD + e % UT] = vu[t];
+      sE[(e % UK) * EPAD + e / UK] = ve[t];
+    }
+#pragma unroll
+    for (int t = 0; t < PU; t++) {
+      const int e = threadIdx.x + 256 * t;
+      sU[(e / UTN) * UPAD + e % UTN] = vu[t];
     }
     __syncthreads();
     const int ksteps = (kn + 3) >> 2;
     for (int ks = 0; ks < ksteps; ks++) {
       const int kk = ks * 4 + fk;
-      double a[4], b[8];
+      double a[4], b[4];
 #pragma unroll
-      for (int m = 0; m < 4; m++) a[m] = sE[kk * UPAD + wm + m * 8 + fr];
+      for (int m = 0; m < 4; m++) a[m] = sE[kk * EPAD + wm + m * 8 + fr];
 #pragma unroll
-      for (int n = 0; n < 8; n++) b[n] = sU[kk * UPAD + wn + n * 8 + fr];
+      for (int n = 0; n < 4; n++) b[n] = sU[kk * UPAD + wn + n * 8 + fr];
 #pragma unroll
       for (int m = 0; m < 4; m++)
 #pragma unroll
-        for (int n = 0; n < 8; n++)
+        for (int n = 0; n < 4; n++)
           asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                        : "+d"(acc[m][n][0]), "+d"(acc[m][n][1])
                        : "d"(a[m]), "d"(b[n]));
     }
     __syncthreads();
   }
-  // W -= acc: per row group, all 16 loads in flight before the stores (W loads and stores may
-  // alias as far as the compiler knows, so interleaving them would serialise 64 round trips)
+  // W -= acc: per row group, all loads in flight before the stores (W loads and stores may alias
+  // as far as the compiler knows, so interleaving them would serialise the round trips)
 #pragma unroll
   for (int m = 0; m < 4; m++) {
     const int r = r0 + wm + m * 8 + fr;
     if (r >= rows) continue;
     double* wr = W + static_cast<int64_t>(r) * cols;
-    double v[8][2];
+    double v[4][2];
 #pragma unroll
-    for (int n = 0; n < 8; n++) {
+    for (int n = 0; n < 4; n++) {
       const int c = c0 + wn + n * 8 + 2 * fk;
       v[n][0] = c < cols ? wr[c] : 0.0;
       v[n][1] = c + 1 < cols ? wr[c + 1] : 0.0;
     }
 #pragma unroll
-    for (int n = 0; n < 8; n++) {
+    for (int n = 0; n < 4; n++) {
       const int c = c0 + wn + n * 8 + 2 * fk;
       if (c < cols) wr[c] = __dsub_rn(v[n][0], acc[m][n][0]);
       if (c + 1 < cols) wr[c + 1] = __dsub_rn(v[n][1], acc[m][n][1]);
@@ -370,7 +387,7 @@ extern "C" int dz_obs_compress(double* W, const double* U, int32_t rows, int32_t
   const int n_cta = (rows + obs::ROWS_PER_CTA - 1) / obs::ROWS_PER_CTA;
   const int bs = cfg->block_size;
   const int stage_u = bs <= 128;
-  const size_t smem = 2 * static_cast<size_t>(bs) * obs::ROWS_PER_CTA * 8 + (stage_u ? static_cast<size_t>(bs) * bs * 8 : 0);
+  const size_t smem = 2 * static_cast<size_t>(bs) * obs::RS * 8 + (stage_u ? static_cast<size_t>(bs) * bs * 8 : 0);
   if (smem > 48 * 1024 && cudaFuncSetAttribute(obs::k_obs_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(smem)) != cudaSuccess)
     return DZ_E_CUDA;
@@ -380,10 +397,10 @@ extern "C" int dz_obs_compress(double* W, const double* U, int32_t rows, int32_t
   double* kept_vals = reinterpret_cast<double*>(packed);  // passthrough 2:4: f64 payload of kept values
   for (int i1 = 0; i1 < cols; i1 += bs) {
     const int i2 = i1 + bs < cols ? i1 + bs : cols;
-    obs::k_obs_block<<<n_cta, obs::ROWS_PER_CTA, smem, s>>>(W, U, rows, cols, i1, i2, c, codes, nib, kept_vals,
+    obs::k_obs_block<<<n_cta, obs::OBS_THREADS, smem, s>>>(W, U, rows, cols, i1, i2, c, codes, nib, kept_vals,
                                                              scales, E, part, stage_u);
     if (i2 < cols) {
-      dim3 grid((cols - i2 + obs::UT - 1) / obs::UT, (rows + obs::UT - 1) / obs::UT);
+      dim3 grid((cols - i2 + obs::UTN - 1) / obs::UTN, (rows + obs::UTM - 1) / obs::UTM);
       obs::k_obs_update<<<grid, 256, obs::UPD_SMEM, s>>>(W, E, U, rows, cols, i1, i2, cfg->block_size);
     }
   }
