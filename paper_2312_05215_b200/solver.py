@@ -6,8 +6,8 @@ Reference: compress.py:178-186 (compute_hessian), :321-336 (_inverse_cholesky_fa
 Split of work:
   * the proxy Hessian H = X X^T + damping * mean(diag) * I and the propagation
     X <- (W_b + ΔW~) X are plain f64 GEMMs (cuBLAS through torch);
-  * the inverse-Hessian factor U (upper, H^-1 = U^T U) is two f64 Cholesky factorisations and a
-    triangular inverse (cuSOLVER through torch.linalg), as the reference does with LAPACK;
+  * the inverse-Hessian factor U (upper, H^-1 = U^T U) is one f64 Cholesky of the reversed H and
+    a triangular inverse (cuSOLVER / cuBLAS through torch.linalg); the reference uses LAPACK;
   * the OBS column solver, the 2:4 mask choice, the RTN grid, the proxy loss and the packing
     into the reference layout are the `dz_obs_compress` kernels (csrc/dz_obs.cu).
 Given the same U the solver reproduces the reference's codes, masks and scales bit for bit
@@ -80,15 +80,21 @@ def compute_hessian(calib: CalibrationSet, damping: float) -> np.ndarray:
 
 
 def inverse_cholesky_factor(h: torch.Tensor, name: str = "layer") -> torch.Tensor:
-    """Upper U with H^-1 = U^T U (compress.py:321-336), f64 on the device."""
-    lo, info = torch.linalg.cholesky_ex(h)
-    if int(info.item()) != 0 or not bool(torch.isfinite(h).all()):
+    """Upper U with H^-1 = U^T U (compress.py:321-336), f64 on the device.
+
+    The reference factors H, inverts it and factors the inverse (LAPACK potrf, potrs, potrf).
+    The same unique factor comes from one Cholesky and one triangular inverse: with J the
+    reversal permutation and J H J = L L^T, U = J L^-1 J is upper triangular with a positive
+    diagonal and U^T U = J (J H J)^-1 J = H^-1. That is 2 cuSOLVER/cuBLAS calls instead of 3
+    and about half the flops."""
+    if not bool(torch.isfinite(h).all()):
         raise NumericDomainError(f"hessian for layer {name!r} is not positive definite")
-    hinv = torch.cholesky_inverse(lo)
-    u, info = torch.linalg.cholesky_ex(hinv, upper=True)
+    lo, info = torch.linalg.cholesky_ex(torch.flip(h, (0, 1)))
     if int(info.item()) != 0:
         raise NumericDomainError(f"hessian for layer {name!r} is not positive definite")
-    return u.contiguous()
+    eye = torch.eye(h.shape[0], dtype=h.dtype, device=h.device)
+    linv = torch.linalg.solve_triangular(lo, eye, upper=False)
+    return torch.flip(linv, (0, 1)).contiguous()
 
 
 @dataclass
