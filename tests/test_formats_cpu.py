@@ -111,3 +111,34 @@ def test_bad_header_json(F, tmp_path):
     p.write_bytes(bytes(b))
     with pytest.raises(F.FormatError, match="header"):
         F.read_delta(p)
+
+
+def test_compress_config_validation_matches_reference():
+    """CompressConfig rejects what the reference rejects (compress.py:52-69)."""
+    import pytest as _pt
+    from paper_2312_05215_b200.formats import CompressConfig
+    for kw in [dict(bits=5), dict(sparsity="1:4"), dict(group_size=0), dict(block_size=0),
+               dict(block_size=6), dict(damping=-1.0), dict(lossless="lz4"), dict(solver="gptq")]:
+        with _pt.raises(ValueError):
+            CompressConfig(**kw)
+    assert CompressConfig(bits=16).is_passthrough and not CompressConfig().is_passthrough
+    CompressConfig(sparsity="none", block_size=6)  # block size only constrained under 2:4
+
+
+def test_solver_output_sizes_match_reference_fixtures():
+    """The GPU solver's output buffers are sized exactly like the reference's packed fields."""
+    import os
+    import numpy as np
+    from paper_2312_05215_b200.formats import CompressConfig
+    from paper_2312_05215_b200.solver import _n_words
+    gold = os.path.join(os.path.dirname(__file__), "golden")
+    for f in sorted(os.listdir(gold)):
+        if not (f.startswith("obs_b") and f.endswith(".npz")):
+            continue
+        z = np.load(os.path.join(gold, f))
+        bits, sp, gs, bs = (int(v) for v in z["cfg"])
+        r, c = z["delta"].shape
+        cfg = CompressConfig(bits=bits, sparsity="two_of_four" if sp else "none", group_size=gs, block_size=bs)
+        assert _n_words(r, c, cfg) == z["packed"].size, f
+        if sp:
+            assert r * c // 8 + (1 if (r * c // 4) % 2 else 0) == z["index"].size, f
