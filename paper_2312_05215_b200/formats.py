@@ -184,6 +184,31 @@ def _layer_arrays(p: _Parsed, rec) -> tuple[str, np.ndarray, bytes, np.ndarray]:
     return name, payload, index, scales
 
 
+def write_delta(cd: CompressedDelta, path) -> None:
+    """Write a DZDL container (reference formats.py:60-97), byte-identical to the reference's
+    writer: the producer side of the swap path, used after `solver.compress_model`."""
+    import struct
+    import zlib
+    lossless = cd.config.lossless == LOSSLESS_DEFLATE
+    header = {"base_model_id": cd.base_model_id, "bits": cd.config.bits, "sparsity": cd.config.sparsity,
+              "group_size": cd.config.group_size, "layer_count": len(cd.layers),
+              "calibration_fingerprint": cd.calibration_fingerprint, "damping": cd.config.damping,
+              "block_size": cd.config.block_size, "codec": LOSSLESS_DEFLATE if lossless else LOSSLESS_OFF}
+    hb = json.dumps(header, sort_keys=True).encode("utf-8")
+    parts = [DELTA_MAGIC, struct.pack("<HHI", 1, 0x1 if lossless else 0, len(hb)), hb]
+    for ld in cd.layers:
+        name = ld.name.encode("utf-8")
+        sc = np.ascontiguousarray(ld.scales, dtype="<f4").tobytes()
+        idx = bytes(ld.index_stream)
+        payload = np.ascontiguousarray(ld.packed_values, dtype="<u4").tobytes()
+        if lossless:
+            payload = zlib.compress(payload, 6)  # compress.py:556-557
+        parts += [struct.pack("<H", len(name)), name, struct.pack("<III", ld.rows, ld.cols, len(sc)), sc,
+                  struct.pack("<I", len(idx)), idx, struct.pack("<I", len(payload)), payload]
+    with open(path, "wb") as f:
+        f.write(b"".join(parts))
+
+
 def read_delta(path) -> CompressedDelta:
     """Reference formats.read_delta (formats.py:102-169): host LayerDeltas of a DZDL file."""
     with open(path, "rb") as f:

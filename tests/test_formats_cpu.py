@@ -142,3 +142,19 @@ def test_solver_output_sizes_match_reference_fixtures():
         assert _n_words(r, c, cfg) == z["packed"].size, f
         if sp:
             assert r * c // 8 + (1 if (r * c // 4) % 2 else 0) == z["index"].size, f
+
+
+def test_write_delta_is_byte_identical_to_reference_files():
+    """read_delta -> write_delta reproduces the reference's own DZDL files byte for byte."""
+    import glob
+    import os
+    import tempfile
+    from paper_2312_05215_b200.formats import read_delta, write_delta
+    files = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "dzdl_*.dzdl")))
+    assert files
+    for f in files:
+        cd = read_delta(f)
+        with tempfile.TemporaryDirectory() as d:
+            out = os.path.join(d, "x.dzdl")
+            write_delta(cd, out)
+            assert open(out, "rb").read() == open(f, "rb").read(), f

@@ -121,3 +121,39 @@ def test_obs_large_layer_vs_oracle():
     words_differ = float(np.mean(ld.packed_values != od.packed_values))
     assert words_differ <= 0.01, words_differ  # exact when the host BLAS accumulates in k order
     assert ld.proxy_loss == pytest.approx(loss, rel=1e-3)
+
+
+def test_compress_write_load_serve_pipeline(tmp_path):
+    """The producer-to-serving path on the GPU: compress_model -> write_delta (DZDL, deflate) ->
+    load_delta (native parse, inflate, upload, re-layout) -> fused SBMM, against the oracle's
+    sbmm on the same compressed layers (rel-err <= 1e-2) and K1 bit-exactness."""
+    import oracle as O
+    from paper_2312_05215_b200 import WeightStack, dequantize_layer
+    from paper_2312_05215_b200.engine import DeltaTable, NativeBase, Plan, sbmm_forward
+    from paper_2312_05215_b200.formats import CompressConfig, load_delta, write_delta
+    from paper_2312_05215_b200.solver import CalibrationSet, compress_model
+    rng = np.random.default_rng(9)
+    out_f, in_f = 256, 512
+    wb = rng.normal(0, 1 / np.sqrt(in_f), (out_f, in_f))
+    wb = torch.from_numpy(wb).to(torch.bfloat16).double().numpy()  # bf16-representable base
+    wf = wb + rng.normal(0, 0.01, wb.shape)
+    cal = CalibrationSet(rng.normal(0, 1, (in_f, 256)))
+    cd = compress_model(WeightStack([("l0", wf)]), WeightStack([("l0", wb)]), cal,
+                        CompressConfig(bits=4, lossless="deflate"))
+    path = tmp_path / "d.dzdl"
+    write_delta(cd, path)
+    meta, natives = load_delta(str(path))
+    ld = cd.layers[0]
+    assert np.array_equal(natives[0].to_dense_f32().cpu().numpy(), dequantize_layer(ld).astype(np.float32))
+    dev = torch.device("cuda", 0)
+    table = DeltaTable(natives, out_f, in_f)
+    base = NativeBase(torch.from_numpy(wb).to(dev).to(torch.bfloat16))
+    T = 16
+    ids = np.zeros(T, np.int32)
+    X = torch.from_numpy(rng.normal(0, 1, (T, in_f)).astype(np.float32)).to(torch.bfloat16)
+    Y = sbmm_forward(X.to(dev), Plan(ids, table.kinds, 1), base, table, y_dtype=torch.float32)
+    od = O.OracleDelta(rows=out_f, cols=in_f, packed_values=ld.packed_values, index_stream=ld.index_stream,
+                       scales=ld.scales, bits=4, sparsity=O.SPARSITY_2_4, group_size=128)
+    ref = O.sbmm_matrix(wb, {0: od}, ids, X.double().numpy())
+    err = (np.linalg.norm(Y.cpu().double().numpy() - ref, axis=1) / np.linalg.norm(ref, axis=1)).max()
+    assert err <= 1e-2, err
