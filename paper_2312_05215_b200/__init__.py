@@ -41,7 +41,7 @@ from .inference import (
     tp_partition,
 )
 
-from .formats import CompressConfig, CompressedDelta
+from .formats import CompressConfig, CompressedDelta, inspect_delta, read_delta, write_delta
 from .solver import CalibrationSet, compress_model, compute_hessian, obs_compress_layer
 
 __version__ = "0.1.0"
