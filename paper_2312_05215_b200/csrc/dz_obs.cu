@@ -10,7 +10,9 @@
 //                   2:4 keep mask at col % 4 == 0 (stable argsort of w^2 / u_ii^2), RTN code,
 //                   err = (w - q) / u_col,col, and the in-block update w1[:, j] -= err * u[col, j]
 //                   held in shared memory; writes the quantized block back into W and err into E;
-//     k_obs_update  W[:, i2:] -= E @ U[i1:i2, i2:] (rank-block_size update, f64 tiles).
+//     k_obs_update  W[:, i2:] -= E @ U[i1:i2, i2:] (rank-block_size update, f64 tiles), applied
+//                   eagerly inside a window of columns (one scale group) and, for the columns
+//                   beyond it, once per window with every block's product rounded in order.
 //   k_obs_loss / k_obs_pack_* then reduce the proxy loss and emit the reference's packed layout
 //   (pack_codes compress.py:243-262, encode_mask_indices compress.py:280-292).
 //
@@ -53,8 +55,8 @@ __global__ void __launch_bounds__(OBS_THREADS) k_obs_block(double* __restrict__ 
                                                            int rows, int cols, int i1, int i2, Cfg cfg,
                                                            int32_t* __restrict__ codes, uint8_t* __restrict__ nib,
                                                            double* __restrict__ kept_vals, float* __restrict__ scales,
-                                                           double* __restrict__ E, double* __restrict__ loss_part,
-                                                           int stage_u) {
+                                                           double* __restrict__ E, int ldE, int e_off,
+                                                           double* __restrict__ loss_part, int stage_u) {
   extern __shared__ double smem[];
   const int nb = i2 - i1;
   double* w1s = smem;                 // [nb][RS]
@@ -150,7 +152,7 @@ __global__ void __launch_bounds__(OBS_THREADS) k_obs_block(double* __restrict__ 
         } else if (!cfg.passthrough) {
           codes[static_cast<int64_t>(row) * cols + col] = code;
         }
-        E[static_cast<int64_t>(row) * cfg.bs + i] = err;
+        E[static_cast<int64_t>(row) * ldE + e_off + i] = err;
       }
     }
     err = __shfl_sync(0xffffffffu, err, gbase + own);
@@ -175,92 +177,112 @@ __global__ void __launch_bounds__(OBS_THREADS) k_obs_block(double* __restrict__ 
 // DMMA is bit-identical to the k-ordered FMA chain fma(a3,b3, fma(a2,b2, fma(a1,b1, fma(a0,b0,c))))
 // (tools/dmma_probe.cu, 2.56M cases), so chaining k-steps from a zero accumulator reproduces the
 // in-order FMA accumulation of the reference's BLAS exactly; one rounded subtraction per element.
-// 64x128 output tile per CTA, 8 warps as 2 (rows) x 4 (cols), 32x32 per warp = 4x4 DMMA tiles;
-// ~120 registers, so two CTAs share an SM and one's loads overlap the other's DMMAs.
-// Shared tiles are [k][cols + 4]: the +4 pad spreads a half-warp's 4 k-rows over all 32 banks.
-constexpr int UTM = 64, UTN = 128, UK = 32, EPAD = UTM + 4, UPAD = UTN + 4;
+//
+// Windowed schedule: W[:, c_begin:c_end] receives the updates of `nch` consecutive blocks
+// (chunks of `bs` columns of E / rows of U) in block order, each chunk's product rounded and
+// subtracted before the next (the reference's per-block `w[:, i2:] -= err1 @ u`). The W tile
+// stays in registers across the chunks, so W is read and written once per window instead of
+// once per block.
+// 64x64 output tile per CTA, 8 warps as 2 (rows) x 4 (cols), 32x16 per warp = 4x2 DMMA tiles.
+// Shared tiles are [k][64 + 4]: the +4 pad spreads a half-warp's 4 k-rows over all 32 banks.
+constexpr int UTM = 64, UTN = 64, UK = 32, EPAD = UTM + 4, UPAD = UTN + 4;
 constexpr size_t UPD_SMEM = static_cast<size_t>(UK) * (EPAD + UPAD) * 8;
-__global__ void __launch_bounds__(256, 2) k_obs_update(double* __restrict__ W, const double* __restrict__ E,
-                                                       const double* __restrict__ U, int rows, int cols, int i1, int i2,
-                                                       int ldE) {
+__global__ void __launch_bounds__(256, 2) k_obs_update(double* __restrict__ W, const double* __restrict__ E, int ldE, int e_base,
+                                                       const double* __restrict__ U, int rows, int cols, int u0,
+                                                       int c_begin, int c_end, int nch, int bs, int last_len) {
   extern __shared__ double sm[];
-  double* sE = sm;              // [UK][EPAD]: E[r0 + row][k0 + k]
-  double* sU = sm + UK * EPAD;  // [UK][UPAD]: U[i1 + k0 + k][c0 + col]
-  const int B = i2 - i1;
-  const int c0 = i2 + blockIdx.x * UTN, r0 = blockIdx.y * UTM;
+  double* sE = sm;              // [UK][EPAD]: E[r0 + row][ch * bs + k0 + k]
+  double* sU = sm + UK * EPAD;  // [UK][UPAD]: U[u0 + ch * bs + k0 + k][c0 + col]
+  const int c0 = c_begin + blockIdx.x * UTN, r0 = blockIdx.y * UTM;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
   const int fr = lane >> 2, fk = lane & 3;
-  double acc[4][4][2];
+  // this thread's W elements: rows wm + 8m + fr, cols wn + 8n + 2fk + {0, 1}
+  double w[4][2][2];
 #pragma unroll
-  for (int a = 0; a < 4; a++)
+  for (int m = 0; m < 4; m++) {
+    const int r = r0 + wm + m * 8 + fr;
 #pragma unroll
-    for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
-  for (int k0 = 0; k0 < B; k0 += UK) {
-    const int kn = min(UK, B - k0);
-    // all global loads of the tile in flight before any shared store (one latency, not many)
-    constexpr int PE = UK * UTM / 256, PU = UK * UTN / 256;
-    double ve[PE], vu[PU];
-#pragma unroll
-    for (int t = 0; t < PE; t++) {
-      const int e = threadIdx.x + 256 * t;
-      const int kr = e % UK, r = r0 + e / UK;
-      ve[t] = (kr < kn && r < rows) ? E[static_cast<int64_t>(r) * ldE + k0 + kr] : 0.0;
+    for (int n = 0; n < 2; n++) {
+      const int c = c0 + wn + n * 8 + 2 * fk;
+      const double* wr = W + static_cast<int64_t>(r) * cols;
+      w[m][n][0] = (r < rows && c < c_end) ? wr[c] : 0.0;
+      w[m][n][1] = (r < rows && c + 1 < c_end) ? wr[c + 1] : 0.0;
     }
-#pragma unroll
-    for (int t = 0; t < PU; t++) {
-      const int e = threadIdx.x + 256 * t;
-      const int kc = e / UTN, c = c0 + e % UTN;
-      vu[t] = (kc < kn && c < cols) ? U[static_cast<int64_t>(i1 + k0 + kc) * cols + c] : 0.0;
-    }
-#pragma unroll
-    for (int t = 0; t < PE; t++) {
-      const int e = threadIdx.x + 256 * t;
-      sE[(e % UK) * EPAD + e / UK] = ve[t];
-    }
-#pragma unroll
-    for (int t = 0; t < PU; t++) {
-      const int e = threadIdx.x + 256 * t;
-      sU[(e / UTN) * UPAD + e % UTN] = vu[t];
-    }
-    __syncthreads();
-    const int ksteps = (kn + 3) >> 2;
-    for (int ks = 0; ks < ksteps; ks++) {
-      const int kk = ks * 4 + fk;
-      double a[4], b[4];
-#pragma unroll
-      for (int m = 0; m < 4; m++) a[m] = sE[kk * EPAD + wm + m * 8 + fr];
-#pragma unroll
-      for (int n = 0; n < 4; n++) b[n] = sU[kk * UPAD + wn + n * 8 + fr];
-#pragma unroll
-      for (int m = 0; m < 4; m++)
-#pragma unroll
-        for (int n = 0; n < 4; n++)
-          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                       : "+d"(acc[m][n][0]), "+d"(acc[m][n][1])
-                       : "d"(a[m]), "d"(b[n]));
-    }
-    __syncthreads();
   }
-  // W -= acc: per row group, all loads in flight before the stores (W loads and stores may alias
-  // as far as the compiler knows, so interleaving them would serialise the round trips)
+  for (int ch = 0; ch < nch; ch++) {
+    const int B = ch == nch - 1 ? last_len : bs;
+    const int e0 = e_base + ch * bs, ur = u0 + ch * bs;
+    double acc[4][2][2];
+#pragma unroll
+    for (int m = 0; m < 4; m++)
+#pragma unroll
+      for (int n = 0; n < 2; n++) acc[m][n][0] = acc[m][n][1] = 0.0;
+    for (int k0 = 0; k0 < B; k0 += UK) {
+      const int kn = min(UK, B - k0);
+      // all global loads of the tile in flight before any shared store
+      constexpr int PE = UK * UTM / 256, PU = UK * UTN / 256;
+      double ve[PE], vu[PU];
+#pragma unroll
+      for (int t = 0; t < PE; t++) {
+        const int e = threadIdx.x + 256 * t;
+        const int kr = e % UK, r = r0 + e / UK;
+        ve[t] = (kr < kn && r < rows) ? E[static_cast<int64_t>(r) * ldE + e0 + k0 + kr] : 0.0;
+      }
+#pragma unroll
+      for (int t = 0; t < PU; t++) {
+        const int e = threadIdx.x + 256 * t;
+        const int kc = e / UTN, c = c0 + e % UTN;
+        vu[t] = (kc < kn && c < c_end) ? U[static_cast<int64_t>(ur + k0 + kc) * cols + c] : 0.0;
+      }
+#pragma unroll
+      for (int t = 0; t < PE; t++) {
+        const int e = threadIdx.x + 256 * t;
+        sE[(e % UK) * EPAD + e / UK] = ve[t];
+      }
+#pragma unroll
+      for (int t = 0; t < PU; t++) {
+        const int e = threadIdx.x + 256 * t;
+        sU[(e / UTN) * UPAD + e % UTN] = vu[t];
+      }
+      __syncthreads();
+      const int ksteps = (kn + 3) >> 2;
+      for (int ks = 0; ks < ksteps; ks++) {
+        const int kk = ks * 4 + fk;
+        double a[4], b[2];
+#pragma unroll
+        for (int m = 0; m < 4; m++) a[m] = sE[kk * EPAD + wm + m * 8 + fr];
+#pragma unroll
+        for (int n = 0; n < 2; n++) b[n] = sU[kk * UPAD + wn + n * 8 + fr];
+#pragma unroll
+        for (int m = 0; m < 4; m++)
+#pragma unroll
+          for (int n = 0; n < 2; n++)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[m][n][0]), "+d"(acc[m][n][1])
+                         : "d"(a[m]), "d"(b[n]));
+      }
+      __syncthreads();
+    }
+    // this block's product is complete: one rounded subtraction per element
+#pragma unroll
+    for (int m = 0; m < 4; m++)
+#pragma unroll
+      for (int n = 0; n < 2; n++) {
+        w[m][n][0] = __dsub_rn(w[m][n][0], acc[m][n][0]);
+        w[m][n][1] = __dsub_rn(w[m][n][1], acc[m][n][1]);
+      }
+  }
 #pragma unroll
   for (int m = 0; m < 4; m++) {
     const int r = r0 + wm + m * 8 + fr;
     if (r >= rows) continue;
     double* wr = W + static_cast<int64_t>(r) * cols;
-    double v[4][2];
 #pragma unroll
-    for (int n = 0; n < 4; n++) {
+    for (int n = 0; n < 2; n++) {
       const int c = c0 + wn + n * 8 + 2 * fk;
-      v[n][0] = c < cols ? wr[c] : 0.0;
-      v[n][1] = c + 1 < cols ? wr[c + 1] : 0.0;
-    }
-#pragma unroll
-    for (int n = 0; n < 4; n++) {
-      const int c = c0 + wn + n * 8 + 2 * fk;
-      if (c < cols) wr[c] = __dsub_rn(v[n][0], acc[m][n][0]);
-      if (c + 1 < cols) wr[c + 1] = __dsub_rn(v[n][1], acc[m][n][1]);
+      if (c < c_end) wr[c] = w[m][n][0];
+      if (c + 1 < c_end) wr[c + 1] = w[m][n][1];
     }
   }
 }
@@ -321,6 +343,16 @@ struct WsLayout {
   size_t E, codes, nib, part, total;
 };
 
+// Columns a window defers: the trailing update of every column beyond the window waits until the
+// window's last block. A window must cover each scale group whole (the group scale at its first
+// column reads the group's current values), so it is the group when block_size divides it;
+// without scales (identity quantizer) any multiple of the block works.
+static int window_cols(const dz_obs_cfg& c) {
+  if (c.bits == 16) return c.block_size * (c.block_size >= 128 ? 1 : 128 / c.block_size);
+  if (c.group_size % c.block_size == 0 && c.group_size <= 512) return c.group_size;
+  return c.block_size;
+}
+
 static WsLayout ws_layout(int rows, int cols, const dz_obs_cfg& c) {
   auto al = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
   const int n_cta = (rows + ROWS_PER_CTA - 1) / ROWS_PER_CTA;
@@ -328,7 +360,7 @@ static WsLayout ws_layout(int rows, int cols, const dz_obs_cfg& c) {
   WsLayout L{};
   size_t off = 0;
   L.E = off;
-  off += al(static_cast<size_t>(rows) * c.block_size * 8);
+  off += al(static_cast<size_t>(rows) * window_cols(c) * 8);
   L.codes = off;
   off += al(static_cast<size_t>(c.sparse ? rc / 2 : rc) * 4);
   L.nib = off;
@@ -395,14 +427,21 @@ extern "C" int dz_obs_compress(double* W, const double* U, int32_t rows, int32_t
                            static_cast<int>(obs::UPD_SMEM)) != cudaSuccess)
     return DZ_E_CUDA;
   double* kept_vals = reinterpret_cast<double*>(packed);  // passthrough 2:4: f64 payload of kept values
-  for (int i1 = 0; i1 < cols; i1 += bs) {
-    const int i2 = i1 + bs < cols ? i1 + bs : cols;
-    obs::k_obs_block<<<n_cta, obs::OBS_THREADS, smem, s>>>(W, U, rows, cols, i1, i2, c, codes, nib, kept_vals,
-                                                             scales, E, part, stage_u);
-    if (i2 < cols) {
-      dim3 grid((cols - i2 + obs::UTN - 1) / obs::UTN, (rows + obs::UTM - 1) / obs::UTM);
-      obs::k_obs_update<<<grid, 256, obs::UPD_SMEM, s>>>(W, E, U, rows, cols, i1, i2, cfg->block_size);
+  const int win = obs::window_cols(*cfg);
+  auto update = [&](int u0, int e_base, int c_begin, int c_end, int nch, int last_len) {
+    dim3 grid((c_end - c_begin + obs::UTN - 1) / obs::UTN, (rows + obs::UTM - 1) / obs::UTM);
+    obs::k_obs_update<<<grid, 256, obs::UPD_SMEM, s>>>(W, E, win, e_base, U, rows, cols, u0, c_begin, c_end, nch, bs,
+                                                       last_len);
+  };
+  for (int g0 = 0; g0 < cols; g0 += win) {
+    const int g1 = g0 + win < cols ? g0 + win : cols;
+    for (int i1 = g0; i1 < g1; i1 += bs) {
+      const int i2 = i1 + bs < g1 ? i1 + bs : g1;
+      obs::k_obs_block<<<n_cta, obs::OBS_THREADS, smem, s>>>(W, U, rows, cols, i1, i2, c, codes, nib, kept_vals,
+                                                               scales, E, win, i1 - g0, part, stage_u);
+      if (i2 < g1) update(i1, i1 - g0, i2, g1, 1, i2 - i1);  // eager inside the window
     }
+    if (g1 < cols) update(g0, 0, g1, cols, (g1 - g0 + bs - 1) / bs, (g1 - g0) - ((g1 - g0 - 1) / bs) * bs);
   }
   obs::k_obs_loss_cols<<<(cols + 255) / 256, 256, 0, s>>>(part, n_cta, cols, U);
   obs::k_obs_loss<<<1, 256, 0, s>>>(part, cols, proxy_loss);
