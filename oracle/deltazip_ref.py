@@ -418,7 +418,7 @@ def obs_compress_layer(delta, hessian, bits: int, sparsity: str, group_size: int
             col = b0 + j
             if not passthrough and col % group_size == 0:   # scale from the block-start `w`
                 mx = np.max(np.abs(w[:, col:min(col + group_size, c)]), axis=1)
-                scales[:, col // group_size] = np.float64(np.float32(mx / q))
+                scales[:, col // group_size] = (mx / q).astype(np.float32).astype(np.float64)
             if sparse and col % 4 == 0:
                 keep[:, col:col + 4] = keep_mask_groups(blk[:, j:j + 4], ud[col:col + 4] ** 2)
             wc, kc = blk[:, j], keep[:, col]

@@ -37,6 +37,11 @@ CASES = [
     ("obs_b4_gs40_20x160_bs8", 20, 160, 4, SPARSITY_2_4, 40, 8, 7),
     ("obs_b16_sparse_16x64", 16, 64, 16, SPARSITY_2_4, 128, 32, 8),
     ("obs_b16_dense_8x40", 8, 40, 16, SPARSITY_NONE, 128, 32, 9),
+    # edge cases of the windowed schedule (window = group when block | group)
+    ("obs_b16_sparse_16x320", 16, 320, 16, SPARSITY_2_4, 128, 32, 10),
+    ("obs_b4_9x48_bs4_gs8", 9, 48, 4, SPARSITY_2_4, 8, 4, 11),
+    ("obs_b2_dense_1x100_bs12_gs36", 1, 100, 2, SPARSITY_NONE, 36, 12, 12),
+    ("obs_b8_70x264_gs64", 70, 264, 8, SPARSITY_2_4, 64, 32, 13),
 ]
 
 
