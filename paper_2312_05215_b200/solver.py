@@ -4,8 +4,8 @@ Reference: compress.py:178-186 (compute_hessian), :321-336 (_inverse_cholesky_fa
 :348-464 (obs_compress_layer), :508-548 (compress_model). Same names, arguments and errors.
 
 Split of work:
-  * the proxy Hessian H = X X^T + damping * mean(diag) * I and the propagation
-    X <- (W_b + ΔW~) X are plain f64 GEMMs (cuBLAS through torch);
+  * the proxy Hessian H = X X^T + damping * mean(diag) * I (one cuBLAS DSYRK) and the
+    propagation X <- (W_b + ΔW~) X (a plain f64 GEMM through torch);
   * the inverse-Hessian factor U (upper, H^-1 = U^T U) is one f64 Cholesky of the reversed H and
     a triangular inverse (cuSOLVER / cuBLAS through torch.linalg); the reference uses LAPACK;
   * the OBS column solver, the 2:4 mask choice, the RTN grid, the proxy loss and the packing
@@ -63,11 +63,53 @@ def _dev_f64(a, device) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(device)
 
 
+_CUBLAS = None
+
+
+def _cublas():
+    """torch's own cuBLAS (already loaded in the process), for DSYRK."""
+    global _CUBLAS
+    if _CUBLAS is None:
+        import glob
+        import os
+        cands = glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "cublas", "lib",
+                                       "libcublas.so.*")) + ["libcublas.so.12", "libcublas.so"]
+        for c in cands:
+            try:
+                lib = C.CDLL(c)
+                lib.cublasDsyrk_v2.restype = C.c_int
+                _CUBLAS = lib
+                break
+            except OSError:
+                continue
+        if _CUBLAS is None:
+            _CUBLAS = False
+    return _CUBLAS
+
+
 def hessian_device(x: torch.Tensor, damping: float) -> torch.Tensor:
-    """H = X X^T + damping * mean(diag(X X^T)) * I on the device (compress.py:178-186)."""
+    """H = X X^T + damping * mean(diag(X X^T)) * I on the device (compress.py:178-186).
+
+    X X^T is symmetric, so it is one cuBLAS DSYRK (half the flops of the GEMM the reference
+    runs) on torch's handle and stream, mirrored into the full matrix."""
     if damping < 0:
         raise ValueError("damping must be nonnegative")
-    h = x @ x.T
+    n, k = x.shape
+    lib = _cublas()
+    h = None
+    if lib:
+        x = x.contiguous()
+        h = torch.zeros(n, n, dtype=torch.float64, device=x.device)
+        one, zero = C.c_double(1.0), C.c_double(0.0)
+        # column-major view: A = X^T (k x n, lda = k); C = A^T A, FILL_MODE_LOWER (0) = row-major upper
+        st = lib.cublasDsyrk_v2(C.c_void_p(torch.cuda.current_blas_handle()), 0, 1, n, k, C.byref(one),
+                                C.c_void_p(x.data_ptr()), k, C.byref(zero), C.c_void_p(h.data_ptr()), n)
+        if st != 0:
+            h = None
+        else:
+            h = torch.triu(h) + torch.triu(h, 1).T
+    if h is None:  # cuBLAS without the symbol: the plain GEMM
+        h = x @ x.T
     d = torch.diagonal(h)
     d += damping * torch.mean(d)
     return h

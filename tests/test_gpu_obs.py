@@ -157,3 +157,15 @@ def test_compress_write_load_serve_pipeline(tmp_path):
     ref = O.sbmm_matrix(wb, {0: od}, ids, X.double().numpy())
     err = (np.linalg.norm(Y.cpu().double().numpy() - ref, axis=1) / np.linalg.norm(ref, axis=1)).max()
     assert err <= 1e-2, err
+
+
+def test_hessian_syrk_matches_gemm():
+    """The DSYRK Hessian is exactly symmetric and agrees with X X^T (compress.py:178-186)."""
+    import oracle as O
+    from paper_2312_05215_b200.solver import hessian_device
+    rng = np.random.default_rng(4)
+    x = rng.normal(0, 1, (300, 517))
+    h = hessian_device(torch.from_numpy(x).cuda(), 0.01).cpu().numpy()
+    assert np.array_equal(h, h.T)
+    ref = O.compute_hessian(x, 0.01)
+    assert np.abs(h - ref).max() <= 1e-12 * np.abs(ref).max()
