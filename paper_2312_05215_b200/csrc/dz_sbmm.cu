@@ -540,7 +540,10 @@ __device__ __forceinline__ void grid_sync(unsigned* count, unsigned* gen) {
 // Tail prefetch: a CTA with no more items warms L2 with the first weight stages of the item its
 // blockIdx takes first in the next linear of the step (items [0, grid) are static there), so the
 // launch boundary keeps HBM busy with bytes the next launch reads anyway.
-constexpr int TAIL_PF_CHUNKS = 6;
+#ifndef DZ_TAIL_PF
+#define DZ_TAIL_PF 6
+#endif
+constexpr int TAIL_PF_CHUNKS = DZ_TAIL_PF;
 __device__ __forceinline__ void tail_prefetch(const dz_sbmm_args& nx) {
   if (nx.perm != nullptr || nx.T <= 0) return;  // decode plans only
   const int nrt = ceil_div(nx.out, RT), nbt = ceil_div(nx.out, BASE_RT), nkb = ceil_div(nx.in, kBlkCols);
