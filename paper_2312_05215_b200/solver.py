@@ -198,7 +198,6 @@ def obs_compress_layer(delta, hessian, cfg: CompressConfig, name: str = "layer",
 
     `u` (optional, host or device f64 [cols, cols]) supplies the inverse-Hessian factor instead
     of factoring `hessian` on the device."""
-    dev = require_cuda()
     delta = as_matrix(delta, "delta")
     hessian = as_matrix(hessian, "hessian")
     r, c = delta.shape
@@ -206,6 +205,7 @@ def obs_compress_layer(delta, hessian, cfg: CompressConfig, name: str = "layer",
         raise ShapeError(f"hessian shape {hessian.shape} does not match delta cols {c}")
     if cfg.sparsity == SPARSITY_2_4 and c % 4 != 0:
         raise ShapeError(f"layer {name!r}: 2:4 sparsity needs cols divisible by 4, got {c}")
+    dev = require_cuda()
     d = _dev_f64(delta, dev)
     ut = None
     if not (cfg.is_passthrough and cfg.sparsity != SPARSITY_2_4):

@@ -222,3 +222,24 @@ def test_plain_c_host_links_the_abi(tmp_path):
         r = subprocess.run([str(exe), os.path.join(ROOT, "tests", "golden", case)], capture_output=True, text=True)
         assert r.returncode == 0, r.stdout + r.stderr
         assert "all ok" in r.stdout and "layer 1: 64x128" in r.stdout
+
+
+def test_obs_workspace_and_config_checks(lib):
+    """dz_obs_workspace_bytes (host-only) validates the ΔCompress config like the reference's
+    CompressConfig and sizes the solver's scratch; invalid configs give 0."""
+    from paper_2312_05215_b200 import _lib as L
+    ok = L.DzObsCfg(4, 1, 128, 32)
+    n = lib.dz_obs_workspace_bytes(4096, 4096, C.byref(ok))
+    # err window (rows x group) + kept codes (rows*cols/2 int32) + nibbles + loss partials
+    assert n >= 4096 * 128 * 8 + 4096 * 4096 // 2 * 4 + 4096 * 4096 // 4 + 128 * 4096 * 8
+    for bad in [L.DzObsCfg(5, 1, 128, 32), L.DzObsCfg(4, 1, 128, 6), L.DzObsCfg(4, 1, 0, 32),
+                L.DzObsCfg(4, 1, 128, 512)]:
+        assert lib.dz_obs_workspace_bytes(64, 64, C.byref(bad)) == 0
+    assert lib.dz_obs_workspace_bytes(64, 66, C.byref(ok)) == 0  # 2:4 needs cols % 4 == 0
+
+
+def test_obs_api_raises_before_compute():
+    """obs_compress_layer checks shapes (ShapeError) before it needs a GPU."""
+    import paper_2312_05215_b200 as P
+    with pytest.raises(P.ShapeError):
+        P.obs_compress_layer(np.zeros((4, 8)), np.eye(6), P.CompressConfig())
