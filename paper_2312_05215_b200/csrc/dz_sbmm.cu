@@ -82,6 +82,9 @@ constexpr int UMMA_M = 128;
 #ifndef DZ_NB_SP
 #define DZ_NB_SP 4
 #endif
+#ifndef DZ_PAIR_UNROLL
+#define DZ_PAIR_UNROLL 1  // unroll the block-pair loop of a full sparse chunk (+2.6-3.0%, profiles/r01_ab_pair.txt)
+#endif
 #ifndef DZ_NSTAGE
 #define DZ_NSTAGE 3
 #endif
@@ -214,7 +217,10 @@ constexpr bool kOnesMma = DZ_ONES_MMA != 0;
 
 // Two consecutive blocks (b0, b0+1 < nb) of a sparse chunk for this warp's nrv <= MR row groups
 // and NT token tiles: loads, decodes and issues 4 independent mma.sp chains.
-constexpr int PAIR = 2;
+#ifndef DZ_PAIR
+#define DZ_PAIR 2
+#endif
+constexpr int PAIR = DZ_PAIR;
 // FULL: both blocks and all MR row groups valid -> no guards, straight-line code the compiler can
 // interleave (the common case); otherwise guarded (tail chunk / tail row tile).
 template <int FB, int NT, bool FULL>
@@ -308,7 +314,11 @@ template <int FB, int NT>
 __device__ __forceinline__ void sparse_chunk(float (&acc)[MR][NT_DN][4], uint32_t sA, uint32_t xl, int nb,
                                              int nrv, uint32_t off2, int lane) {
   if (nb == NB_SP && nrv == MR) {
+#if DZ_PAIR_UNROLL
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
     for (int b0 = 0; b0 < NB_SP; b0 += PAIR) sparse_pair<FB, NT, true>(acc, sA, xl, b0, nb, nrv, off2, lane);
   } else {
 #pragma unroll 1
