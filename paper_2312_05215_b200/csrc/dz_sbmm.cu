@@ -82,6 +82,9 @@ constexpr int UMMA_M = 128;
 #ifndef DZ_NB_SP
 #define DZ_NB_SP 4
 #endif
+#ifndef DZ_DRAIN_BATCH
+#define DZ_DRAIN_BATCH 1  // base drain: two TMEM loads per wait (+0.5-1.4%, profiles/r01_ab_drain.txt)
+#endif
 #ifndef DZ_PAIR_UNROLL
 #define DZ_PAIR_UNROLL 1  // unroll the block-pair loop of a full sparse chunk (+2.6-3.0%, profiles/r01_ab_pair.txt)
 #endif
@@ -423,6 +426,33 @@ __device__ __forceinline__ void drain_base_accumulator(uint32_t tmem_acc, int wa
   const int q = warp & 3, part = warp >> 2;
   const int row = row0 + 32 * q + lane;
   const uint32_t taddr = tmem_acc + (static_cast<uint32_t>(32 * q) << 16);
+#if DZ_DRAIN_BATCH
+  // both TMEM loads of a chunk pair in flight before one wait (half the load latencies)
+#pragma unroll 1
+  for (int c0 = part * PER; c0 < (part + 1) * PER; c0 += 2) {
+    if (c0 * 16 >= tcount) break;
+    uint32_t vv[2][16];
+    tmem_ld16(taddr + c0 * 16, vv[0]);
+    if ((c0 + 1) * 16 < tcount) tmem_ld16(taddr + (c0 + 1) * 16, vv[1]);
+    tmem_ld_wait();
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int c = c0 + h;
+      if (c * 16 >= tcount) break;
+      int tk[16], rw[16];
+      float x[16];
+      bool ok[16];
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        tk[j] = tok_begin + c * 16 + j;
+        rw[j] = row;
+        x[j] = __uint_as_float(vv[h][j]);
+        ok[j] = row < m.out && c * 16 + j < tcount;
+      }
+      merge_batch<16>(m, split, tk, rw, x, ok);
+    }
+  }
+#else
 #pragma unroll 1
   for (int c = part * PER; c < (part + 1) * PER; c++) {
     if (c * 16 >= tcount) break;
@@ -441,6 +471,7 @@ __device__ __forceinline__ void drain_base_accumulator(uint32_t tmem_acc, int wa
     }
     merge_batch<16>(m, split, tk, rw, x, ok);
   }
+#endif
 }
 
 // Dense-delta job partial (mma.sync fragments) -> merge.
