@@ -239,7 +239,7 @@ def measured_peaks():
 def ncu_traffic():
     """Per-launch DRAM bytes (read + write) of the fused kernel from the committed ncu --set full
     capture (profiles/), or None."""
-    p = os.path.join(ROOT, "profiles", "r01_ncu_traffic_v16.json")
+    p = os.path.join(ROOT, "profiles", "r01_ncu_traffic_v17.json")
     if not os.path.exists(p):
         return None, None
     with open(p) as f:
@@ -475,7 +475,7 @@ def main():
                          "traffic": traffic, "traffic_algorithmic": traffic_alg, "peak_kind": peak_kind,
                          "kernel": "k_sbmm (fused base GEMM + SBMM), all 4 x layers launches of one step (QKV, o, "
                                    "gate/up, down); achieved = algorithmic bytes / summed launch time; traffic = "
-                                   "mean DRAM bytes per launch (k_sbmm + k_finalize) from ncu --set full (profiles/r01_ncu_full_v16.md)",
+                                   "mean DRAM bytes per launch (k_sbmm + k_finalize) from ncu --set full (profiles/r01_ncu_full_v17.md)",
                          "per_launch_us": {n: float(np.mean(v) * 1e3) for n, v in per_name.items()},
                          "step_GBps": step_bytes / (ms * 1e-3) / 1e9},
             "clocks": clocks,
