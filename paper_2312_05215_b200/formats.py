@@ -19,6 +19,7 @@ import ctypes as C
 import json
 import mmap
 import os
+import traceback
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -226,17 +227,40 @@ def read_delta(path) -> CompressedDelta:
 
 
 def inspect_delta(path) -> tuple[dict, list[LayerSizes], float]:
-    """Reference formats.inspect_delta (formats.py:189-218)."""
+    """Reference formats.inspect_delta (formats.py:189-218): lenient like the reference — only the
+    magic and truncation are checked (FormatError with the offset); the version, the configuration
+    values and trailing bytes are not, and a bad JSON header raises json's own error."""
+    import struct
     with open(path, "rb") as f:
         data = f.read()
-    p = _parse(data)
+    if len(data) < 4:
+        raise FormatError("truncated file while reading magic", offset=0)
+    if data[:4] != DELTA_MAGIC:
+        raise FormatError("bad magic", offset=0)
+    if len(data) < 12:
+        raise FormatError("truncated file while reading the container header", offset=min(len(data), 8))
+    (hlen,) = struct.unpack_from("<I", data, 8)
+    if 12 + hlen > len(data):
+        raise FormatError("truncated file while reading header", offset=12)
+    header = json.loads(data[12:12 + hlen].decode("utf-8"))
+    count = header["layer_count"]
+    lib = L.lib()
+    ptr, keep = _buf_ptr(data)
+    recs = (L.DzDzdlLayer * max(count, 1))()
+    off = C.c_int64(0)
+    st = lib.dz_dzdl_parse_layers(ptr, len(data), 12 + hlen, count, recs, C.byref(off))
+    if st == L.DZ_E_FORMAT:
+        raise FormatError("truncated file while reading a layer record", offset=off.value)
+    if st not in (L.DZ_OK, L.DZ_E_VALUE):  # DZ_E_VALUE = trailing bytes: ignored, as the reference does
+        L.check(st, "dzdl layers")
+    del keep
     sizes = []
-    for rec in p.layers:
-        name = bytes(np.frombuffer(data, np.uint8)[rec.name_off: rec.name_off + rec.name_len]).decode("utf-8")
+    for rec in list(recs)[:count]:
+        name = data[rec.name_off: rec.name_off + rec.name_len].decode("utf-8")
         sizes.append(LayerSizes(name, int(rec.rows), int(rec.cols), int(rec.scales_len), int(rec.index_len),
                                 int(rec.payload_len)))
     dense = sum(s.dense16_bytes for s in sizes)
-    return p.header, sizes, (dense / len(data) if data else 0.0)
+    return header, sizes, (dense / len(data) if data else 0.0)
 
 
 class _PinnedLayer:
@@ -268,22 +292,33 @@ def load_delta(path, device=None):
     dev = device or require_cuda()
     with open(path, "rb") as f:
         mm = mmap.mmap(f.fileno(), 0, access=mmap.ACCESS_READ) if os.path.getsize(path) else b""
-        try:
-            p = _parse(mm)
-            staged = []
-            for rec in p.layers:
-                name, payload, index, scales = _layer_arrays(p, rec)
-                staged.append(_PinnedLayer((name, payload, index, scales, int(rec.rows), int(rec.cols), p.config), dev))
-                del payload, index, scales  # views into the mapping: released before it closes
-            natives = [NativeDelta.from_ref_device(s.dev, s.ld) for s in staged]
-            torch.cuda.current_stream(dev).synchronize()  # pinned staging buffers may be released now
-            meta = CompressedDelta(base_model_id=p.header["base_model_id"], layers=[s.ld for s in staged],
-                                   config=p.config, calibration_fingerprint=p.header["calibration_fingerprint"])
-        finally:
-            if isinstance(mm, mmap.mmap):
-                del p
-                mm.close()
+    try:
+        meta, staged = _stage_layers(mm, dev)  # every layer copied out of the mapping
+    except BaseException as e:
+        # the traceback's frames hold numpy views of the mapping: drop them so it can close, and the
+        # caller sees the parser's own FormatError / EncodingError (formats.py:102-169)
+        traceback.clear_frames(e.__traceback__)
+        if isinstance(mm, mmap.mmap):
+            mm.close()
+        raise
+    if isinstance(mm, mmap.mmap):
+        mm.close()
+    natives = [NativeDelta.from_ref_device(s.dev, s.ld) for s in staged]
+    torch.cuda.current_stream(dev).synchronize()  # pinned staging buffers may be released now
     return meta, natives
+
+
+def _stage_layers(buf, dev):
+    """Parse a DZDL buffer and stage every layer in pinned host memory (async H2D started)."""
+    p = _parse(buf)
+    staged = []
+    for rec in p.layers:
+        name, payload, index, scales = _layer_arrays(p, rec)
+        staged.append(_PinnedLayer((name, payload, index, scales, int(rec.rows), int(rec.cols), p.config), dev))
+        del payload, index, scales  # views into the mapping: released before it closes
+    meta = CompressedDelta(base_model_id=p.header["base_model_id"], layers=[s.ld for s in staged],
+                           config=p.config, calibration_fingerprint=p.header["calibration_fingerprint"])
+    return meta, staged
 
 
 class DeltaPool:

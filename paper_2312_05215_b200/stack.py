@@ -88,7 +88,10 @@ class LlamaStack:
     rank, so the shards of all ranks partition one model), then sharded and row-fused."""
 
     def __init__(self, model: str, layers: int, n_deltas: int, bits: int, device, rank: int = 0, world: int = 1,
-                 seed: int = 10_000, group=None):
+                 seed: int = 10_000, group=None, keep_refs: bool = False):
+        """keep_refs: also keep every ORIGINAL (unsharded, unfused) linear's bf16 base weight in
+        `base_full[(layer, name)]` and its deltas' reference-layout bytes in `refs[(layer, name, d)]`
+        (the parity tests rebuild each linear's reference output from them)."""
         self.model, self.layers, self.n_deltas, self.bits = model, layers, n_deltas, bits
         self.rank, self.world, self.group, self.device = rank, world, group, device
         shapes = {n: (o, i) for n, o, i in llama_linears(model)}
@@ -100,6 +103,8 @@ class LlamaStack:
         gen = torch.Generator(device=device)
         err = ErrFlag(device)
         self.stack: list[dict[str, FusedLinear]] = []
+        self.base_full: dict = {}
+        self.refs: dict = {}
         for l in range(layers):
             lin = {}
             for fname, members in FUSED.items():
@@ -111,9 +116,14 @@ class LlamaStack:
                     gen.manual_seed(seed + 7 * l + names.index(m))
                     Wf = random_base(out, inp, gen, device)
                     Ws.append(Wf[r0:r1, c0:c1].contiguous())
+                    if keep_refs:
+                        self.base_full[(l, m)] = Wf
                     del Wf
                     for d in range(n_deltas):
-                        nat = random_native_delta(out, inp, bits, gen, device, err)
+                        kr = [] if keep_refs else None
+                        nat = random_native_delta(out, inp, bits, gen, device, err, keep_ref=kr)
+                        if keep_refs:
+                            self.refs[(l, m, d)] = kr[0]
                         per_delta[d].append(shard_sub(nat, r0, r1, c0, c1))
                 W = torch.cat(Ws) if len(Ws) > 1 else Ws[0]
                 nats = [concat_rows(p) if len(p) > 1 else p[0] for p in per_delta]

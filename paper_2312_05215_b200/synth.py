@@ -57,14 +57,18 @@ def random_ref_delta_device(rows: int, cols: int, bits: int, gen: torch.Generato
 
 
 def random_native_delta(rows: int, cols: int, bits: int, gen: torch.Generator, device,
-                        err: ErrFlag | None = None) -> NativeDelta:
+                        err: ErrFlag | None = None, keep_ref: list | None = None) -> NativeDelta:
+    """keep_ref: a list that receives (DzRefDelta, tensors) — the reference-layout bytes the
+    native blocks were built from (parity tests dequantise them with K1 as the reference does)."""
     st, keep = random_ref_delta_device(rows, cols, bits, gen, device)
+    if keep_ref is not None:
+        keep_ref.append((st, keep))
     lib = L.lib()
     nbytes = lib.dz_native_sparse_bytes(rows, cols, bits)
     blocks = torch.empty(nbytes, dtype=torch.uint8, device=device)
     err = err or ErrFlag(device)
     L.check(lib.dz_repack_sparse(st, blocks.data_ptr(), err.ptr, stream_ptr()), "synthetic delta upload")
-    del keep
+    del keep, st
     kind = {2: L.DZ_KIND_SPARSE2, 3: L.DZ_KIND_SPARSE3, 4: L.DZ_KIND_SPARSE4}[bits]
     return NativeDelta(kind, (1 << (bits - 1)) - 1, rows, cols, blocks, bits)
 

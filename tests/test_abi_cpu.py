@@ -243,3 +243,18 @@ def test_obs_api_raises_before_compute():
     import paper_2312_05215_b200 as P
     with pytest.raises(P.ShapeError):
         P.obs_compress_layer(np.zeros((4, 8)), np.eye(6), P.CompressConfig())
+
+
+def test_group_by_delta_large_groups_matches_reference_rule():
+    """group_by_delta is the stable sort of the reference (inference.py:106-123) at any group size:
+    a group past the prefill threshold (>= 192 rows) must not turn `order` into a staged-row
+    index list."""
+    import paper_2312_05215_b200 as P
+    import oracle as O
+    rng = np.random.default_rng(5)
+    for ids in ([0] * 195 + [1] * 5, list(rng.permutation([0] * 300 + [3] * 7 + [1] * 250)),
+                list(rng.integers(0, 4, 1000)), [7] * 256):
+        batch = P.BatchInput([(i, int(d), np.zeros(2)) for i, d in enumerate(ids)])
+        perm, groups = P.group_by_delta(batch)
+        rperm, rgroups = O.group_by_delta([int(d) for d in ids])
+        assert perm == list(rperm) and [tuple(g) for g in groups] == [tuple(g) for g in rgroups]

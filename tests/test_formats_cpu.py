@@ -158,3 +158,31 @@ def test_write_delta_is_byte_identical_to_reference_files():
             out = os.path.join(d, "x.dzdl")
             write_delta(cd, out)
             assert open(out, "rb").read() == open(f, "rb").read(), f
+
+
+def test_inspect_delta_is_lenient_like_the_reference(F, tmp_path):
+    """Reference inspect_delta (formats.py:189-218) checks only the magic and truncation: trailing
+    bytes, an unknown version and out-of-range configuration values are reported, not rejected."""
+    base = F.inspect_delta(os.path.join(GOLD, "dzdl_b4.dzdl"))
+    p = tmp_path / "t.dzdl"
+    p.write_bytes(_blob() + b"xx")
+    header, sizes, _ = F.inspect_delta(p)
+    assert header == base[0] and [s.payload_bytes for s in sizes] == [s.payload_bytes for s in base[1]]
+    b = bytearray(_blob())
+    b[4] = 7  # version 7
+    p.write_bytes(bytes(b))
+    assert F.inspect_delta(p)[0] == base[0]
+    blob = _blob()
+    hlen = int.from_bytes(blob[8:12], "little")
+    hdr = json.loads(blob[12:12 + hlen])
+    hdr["bits"] = 5  # CompressConfig would reject it; inspect does not validate
+    hb = json.dumps(hdr, sort_keys=True).encode()
+    p.write_bytes(blob[:8] + len(hb).to_bytes(4, "little") + hb + blob[12 + hlen:])
+    assert F.inspect_delta(p)[0]["bits"] == 5
+    with pytest.raises(F.FormatError, match="magic"):
+        p.write_bytes(b"NOPE" + blob[4:])
+        F.inspect_delta(p)
+    p.write_bytes(blob[: len(blob) - 5])
+    with pytest.raises(F.FormatError) as ei:
+        F.inspect_delta(p)
+    assert ei.value.offset is not None

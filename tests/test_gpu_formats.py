@@ -74,3 +74,24 @@ def test_pool_tp_shards_partition_the_delta(F):
     full1 = pool1.deltas[0][1].to_dense_f32()
     cat1 = torch.cat([p.deltas[0][1].to_dense_f32() for p in pool2], dim=0)  # column-parallel: output rows
     assert torch.equal(full1, cat1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("damage", ["magic", "truncate", "trailing", "deflate"])
+def test_load_delta_corrupt_file_raises_format_error(F, tmp_path, damage):
+    """A corrupt container raises the reference's FormatError from load_delta (never an
+    UnboundLocalError / BufferError from closing the mapping)."""
+    case = "dzdl_b4_deflate" if damage == "deflate" else "dzdl_b4"
+    blob = bytearray(open(os.path.join(GOLD, case + ".dzdl"), "rb").read())
+    if damage == "magic":
+        blob[:4] = b"NOPE"
+    elif damage == "truncate":
+        blob = blob[: len(blob) - 10]
+    elif damage == "trailing":
+        blob += b"xx"
+    else:
+        blob[len(blob) - 40: len(blob) - 32] = b"\xff" * 8  # inside the last layer's deflate payload
+    p = tmp_path / "bad.dzdl"
+    p.write_bytes(bytes(blob))
+    with pytest.raises(F.FormatError):
+        F.load_delta(str(p))

@@ -309,9 +309,11 @@ def test_full_size_llama_linear(P, out_f, in_f, bits):
     assert rel_err_rows(Y[:2].double().cpu().numpy(), Ro).max() <= REL_TOL
 
 
-def test_sbmm_api_large_group_takes_prefill_path(P):
-    """The drop-in `sbmm` (inference.py:126-154) on a batch whose main group is above the prefill
-    threshold: the mixed plan (K3 tcgen05 prefill + K2 decode) matches the reference oracle."""
+def test_sbmm_api_large_group_batch_invariant(P):
+    """The drop-in `sbmm` (inference.py:126-154) on a batch whose main group is far above the
+    engine's prefill threshold stays on the decode kernel (pf_min=0): it matches the reference
+    oracle, and every row equals its solo `decoupled_linear` call bit for bit (the reference's
+    batch invariance, test_inference.py:105-147)."""
     from paper_2312_05215_b200.engine import PF_MIN
     rng = np.random.default_rng(31)
     W, ods, pds, X, _ = _random_case(P, rng, 192, 384, 4, 3, 8)
@@ -321,3 +323,5 @@ def test_sbmm_api_large_group_takes_prefill_path(P):
     Y = np.stack([out[i] for i in range(ids.size)])
     R = O.sbmm_matrix(W, ods, ids, X)
     assert rel_err_rows(Y, R).max() <= REL_TOL
+    for i in (0, 1, PF_MIN + 49, ids.size - 1):
+        assert np.array_equal(out[i], P.decoupled_linear(W, pds[int(ids[i])], X[i])), i
