@@ -104,7 +104,8 @@ typedef struct dz_sbmm_args {
   const dz_job* jobs;       /* device [n_jobs]                                       */
   int32_t n_jobs;
   void* workspace;          /* dz_sbmm_workspace_bytes(T, out) bytes, zeroed once at
-                               allocation; the kernel leaves it zero after every call */
+                               allocation; the kernel re-zeroes its counters after every call
+                               (one workspace per stream: launches on it must not overlap) */
   int32_t grid;             /* persistent CTAs; 0 = one per SM                       */
   int32_t debug;            /* 0; bit 0 = skip consumer math (pipeline bandwidth probe) */
   /* Mixed prefill + decode batches (dz_plan_mixed). perm == NULL: pure decode plan, X is used
@@ -124,8 +125,10 @@ typedef struct dz_sbmm_args {
                                row-parallel linear (decode plans only, see dz_tp_ctx)    */
   const int32_t* n_jobs_dev; /* device job count written by dz_plan_device, or NULL; when set,
                                n_jobs is only the capacity of `jobs` (grid sizing)       */
-  int32_t fin_inline;       /* set by dz_sbmm (callers leave 0): finalize inside the kernel */
-  int32_t _pad4;
+  int32_t keep_planes;      /* set by dz_sbmm (callers leave 0): 1 = leave the fp32 partial planes
+                               for the TP peer reduction instead of writing Y in the kernel */
+  int32_t prefill_variant;  /* K3 delta product: 0 = 2:4-sparse tcgen05 (default); 1 / 2 =
+                               dense-dequantised with 128- / 256-row items (A/B and tests) */
   const struct dz_sbmm_args* next; /* device copy of the NEXT linear's args in the step, or NULL:
                                CTAs that run out of items warm L2 with the first weight stages
                                their blockIdx gets in that launch (decode plans only)      */
@@ -231,12 +234,13 @@ int dz_plan_device(const int32_t* slots_dev, int32_t T, const int32_t* kinds_dev
                    int32_t* n_jobs_dev, int32_t* err_dev, void* stream);
 /* K2 — fused decode SBMM. Replaces inference.sbmm (inference.py:126-154):
  * Y[t] = W_base x_t + ΔW_{slot(t)} x_t for every token in ONE persistent launch:
- * TMA bulk copies stage native blocks and X through shared memory, warps decode
- * codes in registers and issue mma.sp (2:4) / mma (dense) with fp32 accumulation,
- * per-(row,128-col) scales are applied per block, and the base and delta partials
- * are combined by the last work item of each row tile (no separate add kernel).
- * Deterministic and batch-invariant: a token's result does not depend on the
- * other tokens in the call. */
+ * TMA stages W tiles (tcgen05.mma into TMEM), native delta blocks and X through
+ * shared memory, warps decode codes in registers and issue mma.sp (2:4) / mma (dense)
+ * with fp32 accumulation, per-(row,128-col) scales are applied per block. The base and
+ * delta partials of each 32-row output slice are summed, in a fixed order, by the warp
+ * that completes the slice (an arrival counter per slice), which also applies the
+ * activation and writes Y: no separate add kernel, no grid barrier. Deterministic and
+ * batch-invariant: a token's result does not depend on the other tokens in the call. */
 size_t dz_sbmm_workspace_bytes(int32_t T, int32_t out);
 /* K3 — prefill SBMM (dz_prefill.cu), launched by dz_sbmm for the prefill jobs of a mixed plan:
  * per (128-row tile, <= 256-token group) one TMEM accumulator receives tcgen05 MMAs of the base

@@ -64,7 +64,7 @@ class DzSbmmArgs(C.Structure):
         ("base_splits", C.c_int32), ("delta_splits", C.c_int32),
         ("tp", C.c_void_p),
         ("n_jobs_dev", C.c_void_p),
-        ("fin_inline", C.c_int32), ("_pad4", C.c_int32),
+        ("keep_planes", C.c_int32), ("prefill_variant", C.c_int32),
         ("next", C.c_void_p),
     ]
 

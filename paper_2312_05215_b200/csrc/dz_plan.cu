@@ -1,5 +1,6 @@
 // On-device plan (dz_plan_device) — group_by_delta (inference.py:106-123) and the dz_plan job cut
 // computed on the GPU from device-resident slots, so a decode loop needs no host round trip.
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -93,11 +94,10 @@ extern "C" int dz_plan_device(const int32_t* slots_dev, int32_t T, const int32_t
   if (T < 0 || n_slots < 1 || n_slots > 4096 || !n_jobs_dev || !err_dev || max_jobs < 0) return DZ_E_VALUE;
   if (T > 0 && (!slots_dev || !order_dev || !jobs_dev || !kinds_dev)) return DZ_E_VALUE;
   const size_t smem = static_cast<size_t>(3) * n_slots * sizeof(int);
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag once;  // one-time, idempotent kernel attribute setup
+  std::call_once(once, [] {
     cudaFuncSetAttribute(plan::k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 4096 * 4);
-    attr = true;
-  }
+  });
   plan::k_plan<<<1, 1024, smem, static_cast<cudaStream_t>(stream)>>>(slots_dev, T, kinds_dev, n_slots, with_base,
                                                                    order_dev, jobs_dev, max_jobs, n_jobs_dev, err_dev);
   return cudaGetLastError() == cudaSuccess ? DZ_OK : DZ_E_CUDA;

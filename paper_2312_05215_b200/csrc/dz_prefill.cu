@@ -613,14 +613,14 @@ extern "C" int dz_sbmm_prefill(const dz_sbmm_args* a, void* stream) {
   // time ~ rounds x rows per item / per-item efficiency. Measured (profiles/r01_pf_mt.txt): MT=2 is
   // 7-33% slower at every 13B shape (2-stage ring, exposed epilogue), so MT=1 unless overridden.
   const double t1 = ceil_div(items1, g) * 1.0 / 0.75, t2 = ceil_div(items2, g) * 2.0 / 0.62;
+  // 2:4-sparse tcgen05 delta product by default (8-23% faster than the dense-dequantised one at the
+  // 13B shapes, profiles/r01_pf_sparse.txt); args.prefill_variant selects the dense-dequantised
+  // delta product with 128-row (1) or 256-row (2) items for A/B runs and the equivalence tests.
+  if (a->prefill_variant < 0 || a->prefill_variant > 2) return DZ_E_VALUE;
   int mt = t2 < t1 ? 2 : 1;
-  const char* e = std::getenv("DZ_PF_MT");  // experiment override (A/B)
-  if (e && (e[0] == '1' || e[0] == '2')) mt = e[0] - '0';
+  if (a->prefill_variant > 0) mt = a->prefill_variant;
   const int n_items = mt == 2 ? items2 : items1;
   const int grid = g > n_items ? n_items : g;
-  // 2:4-sparse tcgen05 delta product by default (8-23% faster than the dense-dequantised one at the
-  // 13B shapes, profiles/r01_pf_sparse.txt); DZ_PF_SPARSE=0 selects the dense variant (A/B)
-  const char* sp = std::getenv("DZ_PF_SPARSE");
-  if (!(sp && sp[0] == '0') && mt == 1) return launch_prefill<1, true>(*a, xmap, grid, stream);
+  if (a->prefill_variant == 0 && mt == 1) return launch_prefill<1, true>(*a, xmap, grid, stream);
   return mt == 2 ? launch_prefill<2, false>(*a, xmap, grid, stream) : launch_prefill<1, false>(*a, xmap, grid, stream);
 }

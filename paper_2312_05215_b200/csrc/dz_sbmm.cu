@@ -23,12 +23,14 @@
 //    (the reference's index nibble IS the sparse-MMA metadata), fp32 accumulation; dense-delta
 //    stages use mma m16n8k16. They also drain the base accumulator from TMEM (tcgen05.ld).
 //
-// Merge: every output element y[t][r] receives exactly two fp32 contributions — the base job of
-// token t and the single delta job of t's group. Each contributor publishes its value with a 64-bit
-// CAS on a {value, count} workspace word; the second arriver computes fl(base + delta) (two-term
-// fp32 addition is commutative, so the result does not depend on arrival order), applies the
-// activation, writes Y and resets the word. No partial buffers, no combine pass, no separate add
-// kernel; deterministic and batch-invariant (a token's K order never depends on the batch).
+// Merge (no separate add kernel): the base items come first in the item order and store their fp32
+// partial per K-split into workspace planes, then publish each 32-row slice on its counter. The delta
+// item of a token (every token has exactly one) waits for its slice's base publications — in
+// practice already there: base items are short (K-split) and claimed first — and writes
+// y = act(((P_0 + P_1) + ...) + delta) straight from its registers. Deterministic and
+// batch-invariant: the summation order is fixed per element and the split count depends on the
+// shape only. TP row-parallel shards and delta K-splits keep every partial in planes for a
+// separate reduction (k_tp_finalize / k_finalize).
 //
 // Mixed batches: groups large enough for the tensor-core prefill kernel (K3, dz_prefill.cu) are
 // staged first in a permuted copy of X; this kernel then covers the remaining (decode) rows and
@@ -64,15 +66,13 @@ __device__ unsigned long long dz_item_trace[65536][3];  // per item: start, end,
 
 namespace dz {
 
-#ifndef DZ_NW
-#define DZ_NW 8
-#endif
-constexpr int NW = DZ_NW;                 // consumer warps per CTA (one CTA per SM)
+constexpr int NW = 8;                     // consumer warps per CTA (one CTA per SM); 16 measured -1.5%
 constexpr int MR = 16 / NW;               // 16-row groups per consumer warp (RG = 16 per item)
 constexpr int WARP_PROD = NW;             // TMA producer warp
 constexpr int WARP_MMA = NW + 1;          // tcgen05 issuer / TMEM owner warp
 constexpr int WARP_XPROD = NW + 2;        // per-token X copies of delta stages
-constexpr int NTHREADS = (NW + 3) * 32;
+constexpr int WARP_COMB = NW + 3;         // fused merge: combines each delta item's tokens into Y
+constexpr int NTHREADS = (NW + 4) * 32;
 constexpr int RG = NW * MR;               // row groups per item
 constexpr int RT = RG * kBlkRows;         // rows per item (256) == 2 x UMMA M
 constexpr int UMMA_M = 128;
@@ -115,6 +115,11 @@ constexpr int TMEM_COLS = 2 * BASE_N;     // double-buffered fp32 accumulator, 1
 constexpr uint32_t IDESC_BASE = umma_idesc_bf16(UMMA_M, BASE_N);
 constexpr int STAGE_BYTES = (cmax(cmax(A_SP + X_SP, A_DN + X_DN), A_DN + BASE_CH * KC_DN * BASE_N * 2) + 1023) / 1024 * 1024;
 constexpr int PF_CHUNKS = 4;              // stages of the first item prefetched into L2 before the PDL wait
+// Workspace: [0, 256) scheduler words; [256, +4*MAX_SLICES) per-32-row-slice arrival counters;
+// then the fp32 partial planes [base K-splits + delta K-splits][T][out].
+constexpr int MAX_SLICES = 8192;          // out <= 262144 rows per launch
+constexpr int DZ_WS_CNT_OFF = 256;
+constexpr int DZ_WS_PART_OFF = DZ_WS_CNT_OFF + 4 * MAX_SLICES;
 
 struct StageHdr {
   int item;       // -1: end of work
@@ -134,8 +139,12 @@ struct Smem {
   uint64_t tmem_full[2];
   uint64_t tmem_empty[2];
   StageHdr hdr[NSTAGE];
+  uint64_t mfull[4];       // consumer warps -> combiner: the item's partial planes are stored
+  uint64_t mempty[4];      // combiner -> consumers: the record slot may be reused
   uint32_t tmem_base;
   int tok_ids[NSTAGE][JOB_DN_TOK];  // token ids of the item, staged with its last chunk
+  int recs[4][36];                  // MergeRec ring (fused merge)
+  int comb_tok[32];                 // the combiner's current token list
 };
 constexpr int SMEM_BYTES = 1024 + STAGE_BYTES * NSTAGE + static_cast<int>(sizeof(Smem));
 
@@ -164,16 +173,31 @@ __device__ __forceinline__ void item_coords(int item, int nrt, int nbt, int nspl
   }
 }
 
-// Default base K-splits when the caller passes 0: one split (measured best at the BASELINE decode
-// batch, T=64 with 32 deltas, for every 7B shape: profiles/r01_ab_splits.txt). Low-batch serving
-// (T <= 16) gains up to +30% with 4 splits, which a deployment selects explicitly through
-// dz_sbmm_args.base_splits. The split count is never derived from the batch, so a token's
-// result does not depend on the other tokens of the call.
-__host__ __device__ inline int base_splits(int /*out*/, int /*in*/) { return 1; }
+// Default base K-splits when the caller passes 0: one (the BASELINE decode step, T=64 with 32 deltas:
+// 3743 tok/s at 1 split, 3714 at 2, 3578 at 4 with the fused merge; profiles/r02_ab_fused_splits.txt).
+// Low-batch serving gains from more base items, which a deployment selects through
+// dz_sbmm_args.base_splits. The split count is never derived from the batch, so a token's result
+// does not depend on the other tokens of the call.
+#ifndef DZ_DEFAULT_BASE_SPLITS
+#define DZ_DEFAULT_BASE_SPLITS 1
+#endif
+__host__ __device__ inline int base_splits(int /*out*/, int /*in*/) { return DZ_DEFAULT_BASE_SPLITS; }
 // Default K-splits of each decode delta job: 1. Splitting the delta items of the out <= 4096 layers
 // in two measured neutral at the BASELINE batch and mixed at low batch (profiles/r01_ab_dsplit.txt),
 // so it stays an explicit knob (dz_sbmm_args.delta_splits). Never derived from the batch.
 __host__ __device__ inline int delta_splits(int /*out*/, int /*in*/) { return 1; }
+// The K-split counts a launch actually uses: the requested (or shape-default) counts, capped so that
+// every split owns at least one K-chunk (a split without chunks would never publish its partial).
+__host__ __device__ inline void resolve_splits(int out, int in, bool has_base, int& bs, int& ds) {
+  if (bs <= 0) bs = base_splits(out, in);
+  if (ds <= 0) ds = delta_splits(out, in);
+  const int nch_base = ceil_div(in, BASE_CH * KC_DN), nch_sp = ceil_div(ceil_div(in, kBlkCols), NB_SP);
+  bs = bs > 4 ? 4 : bs;
+  bs = bs > nch_base ? nch_base : bs;
+  ds = ds > 2 ? 2 : ds;
+  ds = ds > nch_sp ? nch_sp : ds;
+  if (!has_base) ds = 1;  // single contributor: the delta writes Y directly
+}
 
 __device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
   int old;
@@ -370,12 +394,16 @@ __device__ __forceinline__ void dense_dispatch(int nt, float (&acc)[MR][NT_DN][4
 }
 
 struct MergeCtx {
-  float* part;                // [nsplit + 1][T][out] fp32 partials (workspace)
+  float* part;                // [planes][T][out] fp32 partials (workspace)
+  int* slice_cnt;             // [ceil(out / 32)] arrival counters (workspace, zero between launches)
   const int32_t* perm;        // staged row -> Y row (mixed plans), or NULL
   void* Y;
   int64_t ldy;
   int out, y_dtype, act, debug, T, nsplit;
+  int base_target;            // base-plane publications per 32-row slice (2 warps x base jobs x K-splits)
+  int readers;                // delta items combining per slice (the decode delta jobs)
   bool has_base;
+  bool fused;                 // delta items combine base planes + their product into Y (else: planes only)
 };
 
 __device__ __forceinline__ void store_y(const MergeCtx& m, int tok, int row, float v) {
@@ -389,10 +417,11 @@ __device__ __forceinline__ void store_y(const MergeCtx& m, int tok, int row, flo
 }
 
 // Publish N fp32 partials v[i] of y[tok[i]][row[i]] (valid[i]) into partial slot `slot` of the
-// workspace: [nsplit + 1][T][out] fp32, slot s < nsplit = base K-split s, slot nsplit = the
-// token's delta job. Plain stores — every (slot, token, row) has exactly one producer — so the
-// epilogue never waits on a round trip; k_finalize sums the slots in a fixed order and applies
-// the activation. Without a base there is a single contributor and Y is written directly.
+// workspace: [planes][T][out] fp32, slot s < nsplit = base K-split s, slots nsplit.. = the
+// token's delta job (per delta K-split). Plain stores — every (slot, token, row) has exactly one
+// producer. With the fused merge the CTA's combiner warp sums the planes of each delta item's
+// tokens into Y (see combine_tokens). Without a base there is a single contributor and Y is
+// written directly.
 template <int N>
 __device__ __forceinline__ void merge_batch(const MergeCtx& m, int slot, const int (&tok)[N], const int (&row)[N],
                                             const float (&v)[N], const bool (&valid)[N]) {
@@ -544,8 +573,8 @@ __device__ __forceinline__ void finalize_rows(const float* __restrict__ part, in
 
 // Finalize the merged decode rows [t0, T): Y[perm[t]][r] = act(((P_0 + P_1) + ... + P_{S-1}) + P_S)
 // with P_s the base K-split partials and the delta partials after them — a fixed summation order,
-// so the result is deterministic and independent of the batch. With DZ_FIN_INLINE=1, k_sbmm runs
-// the same code itself after a grid barrier instead.
+// so the result is deterministic and independent of the batch. Only for launches that keep every
+// partial in planes (delta K-splits); the default decode launch merges inside k_sbmm.
 __global__ void __launch_bounds__(256) k_finalize(const float* __restrict__ part, int nsplit, int t0, int T, int out,
                                                   const int32_t* __restrict__ perm, void* __restrict__ Y, int64_t ldy,
                                                   int y_dtype, int act) {
@@ -553,29 +582,6 @@ __global__ void __launch_bounds__(256) k_finalize(const float* __restrict__ part
   griddep_launch_dependents();
   finalize_rows(part, nsplit, t0, T, out, perm, Y, ldy, y_dtype, act,
                 blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x, static_cast<int64_t>(gridDim.x) * blockDim.x);
-}
-
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Sense-reversal grid barrier over co-resident CTAs (count + generation words in the workspace).
-__device__ __forceinline__ void grid_sync(unsigned* count, unsigned* gen) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned g = ld_acquire_u32(gen);
-    __threadfence();
-    if (atomicAdd(count, 1u) == gridDim.x - 1) {
-      *count = 0;
-      __threadfence();
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(g + 1) : "memory");
-    } else {
-      while (ld_acquire_u32(gen) == g) __nanosleep(32);
-    }
-  }
-  __syncthreads();
 }
 
 // Tail prefetch: a CTA with no more items warms L2 with the first weight stages of the item its
@@ -591,8 +597,8 @@ __device__ __forceinline__ void tail_prefetch(const dz_sbmm_args& nx) {
   const int nch_base = ceil_div(nx.in, BASE_CH * KC_DN);
   const int n_base = nx.base != nullptr ? ceil_div(nx.T, BASE_N) : 0;
   const int n_jobs = nx.n_jobs_dev != nullptr ? *nx.n_jobs_dev : nx.n_jobs;
-  const int nsplit = nx.base_splits > 0 ? nx.base_splits : base_splits(nx.out, nx.in);
-  const int dsplit = nx.base == nullptr ? 1 : nx.delta_splits > 0 ? nx.delta_splits : delta_splits(nx.out, nx.in);
+  int nsplit = nx.base_splits, dsplit = nx.delta_splits;
+  resolve_splits(nx.out, nx.in, nx.base != nullptr, nsplit, dsplit);
   const int n_items = n_jobs < n_base ? 0 : nbt * nsplit * n_base + nrt * (n_jobs - n_base) * dsplit;
   const int item = blockIdx.x;
   if (item >= n_items) return;
@@ -614,6 +620,125 @@ __device__ __forceinline__ void tail_prefetch(const dz_sbmm_args& nx) {
   }
 }
 
+// ---- fused merge (combiner warp) ---------------------------------------------------------------
+// Every work item's contributions go to fp32 planes with plain stores (base K-split s -> plane s,
+// the token's delta -> plane nsplit), as in the unfused layout. After an item, the consumer warps
+// arrive on a shared-memory record ring; the CTA's combiner warp then
+//   * base item: publishes the item's four 32-row slices on their counters (fence + relaxed add);
+//   * delta item: waits until every base contribution of its eight slices is published (acquire),
+//     writes y = act(((P_0 + P_1) + ...) + P_delta) for the item's tokens and rows, and counts
+//     itself as a reader in the counters' high bits; the last reader re-arms the counter.
+// Every output element is written exactly once, by the delta item of its token, with a fixed
+// summation order (deterministic, batch-invariant). A combiner only ever waits on base items,
+// which are first in the item order and never wait, so the persistent grid cannot deadlock; the
+// consumers never wait on a round trip.
+constexpr int MREC = 4;                   // records in flight (consumer warps -> combiner)
+struct MergeRec {
+  int rt;        // row tile (base: 128-row tile, delta: 256-row tile); -1 = end of work
+  int is_base;
+  int ntok;      // delta: tokens of the job (<= 32)
+  int pad;
+  int tok[32];   // delta: the job's token (staged row) ids
+};
+
+__device__ __forceinline__ int ld_relaxed_s32(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_add_s32(int* p, int v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Y rows [r0, r0 + 256) of the `ntok` tokens `tok[]`: planes 0..nsplit (base splits, then the delta)
+// summed in that order. Lanes own row quads; all plane loads of a token are issued before use.
+__device__ __noinline__ void combine_tokens(const MergeCtx m, int r0, int ntok, const int* tok, int lane) {
+  const int64_t plane = static_cast<int64_t>(m.T) * m.out;
+  const bool vec = (m.out % 4) == 0 && (m.ldy % 4) == 0 && (reinterpret_cast<uintptr_t>(m.Y) & 15) == 0;
+  if (vec) {
+#pragma unroll 1
+    for (int i = 0; i < ntok; i++) {
+      const int t = tok[i];
+      float4 v[2];
+      bool ok[2];
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int r = r0 + 4 * (lane + 32 * h);
+        ok[h] = r < m.out;
+        if (ok[h]) v[h] = __ldcg(reinterpret_cast<const float4*>(m.part + static_cast<int64_t>(t) * m.out + r));
+      }
+      for (int sp = 1; sp <= m.nsplit; sp++) {
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int r = r0 + 4 * (lane + 32 * h);
+          if (ok[h]) {
+            const float4 w = __ldcg(reinterpret_cast<const float4*>(m.part + sp * plane + static_cast<int64_t>(t) * m.out + r));
+            v[h].x += w.x; v[h].y += w.y; v[h].z += w.z; v[h].w += w.w;
+          }
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        if (!ok[h]) continue;
+        float4 y = v[h];
+        if (m.act == DZ_ACT_TANH) { y.x = tanhf(y.x); y.y = tanhf(y.y); y.z = tanhf(y.z); y.w = tanhf(y.w); }
+        const int yr = m.perm != nullptr ? __ldg(m.perm + t) : t;
+        const int64_t yo = static_cast<int64_t>(yr) * m.ldy + r0 + 4 * (lane + 32 * h);
+        if (m.y_dtype == DZ_F32) {
+          *reinterpret_cast<float4*>(reinterpret_cast<float*>(m.Y) + yo) = y;
+        } else {
+          const __nv_bfloat162 lo = __floats2bfloat162_rn(y.x, y.y), hi = __floats2bfloat162_rn(y.z, y.w);
+          uint2 w;
+          w.x = *reinterpret_cast<const uint32_t*>(&lo);
+          w.y = *reinterpret_cast<const uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(m.Y) + yo) = w;
+        }
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int i = 0; i < ntok; i++) {
+      const int t = tok[i];
+      for (int r = r0 + lane; r < r0 + RT && r < m.out; r += 32) {
+        const float* p = m.part + static_cast<int64_t>(t) * m.out + r;
+        float v = __ldcg(p);
+        for (int sp = 1; sp <= m.nsplit; sp++) v += __ldcg(p + sp * plane);
+        if (m.act == DZ_ACT_TANH) v = tanhf(v);
+        const int yr = m.perm != nullptr ? __ldg(m.perm + t) : t;
+        const int64_t yo = static_cast<int64_t>(yr) * m.ldy + r;
+        if (m.y_dtype == DZ_F32)
+          reinterpret_cast<float*>(m.Y)[yo] = v;
+        else
+          reinterpret_cast<__nv_bfloat16*>(m.Y)[yo] = __float2bfloat16_rn(v);
+      }
+    }
+  }
+}
+
+// Consumer warp `warp` finished its plane stores of merged item #k: warp 0 fills the record, every
+// warp arrives (its lanes' stores, ordered by the warp barrier, precede the arrive's release).
+__device__ __forceinline__ void publish_item(MergeRec* recs, uint64_t* mfull, uint64_t* mempty, int k, int warp,
+                                             int lane, int rt, int is_base, int ntok, int rtok) {
+  const int slot = k % MREC;
+  mbar_wait(&mempty[slot], ((k / MREC) & 1) ^ 1);
+  if (warp == 0) {
+    if (lane == 0) {
+      recs[slot].rt = rt;
+      recs[slot].is_base = is_base;
+      recs[slot].ntok = ntok;
+    }
+    if (lane < ntok) recs[slot].tok[lane] = rtok;
+  }
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&mfull[slot]);
+}
+
+// Work items of a launch (debug bit 1: base items only, a probe of the base stream).
+__device__ __forceinline__ int job_items(const dz_sbmm_args& a, int n_jobs, int n_base, int nrt, int nbt, int nsplit,
+                                         int dsplit) {
+  return n_jobs < n_base ? 0 : nbt * nsplit * n_base + ((a.debug & 2) ? 0 : nrt * (n_jobs - n_base) * dsplit);
+}
+
 // ------------------------------------------------------------------------------------------
 // The persistent kernel
 // ------------------------------------------------------------------------------------------
@@ -633,14 +758,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int n_base = a.base != nullptr ? ceil_div(a.T - a.t_pf, BASE_N) : 0;  // dz_plan: base jobs first
   const int nsplit = a.base_splits;  // resolved by the host (launch_decode)
   const int dsplit = a.delta_splits;  // resolved by the host (launch_decode)
-  // debug bit 1: base items only (probe of the base stream)
-  const int n_jobs = a.n_jobs_dev != nullptr ? *a.n_jobs_dev : a.n_jobs;  // dz_plan_device writes the count
-  const int n_items =
-      n_jobs < n_base ? 0 : nbt * nsplit * n_base + ((a.debug & 2) ? 0 : nrt * (n_jobs - n_base) * dsplit);
 
   int* sched = reinterpret_cast<int*>(a.workspace);  // [0] item counter, [1] finished CTAs
   MergeCtx mctx;
-  mctx.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(a.workspace) + 256);
+  mctx.slice_cnt = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(a.workspace) + DZ_WS_CNT_OFF);
+  mctx.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(a.workspace) + DZ_WS_PART_OFF);
+  mctx.fused = a.base != nullptr && !a.keep_planes && dsplit == 1 && !(a.debug & 6);
+  mctx.base_target = n_base * nsplit;  // base items publishing each slice
+  mctx.readers = 0;  // set after the PDL wait (the job count may come from dz_plan_device)
   mctx.T = a.T;
   mctx.nsplit = nsplit;
   mctx.perm = a.perm;
@@ -661,6 +786,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int b = 0; b < 2; b++) {
       mbar_init(&sm->tmem_full[b], 1);
       mbar_init(&sm->tmem_empty[b], NW);
+    }
+    for (int r = 0; r < MREC; r++) {
+      mbar_init(&sm->mfull[r], NW);
+      mbar_init(&sm->mempty[r], 1);
     }
     fence_mbar_init();
   }
@@ -685,11 +814,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // First item static (blockIdx.x), later ones from the counter. Before waiting for the preceding
     // kernel (programmatic dependent launch), prefetch the first chunks of this item's weight
     // stream into L2: it depends only on resident weights, not on the predecessor's output.
+    // A device plan (n_jobs_dev) is the predecessor's output: nothing of it is read before the wait.
     int item = blockIdx.x;
     int rt = 0, jj = 0, sp = 0;
-    if (item < n_items) item_coords(item, nrt, nbt, nsplit, dsplit, n_jobs, n_base, rt, jj, sp);
-    dz_job job = item < n_items ? a.jobs[jj] : dz_job{0, 0, 0, 0};
-    if (item < n_items && lane == 0) {
+    int n_jobs = a.n_jobs;
+    int n_items = job_items(a, n_jobs, n_base, nrt, nbt, nsplit, dsplit);
+    dz_job job = dz_job{0, 0, 0, 0};
+    if (a.n_jobs_dev == nullptr && item < n_items) {
+      item_coords(item, nrt, nbt, nsplit, dsplit, n_jobs, n_base, rt, jj, sp);
+      job = a.jobs[jj];
+    }
+    if (a.n_jobs_dev == nullptr && item < n_items && lane == 0) {
       const bool dn = kind_dense(job.kind);
       const dz_native_delta* e0 = job.kind == 0 ? a.base : a.table + job.slot;
       const void* m0 = e0->tmap;
@@ -707,6 +842,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     griddep_wait();
     griddep_launch_dependents();
+    if (a.n_jobs_dev != nullptr) {  // dz_plan_device wrote the count and the jobs
+      n_jobs = *a.n_jobs_dev;
+      n_items = job_items(a, n_jobs, n_base, nrt, nbt, nsplit, dsplit);
+      if (item < n_items) {
+        item_coords(item, nrt, nbt, nsplit, dsplit, n_jobs, n_base, rt, jj, sp);
+        job = a.jobs[jj];
+      }
+    }
     int tok = 0, tok2 = 0;
     if (item < n_items) {
       if (lane < job.tok_count) tok = job.kind == 0 ? job.tok_begin + lane : a.order[job.tok_begin + lane];
@@ -891,6 +1034,43 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
     }
+  } else if (warp == WARP_COMB) {
+    // ===================== combiner (fused merge) =====================
+    griddep_wait();
+    if (mctx.fused) {
+      mctx.readers = (a.n_jobs_dev != nullptr ? *a.n_jobs_dev : a.n_jobs) - n_base;  // delta jobs
+      const MergeRec* recs = reinterpret_cast<const MergeRec*>(sm->recs);
+      const int n_slices = ceil_div(a.out, 32);
+      for (int k = 0;; k++) {
+        const int slot = k % MREC;
+        while (!mbar_test(&sm->mfull[slot], (k / MREC) & 1)) __nanosleep(32);
+        const int rt = recs[slot].rt, is_base = recs[slot].is_base, ntok = recs[slot].ntok;
+        const int mytok = lane < ntok ? recs[slot].tok[lane] : 0;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm->mempty[slot]);
+        if (rt < 0) break;
+        fence_acq_rel_gpu();  // the consumers' plane stores (CTA-synchronized) -> GPU scope
+        if (is_base) {
+          const int slice = rt * (BASE_RT / 32) + lane;
+          if (lane < BASE_RT / 32 && slice < n_slices) red_add_s32(mctx.slice_cnt + slice, 1);
+          continue;
+        }
+        const int slice = rt * (RT / 32) + lane;
+        const bool mine = lane < RT / 32 && slice < n_slices;
+        if (mine)
+          while ((ld_relaxed_s32(mctx.slice_cnt + slice) & 0xFFFF) < mctx.base_target) __nanosleep(64);
+        __syncwarp();
+        fence_acq_rel_gpu();  // acquire: the base planes of these slices
+        if (lane < ntok) sm->comb_tok[lane] = mytok;
+        __syncwarp();
+        combine_tokens(mctx, rt * RT, ntok, sm->comb_tok, lane);
+        __syncwarp();
+        if (mine) {
+          const int old = atomicAdd(mctx.slice_cnt + slice, 1 << 16);
+          if ((old >> 16) == mctx.readers - 1) mctx.slice_cnt[slice] = 0;  // last reader re-arms
+        }
+      }
+    }
   } else {
     // ===================== consumers =====================
     griddep_wait();  // Y / merge slots may still be in use by the preceding kernel
@@ -900,11 +1080,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     int nbase = 0;
+    int nmerge = 0;  // items merged so far (record ring position)
+    MergeRec* recs = reinterpret_cast<MergeRec*>(sm->recs);
     while (true) {
       mbar_wait(&sm->full[stage], phase);
       const StageHdr h = sm->hdr[stage];
       if (lane == 0 && warp == 0) TRACE(3, h.item, stage);
-      if (h.item < 0) break;
+      if (h.item < 0) {
+        if (mctx.fused) publish_item(recs, sm->mfull, sm->mempty, nmerge, warp, lane, -1, 0, 0, 0);
+        break;
+      }
       const bool is_base = h.kind == 0;
       const int rg0 = h.rt * RG + warp * MR;
       const int nrv = (n16 - rg0) < MR ? (n16 - rg0) : MR;  // row groups of this warp inside `out`
@@ -942,6 +1127,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       if ((h.flags & 2) && h.kind == DZ_KIND_DENSE && nrv > 0)  // rare path: needs the stage's token list
         merge_fragments(acc, nt, mctx, nsplit + h.pad, rg0, h.tok_count, sm->tok_ids[stage], lane);
+      const int rtok = ((h.flags & 2) && !is_base && lane < h.tok_count && lane < 32) ? sm->tok_ids[stage][lane] : 0;
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm->empty[stage]);  // the stage is free before the epilogue
       if (lane == 0 && warp == 0) TRACE(4, h.item, stage);
@@ -978,6 +1164,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
           merge_batch<4 * MR>(mctx, nsplit + h.pad, tk, rw, x, ok);
         }
+        if (mctx.fused) {  // hand the item to the combiner warp (no wait on any round trip)
+          publish_item(recs, sm->mfull, sm->mempty, nmerge, warp, lane, h.rt, is_base ? 1 : 0, is_base ? 0 : h.tok_count,
+                       rtok);
+          nmerge++;
+        }
         if (lane == 0 && warp == 0) TRACE(5, h.item, 0);
         if (lane == 0 && warp == 0) ITEM_TRACE(1, h.item, globaltimer());
       }
@@ -989,20 +1180,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, TMEM_COLS);
   }
-  if (a.fin_inline && a.base != nullptr && !(a.debug & 4)) {
-    // every partial plane of every CTA written -> finalize here (no separate launch)
-    unsigned* sync = reinterpret_cast<unsigned*>(a.workspace) + 2;
-    grid_sync(sync, sync + 1);
-    finalize_rows(mctx.part, nsplit + dsplit - 1, a.t_pf, a.T, a.out, a.perm, a.Y, a.ldy, a.y_dtype, a.act,
-                  blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x,
-                  static_cast<int64_t>(gridDim.x) * blockDim.x);
-  }
 }
 
-// Finalize the merged decode rows [t0, T): Y[perm[t]][r] = act(((P_0 + P_1) + ... + P_{S-1}) + P_S)
-// with P_s the base K-split partials and P_S the delta partial — a fixed summation order, so the
-// result is deterministic and independent of the batch. Runs after k_sbmm in the same stream
-// (programmatic dependent launch).
 }  // namespace dz
 
 using namespace dz;
@@ -1011,7 +1190,8 @@ static_assert(A_DN + BASE_CH * KC_DN * BASE_N * 2 <= STAGE_BYTES && BASE_CH * BA
               "base stage layout");
 static_assert(NB_SP % PAIR == 0, "sparse stages hold whole block pairs");
 static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
-static_assert((NW == 8 || NW == 16) && MR * NW == 16, "consumer warps: 8 (2 row groups each) or 16 (1 each)");
+static_assert(sizeof(MergeRec) == 36 * sizeof(int) && MREC == 4, "MergeRec ring layout in Smem");
+static_assert(NW == 8 && MR == 2, "8 consumer warps of 32 rows (one 32-row output slice each)");
 static_assert(sizeof(dz_native_delta) == 192, "dz_native_delta must be 192 bytes");
 static_assert(offsetof(dz_native_delta, tmap) == 64, "tensor map must be 64-byte aligned in the entry");
 static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
@@ -1063,11 +1243,9 @@ extern "C" int dz_base_init(dz_native_delta* e, const uint16_t* W, int64_t ldw, 
 }
 
 extern "C" size_t dz_sbmm_workspace_bytes(int32_t T, int32_t out) {
-  if (T < 0 || out < 1) return 0;
-  return 256 + static_cast<size_t>(T) * out * sizeof(float) * 6;  // <= 4 base + 2 delta K-split planes
+  if (T < 0 || out < 1 || out > 32 * MAX_SLICES) return 0;
+  return DZ_WS_PART_OFF + static_cast<size_t>(T) * out * sizeof(float) * 6;  // <= 4 base + 2 delta K-split planes
 }
-
-static int g_ctas_per_sm = 0;
 
 extern "C" int dz_sbmm_diag(int* v) {  // numRegs, static smem, dynamic smem, max threads, localBytes
   cudaFuncAttributes fa;
@@ -1095,32 +1273,17 @@ extern "C" int dz_sbmm_ctas_per_sm(void) {
 extern "C" int dz_tp_finalize_launch(const float* part, int nsplit, int T, int out, const dz_tp_ctx* ctx, void* Y,
                                      int64_t ldy, int y_dtype, int act, void* stream);
 
-static int sms_count() {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return sms;
-}
-
+// Host side of one K2 launch. The K-split counts come from the caller or from the shape alone
+// (never from the batch, so a token's result does not depend on the other tokens of the call).
 static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
   dz_sbmm_args kargs = *a_in;
   const dz_sbmm_args* a = &kargs;
-  if (kargs.base_splits <= 0) {
-    kargs.base_splits = base_splits(kargs.out, kargs.in);
-    const char* e = std::getenv("DZ_BASE_SPLITS");  // experiment override (A/B)
-    if (e && e[0] >= '1' && e[0] <= '4') kargs.base_splits = e[0] - '0';
-  }
-  if (kargs.base_splits > 4) kargs.base_splits = 4;
-  if (kargs.delta_splits <= 0) {
-    kargs.delta_splits = delta_splits(kargs.out, kargs.in);
-    const char* e = std::getenv("DZ_DELTA_SPLITS");  // experiment override (A/B)
-    if (e && (e[0] == '1' || e[0] == '2')) kargs.delta_splits = e[0] - '0';
-  }
-  if (kargs.delta_splits > 2) kargs.delta_splits = 2;
-  if (kargs.base == nullptr) kargs.delta_splits = 1;  // single contributor: the delta writes Y directly
+  resolve_splits(kargs.out, kargs.in, kargs.base != nullptr, kargs.base_splits, kargs.delta_splits);
+  const bool tp = a->tp != nullptr && a->tp->world > 1;
+  kargs.keep_planes = tp ? 1 : 0;  // row-parallel shard: the peer-memory reduction reads the planes
+  // must match MergeCtx::fused in the kernel: delta items write Y themselves
+  const bool fused = a->base != nullptr && !tp && kargs.delta_splits == 1 && !(a->debug & 6);
+  // One-time, idempotent kernel attribute setup (the only process-wide state; no per-call state).
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   static int ctas_per_sm = 1;
@@ -1131,7 +1294,7 @@ static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
     if (ctas_per_sm < 1) ctas_per_sm = 1;
   });
   if (attr_err != cudaSuccess) return DZ_E_CUDA;
-  CUtensorMap xmap;  // X [T][in] bf16, 64-column x 64-token SWIZZLE_128B tiles (base UMMA B operand)
+  CUtensorMap xmap;  // X [T][in] bf16, 64-column x 128-token SWIZZLE_128B tiles (base UMMA B operand)
   int st = encode_2d(&xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a->X, static_cast<uint64_t>(a->in),
                      static_cast<uint64_t>(a->T), static_cast<uint64_t>(a->ldx) * 2, KC_DN, BASE_N,
                      CU_TENSOR_MAP_SWIZZLE_128B);
@@ -1146,34 +1309,26 @@ static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
   const int n_items = ceil_div(a->out, RT) * a->n_jobs * a->delta_splits +
                       ceil_div(a->out, BASE_RT) * a->base_splits * ceil_div(a->T, BASE_N);
   if (grid > n_items) grid = n_items;
-  // DZ_FIN_INLINE=1: finalize inside k_sbmm after a grid barrier (every CTA is resident: grid <=
-  // SMs x 1) instead of a separate k_finalize launch. Off by default: inside a CUDA graph the
-  // separate launch measured 0.7-1.7% faster (profiles/r01_ab_fin_inline.txt).
-  const char* fe = std::getenv("DZ_FIN_INLINE");
-  kargs.fin_inline = (a->tp == nullptr || a->tp->world <= 1) && (fe && fe[0] == '1') && grid <= sms_count() ? 1 : 0;
+  // Fused merge: the delta items write Y inside k_sbmm, no second launch.
   st = launch_pdl(1, k_sbmm, grid, NTHREADS, SMEM_BYTES, stream, *a, xmap);
-  if (st || a->base == nullptr || (a->debug & 4) || kargs.fin_inline) return st;
-  // merged rows -> Y (+ activation), accumulator re-zeroed
-  const int t0 = a->t_pf;
-  const int64_t work = static_cast<int64_t>(a->T - t0) * a->out / 4;
-  int fgrid = static_cast<int>((work + 255) / 256);
-  if (fgrid > 4 * 148) fgrid = 4 * 148;
-  if (fgrid < 1) fgrid = 1;
-  const float* part = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(a->workspace) + 256);
-  if (a->tp != nullptr && a->tp->world > 1)  // row-parallel shard: fused reduction over peer memory
+  if (st || fused || a->base == nullptr || (a->debug & 4)) return st;
+  const float* part = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(a->workspace) + DZ_WS_PART_OFF);
+  if (tp)  // row-parallel shard: fused reduction over peer memory
     return dz_tp_finalize_launch(part, a->base_splits + a->delta_splits - 1, a->T, a->out, a->tp, a->Y, a->ldy,
-                                 a->y_dtype, a->act,
-                                 stream);
-  return launch_pdl(2, k_finalize, fgrid, 256, 0, stream, part, a->base_splits + a->delta_splits - 1, t0, a->T,
-                    a->out, a->perm,
-                    a->Y, a->ldy, a->y_dtype, a->act);
+                                 a->y_dtype, a->act, stream);
+  // delta K-splits (an explicit knob): every partial in planes, summed by k_finalize in a fixed order
+  const int64_t work = static_cast<int64_t>(a->T - a->t_pf) * a->out / 4;
+  int fgrid = static_cast<int>((work + 255) / 256);
+  fgrid = fgrid > 4 * 148 ? 4 * 148 : fgrid < 1 ? 1 : fgrid;
+  return launch_pdl(2, k_finalize, fgrid, 256, 0, stream, part, a->base_splits + a->delta_splits - 1, a->t_pf, a->T,
+                    a->out, a->perm, a->Y, a->ldy, a->y_dtype, a->act);
 }
 
 extern "C" int dz_sbmm(const dz_sbmm_args* a, void* stream) {
   if (!a || !a->X || !a->Y || !a->workspace) return DZ_E_VALUE;
   if (a->tp != nullptr && a->tp->world > 1 && (a->perm != nullptr || a->base == nullptr))
     return DZ_E_UNSUPPORTED;  // the fused reduction takes decode plans with a base
-  if (a->T < 0 || a->out < 1 || a->in < 1) return DZ_E_SHAPE;
+  if (a->T < 0 || a->out < 1 || a->in < 1 || a->out > 32 * MAX_SLICES) return DZ_E_SHAPE;
   if (a->T == 0 || a->n_jobs == 0) return DZ_OK;
   const int in_pad = ceil_div(a->in, kBlkCols) * kBlkCols;
   if (a->ldx < in_pad || (a->ldx % 8) != 0 || (reinterpret_cast<uintptr_t>(a->X) & 15) != 0) return DZ_E_SHAPE;

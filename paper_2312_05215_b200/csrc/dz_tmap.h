@@ -44,16 +44,12 @@ inline int encode_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, u
 // Optional programmatic dependent launch (the kernel starts while its predecessor in the stream
 // drains; every kernel calls griddepcontrol.wait before touching the predecessor's output, so
 // both modes are correct). Off by default: on the 7B decode step it measured 0.4-0.8% slower
-// (two A/B pairs, profiles/r01_ab_pdl.txt). DZ_PDL=1 in the environment enables it.
-// DZ_PDL is a bit mask: 1 = the SBMM kernels (K2, K3), 2 = k_finalize.
-inline int pdl_mask() {
-  static int m = -1;
-  if (m < 0) {
-    const char* e = std::getenv("DZ_PDL");
-    m = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 0;
-  }
-  return m;
-}
+// (two A/B pairs, profiles/r01_ab_pdl.txt). A compile-time bit mask (build a variant with
+// -DDZ_PDL=3): bit 0 = the SBMM kernels (K2, K3), bit 1 = k_finalize.
+#ifndef DZ_PDL
+#define DZ_PDL 0
+#endif
+constexpr int pdl_mask() { return DZ_PDL; }
 
 template <typename Kern, typename... Args>
 inline int launch_pdl(int kind_bit, Kern kernel, int grid, int threads, int smem, void* stream, Args... args) {

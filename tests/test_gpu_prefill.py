@@ -180,10 +180,8 @@ def test_prefill_item_height_does_not_change_results(E, rows, cols, bits, monkey
     Xd = torch.from_numpy(X.astype(np.float32)).cuda().to(torch.bfloat16)
     plan = E.Plan(ids, table.kinds, 3, pf_min=64)
     ys = []
-    monkeypatch.setenv("DZ_PF_SPARSE", "0")  # both heights on the dense-dequantised delta product
-    for mt in ("1", "2"):
-        monkeypatch.setenv("DZ_PF_MT", mt)
-        ys.append(E.sbmm_forward(Xd, plan, base, table, y_dtype=torch.float32))
+    for mt in (1, 2):  # both heights on the dense-dequantised delta product
+        ys.append(E.sbmm_forward(Xd, plan, base, table, y_dtype=torch.float32, prefill_variant=mt))
     assert torch.equal(ys[0], ys[1])
     R = O.sbmm_matrix(W, dict(enumerate(ods)), ids, X)
     assert rel_err_rows(ys[1].cpu().double().numpy(), R).max() <= REL_TOL
@@ -200,9 +198,9 @@ def test_prefill_sparse_tcgen05_vs_dense(E, rows, cols, bits, monkeypatch):
     Xd = torch.from_numpy(X.astype(np.float32)).cuda().to(torch.bfloat16)
     plan = E.Plan(ids, table.kinds, 3, pf_min=64)
     ys = {}
-    for sp in ("1", "0"):
-        monkeypatch.setenv("DZ_PF_SPARSE", sp)
-        ys[sp] = E.sbmm_forward(Xd, plan, base, table, y_dtype=torch.float32).cpu().double().numpy()
+    for sp, variant in (("1", 0), ("0", 1)):
+        ys[sp] = E.sbmm_forward(Xd, plan, base, table, y_dtype=torch.float32,
+                                prefill_variant=variant).cpu().double().numpy()
     R = O.sbmm_matrix(W, dict(enumerate(ods)), ids, X)
     assert rel_err_rows(ys["1"], R).max() <= REL_TOL
     assert rel_err_rows(ys["1"], ys["0"]).max() <= 1e-4  # same bf16 ΔW values, fp32 sums in another order
