@@ -129,6 +129,10 @@ typedef struct dz_sbmm_args {
                                for the TP peer reduction instead of writing Y in the kernel */
   int32_t prefill_variant;  /* K3 delta product: 0 = 2:4-sparse tcgen05 (default); 1 / 2 =
                                dense-dequantised with 128- / 256-row items (A/B and tests) */
+  int32_t fused_merge;      /* 1: Y written inside k_sbmm by a combiner warp per CTA (one launch per
+                               linear, no k_finalize); 0 (default): k_finalize sums the partial
+                               planes (measured faster, profiles/r02_ab_fused_merge.txt) */
+  int32_t _pad5;
   const struct dz_sbmm_args* next; /* device copy of the NEXT linear's args in the step, or NULL:
                                CTAs that run out of items warm L2 with the first weight stages
                                their blockIdx gets in that launch (decode plans only)      */
@@ -237,10 +241,10 @@ int dz_plan_device(const int32_t* slots_dev, int32_t T, const int32_t* kinds_dev
  * TMA stages W tiles (tcgen05.mma into TMEM), native delta blocks and X through
  * shared memory, warps decode codes in registers and issue mma.sp (2:4) / mma (dense)
  * with fp32 accumulation, per-(row,128-col) scales are applied per block. The base and
- * delta partials of each 32-row output slice are summed, in a fixed order, by the warp
- * that completes the slice (an arrival counter per slice), which also applies the
- * activation and writes Y: no separate add kernel, no grid barrier. Deterministic and
- * batch-invariant: a token's result does not depend on the other tokens in the call. */
+ * delta partials go to fp32 planes (one writer per element) and are summed in a fixed
+ * order with the activation applied: by a short k_finalize launch (default), or inside
+ * k_sbmm by a combiner warp (args.fused_merge = 1). Deterministic and batch-invariant:
+ * a token's result does not depend on the other tokens in the call. */
 size_t dz_sbmm_workspace_bytes(int32_t T, int32_t out);
 /* K3 — prefill SBMM (dz_prefill.cu), launched by dz_sbmm for the prefill jobs of a mixed plan:
  * per (128-row tile, <= 256-token group) one TMEM accumulator receives tcgen05 MMAs of the base

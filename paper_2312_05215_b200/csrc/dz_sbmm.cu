@@ -23,14 +23,15 @@
 //    (the reference's index nibble IS the sparse-MMA metadata), fp32 accumulation; dense-delta
 //    stages use mma m16n8k16. They also drain the base accumulator from TMEM (tcgen05.ld).
 //
-// Merge (no separate add kernel): the base items come first in the item order and store their fp32
-// partial per K-split into workspace planes, then publish each 32-row slice on its counter. The delta
-// item of a token (every token has exactly one) waits for its slice's base publications — in
-// practice already there: base items are short (K-split) and claimed first — and writes
-// y = act(((P_0 + P_1) + ...) + delta) straight from its registers. Deterministic and
-// batch-invariant: the summation order is fixed per element and the split count depends on the
-// shape only. TP row-parallel shards and delta K-splits keep every partial in planes for a
-// separate reduction (k_tp_finalize / k_finalize).
+// Merge: every contributor of y[t][r] — the base job's K-split s, the token's delta job — stores its
+// fp32 partial with a plain store into its own plane of the workspace (exactly one writer per
+// element, no atomics on data). Two ways to finish (dz_sbmm_args.fused_merge):
+//  * default: k_finalize (one short launch) sums the planes in a fixed order and writes Y;
+//  * fused (k_sbmm<true>): a 12th "combiner" warp per CTA writes Y for each delta item's tokens
+//    once the base partials of its rows are published (per-32-row-slice counters), so no second
+//    launch. Measured ~1% slower on the 7B step and 5-10% slower at cfg5 points than the
+//    k_finalize path on the same box (profiles/r02_ab_fused_merge.txt), hence opt-in.
+// Both are deterministic and batch-invariant: the summation order is fixed per element.
 //
 // Mixed batches: groups large enough for the tensor-core prefill kernel (K3, dz_prefill.cu) are
 // staged first in a permuted copy of X; this kernel then covers the remaining (decode) rows and
@@ -71,8 +72,10 @@ constexpr int MR = 16 / NW;               // 16-row groups per consumer warp (RG
 constexpr int WARP_PROD = NW;             // TMA producer warp
 constexpr int WARP_MMA = NW + 1;          // tcgen05 issuer / TMEM owner warp
 constexpr int WARP_XPROD = NW + 2;        // per-token X copies of delta stages
-constexpr int WARP_COMB = NW + 3;         // fused merge: combines each delta item's tokens into Y
-constexpr int NTHREADS = (NW + 4) * 32;
+constexpr int WARP_COMB = NW + 3;         // fused-merge instantiation only: combines delta items into Y
+constexpr int NTHREADS = (NW + 3) * 32;   // k_sbmm<false>; k_sbmm<true> has one more warp
+template <bool FUSED>
+constexpr int nthreads() { return FUSED ? NTHREADS + 32 : NTHREADS; }
 constexpr int RG = NW * MR;               // row groups per item
 constexpr int RT = RG * kBlkRows;         // rows per item (256) == 2 x UMMA M
 constexpr int UMMA_M = 128;
@@ -574,7 +577,7 @@ __device__ __forceinline__ void finalize_rows(const float* __restrict__ part, in
 // Finalize the merged decode rows [t0, T): Y[perm[t]][r] = act(((P_0 + P_1) + ... + P_{S-1}) + P_S)
 // with P_s the base K-split partials and the delta partials after them — a fixed summation order,
 // so the result is deterministic and independent of the batch. Only for launches that keep every
-// partial in planes (delta K-splits); the default decode launch merges inside k_sbmm.
+// partial in planes: the default decode launch (k_sbmm<false>), delta K-splits, probes.
 __global__ void __launch_bounds__(256) k_finalize(const float* __restrict__ part, int nsplit, int t0, int T, int out,
                                                   const int32_t* __restrict__ perm, void* __restrict__ Y, int64_t ldy,
                                                   int y_dtype, int act) {
@@ -651,48 +654,66 @@ __device__ __forceinline__ void red_add_s32(int* p, int v) {
 }
 
 // Y rows [r0, r0 + 256) of the `ntok` tokens `tok[]`: planes 0..nsplit (base splits, then the delta)
-// summed in that order. Lanes own row quads; all plane loads of a token are issued before use.
+// summed in that order. Lanes own row quads (two per lane); the loads of a group of CT tokens are all
+// in flight before any add, so a group costs about one L2 round trip per plane pass.
+constexpr int CT = 4;
+__device__ __forceinline__ void store_y4(const MergeCtx& m, int t, int r, float4 y) {
+  if (m.act == DZ_ACT_TANH) { y.x = tanhf(y.x); y.y = tanhf(y.y); y.z = tanhf(y.z); y.w = tanhf(y.w); }
+  const int yr = m.perm != nullptr ? __ldg(m.perm + t) : t;
+  const int64_t yo = static_cast<int64_t>(yr) * m.ldy + r;
+  if (m.y_dtype == DZ_F32) {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(m.Y) + yo) = y;
+  } else {
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(y.x, y.y), hi = __floats2bfloat162_rn(y.z, y.w);
+    uint2 w;
+    w.x = *reinterpret_cast<const uint32_t*>(&lo);
+    w.y = *reinterpret_cast<const uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(m.Y) + yo) = w;
+  }
+}
+
 __device__ __noinline__ void combine_tokens(const MergeCtx m, int r0, int ntok, const int* tok, int lane) {
   const int64_t plane = static_cast<int64_t>(m.T) * m.out;
   const bool vec = (m.out % 4) == 0 && (m.ldy % 4) == 0 && (reinterpret_cast<uintptr_t>(m.Y) & 15) == 0;
   if (vec) {
+    const int ra = r0 + 4 * lane, rb = ra + 128;
+    const bool oka = ra < m.out, okb = rb < m.out;
 #pragma unroll 1
-    for (int i = 0; i < ntok; i++) {
-      const int t = tok[i];
-      float4 v[2];
-      bool ok[2];
+    for (int i0 = 0; i0 < ntok; i0 += CT) {
+      float4 va[CT], vb[CT], da[CT], db[CT];
+      int t[CT];
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int r = r0 + 4 * (lane + 32 * h);
-        ok[h] = r < m.out;
-        if (ok[h]) v[h] = __ldcg(reinterpret_cast<const float4*>(m.part + static_cast<int64_t>(t) * m.out + r));
+      for (int c = 0; c < CT; c++) {
+        t[c] = i0 + c < ntok ? tok[i0 + c] : -1;
+        const float* p = m.part + static_cast<int64_t>(t[c] < 0 ? 0 : t[c]) * m.out;
+        if (t[c] >= 0 && oka) {
+          va[c] = __ldcg(reinterpret_cast<const float4*>(p + ra));
+          da[c] = __ldcg(reinterpret_cast<const float4*>(p + m.nsplit * plane + ra));
+        }
+        if (t[c] >= 0 && okb) {
+          vb[c] = __ldcg(reinterpret_cast<const float4*>(p + rb));
+          db[c] = __ldcg(reinterpret_cast<const float4*>(p + m.nsplit * plane + rb));
+        }
       }
-      for (int sp = 1; sp <= m.nsplit; sp++) {
+      for (int sp = 1; sp < m.nsplit; sp++) {  // further base K-splits, in order
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const int r = r0 + 4 * (lane + 32 * h);
-          if (ok[h]) {
-            const float4 w = __ldcg(reinterpret_cast<const float4*>(m.part + sp * plane + static_cast<int64_t>(t) * m.out + r));
-            v[h].x += w.x; v[h].y += w.y; v[h].z += w.z; v[h].w += w.w;
+        for (int c = 0; c < CT; c++) {
+          const float* p = m.part + sp * plane + static_cast<int64_t>(t[c] < 0 ? 0 : t[c]) * m.out;
+          if (t[c] >= 0 && oka) {
+            const float4 w = __ldcg(reinterpret_cast<const float4*>(p + ra));
+            va[c].x += w.x; va[c].y += w.y; va[c].z += w.z; va[c].w += w.w;
+          }
+          if (t[c] >= 0 && okb) {
+            const float4 w = __ldcg(reinterpret_cast<const float4*>(p + rb));
+            vb[c].x += w.x; vb[c].y += w.y; vb[c].z += w.z; vb[c].w += w.w;
           }
         }
       }
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
-        if (!ok[h]) continue;
-        float4 y = v[h];
-        if (m.act == DZ_ACT_TANH) { y.x = tanhf(y.x); y.y = tanhf(y.y); y.z = tanhf(y.z); y.w = tanhf(y.w); }
-        const int yr = m.perm != nullptr ? __ldg(m.perm + t) : t;
-        const int64_t yo = static_cast<int64_t>(yr) * m.ldy + r0 + 4 * (lane + 32 * h);
-        if (m.y_dtype == DZ_F32) {
-          *reinterpret_cast<float4*>(reinterpret_cast<float*>(m.Y) + yo) = y;
-        } else {
-          const __nv_bfloat162 lo = __floats2bfloat162_rn(y.x, y.y), hi = __floats2bfloat162_rn(y.z, y.w);
-          uint2 w;
-          w.x = *reinterpret_cast<const uint32_t*>(&lo);
-          w.y = *reinterpret_cast<const uint32_t*>(&hi);
-          *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(m.Y) + yo) = w;
-        }
+      for (int c = 0; c < CT; c++) {
+        if (t[c] < 0) continue;
+        if (oka) store_y4(m, t[c], ra, make_float4(va[c].x + da[c].x, va[c].y + da[c].y, va[c].z + da[c].z, va[c].w + da[c].w));
+        if (okb) store_y4(m, t[c], rb, make_float4(vb[c].x + db[c].x, vb[c].y + db[c].y, vb[c].z + db[c].z, vb[c].w + db[c].w));
       }
     }
   } else {
@@ -733,6 +754,38 @@ __device__ __forceinline__ void publish_item(MergeRec* recs, uint64_t* mfull, ui
   if (lane == 0) mbar_arrive(&mfull[slot]);
 }
 
+// The combiner's work for merged item #k (its record is complete): returns false at end of work.
+__device__ __forceinline__ bool service_record(Smem* sm, const MergeCtx& mctx, int k, int lane) {
+  const MergeRec* recs = reinterpret_cast<const MergeRec*>(sm->recs);
+  const int slot = k % MREC;
+  const int n_slices = ceil_div(mctx.out, 32);
+  const int rt = recs[slot].rt, is_base = recs[slot].is_base, ntok = recs[slot].ntok;
+  const int mytok = lane < ntok ? recs[slot].tok[lane] : 0;
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&sm->mempty[slot]);
+  if (rt < 0) return false;
+  if (is_base) {
+    fence_acq_rel_gpu();  // release: the consumers' plane stores (CTA-synchronized) -> GPU scope
+    const int slice = rt * (BASE_RT / 32) + lane;
+    if (lane < BASE_RT / 32 && slice < n_slices) red_add_s32(mctx.slice_cnt + slice, 1);
+    return true;
+  }
+  const int slice = rt * (RT / 32) + lane;
+  const bool mine = lane < RT / 32 && slice < n_slices;
+  if (mine)
+    while ((ld_relaxed_s32(mctx.slice_cnt + slice) & 0xFFFF) < mctx.base_target) __nanosleep(32);
+  __syncwarp();
+  fence_acq_rel_gpu();  // acquire: the base planes of these slices (and this CTA's delta plane)
+  // count this reader now (every reader has passed its wait once the count completes); the result
+  // is only needed after the combine, so its round trip overlaps the plane loads
+  const int old = mine ? atomicAdd(mctx.slice_cnt + slice, 1 << 16) : 0;
+  if (lane < ntok) sm->comb_tok[lane] = mytok;
+  __syncwarp();
+  combine_tokens(mctx, rt * RT, ntok, sm->comb_tok, lane);
+  if (mine && (old >> 16) == mctx.readers - 1) mctx.slice_cnt[slice] = 0;  // last reader re-arms
+  return true;
+}
+
 // Work items of a launch (debug bit 1: base items only, a probe of the base stream).
 __device__ __forceinline__ int job_items(const dz_sbmm_args& a, int n_jobs, int n_base, int nrt, int nbt, int nsplit,
                                          int dsplit) {
@@ -742,7 +795,8 @@ __device__ __forceinline__ int job_items(const dz_sbmm_args& a, int n_jobs, int 
 // ------------------------------------------------------------------------------------------
 // The persistent kernel
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NTHREADS, 1)
+template <bool FUSED>
+__global__ void __launch_bounds__(nthreads<FUSED>(), 1)
     k_sbmm(const __grid_constant__ dz_sbmm_args a, const __grid_constant__ CUtensorMap xmap) {
   extern __shared__ uint8_t smem_dyn[];
   // 1024-B alignment for the SWIZZLE_128B tiles
@@ -763,7 +817,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   MergeCtx mctx;
   mctx.slice_cnt = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(a.workspace) + DZ_WS_CNT_OFF);
   mctx.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(a.workspace) + DZ_WS_PART_OFF);
-  mctx.fused = a.base != nullptr && !a.keep_planes && dsplit == 1 && !(a.debug & 6);
+  mctx.fused = FUSED && a.base != nullptr && !a.keep_planes && dsplit == 1 && !(a.debug & 6);
   mctx.base_target = n_base * nsplit;  // base items publishing each slice
   mctx.readers = 0;  // set after the PDL wait (the job count may come from dz_plan_device)
   mctx.T = a.T;
@@ -1034,41 +1088,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
     }
-  } else if (warp == WARP_COMB) {
+  } else if (FUSED && warp == WARP_COMB) {
     // ===================== combiner (fused merge) =====================
     griddep_wait();
     if (mctx.fused) {
       mctx.readers = (a.n_jobs_dev != nullptr ? *a.n_jobs_dev : a.n_jobs) - n_base;  // delta jobs
-      const MergeRec* recs = reinterpret_cast<const MergeRec*>(sm->recs);
-      const int n_slices = ceil_div(a.out, 32);
       for (int k = 0;; k++) {
-        const int slot = k % MREC;
-        while (!mbar_test(&sm->mfull[slot], (k / MREC) & 1)) __nanosleep(32);
-        const int rt = recs[slot].rt, is_base = recs[slot].is_base, ntok = recs[slot].ntok;
-        const int mytok = lane < ntok ? recs[slot].tok[lane] : 0;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm->mempty[slot]);
-        if (rt < 0) break;
-        fence_acq_rel_gpu();  // the consumers' plane stores (CTA-synchronized) -> GPU scope
-        if (is_base) {
-          const int slice = rt * (BASE_RT / 32) + lane;
-          if (lane < BASE_RT / 32 && slice < n_slices) red_add_s32(mctx.slice_cnt + slice, 1);
-          continue;
-        }
-        const int slice = rt * (RT / 32) + lane;
-        const bool mine = lane < RT / 32 && slice < n_slices;
-        if (mine)
-          while ((ld_relaxed_s32(mctx.slice_cnt + slice) & 0xFFFF) < mctx.base_target) __nanosleep(64);
-        __syncwarp();
-        fence_acq_rel_gpu();  // acquire: the base planes of these slices
-        if (lane < ntok) sm->comb_tok[lane] = mytok;
-        __syncwarp();
-        combine_tokens(mctx, rt * RT, ntok, sm->comb_tok, lane);
-        __syncwarp();
-        if (mine) {
-          const int old = atomicAdd(mctx.slice_cnt + slice, 1 << 16);
-          if ((old >> 16) == mctx.readers - 1) mctx.slice_cnt[slice] = 0;  // last reader re-arms
-        }
+        while (!mbar_test(&sm->mfull[k % MREC], (k / MREC) & 1)) __nanosleep(32);
+        if (!service_record(sm, mctx, k, lane)) break;
       }
     }
   } else {
@@ -1249,24 +1276,24 @@ extern "C" size_t dz_sbmm_workspace_bytes(int32_t T, int32_t out) {
 
 extern "C" int dz_sbmm_diag(int* v) {  // numRegs, static smem, dynamic smem, max threads, localBytes
   cudaFuncAttributes fa;
-  if (cudaFuncGetAttributes(&fa, k_sbmm) != cudaSuccess) return -1;
+  if (cudaFuncGetAttributes(&fa, k_sbmm<false>) != cudaSuccess) return -1;
   v[0] = fa.numRegs; v[1] = static_cast<int>(fa.sharedSizeBytes); v[2] = SMEM_BYTES;
   v[3] = fa.maxThreadsPerBlock; v[4] = static_cast<int>(fa.localSizeBytes);
   size_t avail = 0;
-  cudaFuncSetAttribute(k_sbmm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  cudaOccupancyAvailableDynamicSMemPerBlock(&avail, k_sbmm, 2, NTHREADS);
+  cudaFuncSetAttribute(k_sbmm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaOccupancyAvailableDynamicSMemPerBlock(&avail, k_sbmm<false>, 2, NTHREADS);
   v[5] = static_cast<int>(avail);
-  cudaFuncSetAttribute(k_sbmm, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(k_sbmm<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_sbmm, NTHREADS, SMEM_BYTES);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_sbmm<false>, NTHREADS, SMEM_BYTES);
   v[6] = n;
   return 0;
 }
 
 extern "C" int dz_sbmm_ctas_per_sm(void) {
   int n = 0;
-  if (cudaFuncSetAttribute(k_sbmm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess) return -1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_sbmm, NTHREADS, SMEM_BYTES) != cudaSuccess) return -1;
+  if (cudaFuncSetAttribute(k_sbmm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess) return -1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_sbmm<false>, NTHREADS, SMEM_BYTES) != cudaSuccess) return -1;
   return n;
 }
 
@@ -1281,16 +1308,18 @@ static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
   resolve_splits(kargs.out, kargs.in, kargs.base != nullptr, kargs.base_splits, kargs.delta_splits);
   const bool tp = a->tp != nullptr && a->tp->world > 1;
   kargs.keep_planes = tp ? 1 : 0;  // row-parallel shard: the peer-memory reduction reads the planes
-  // must match MergeCtx::fused in the kernel: delta items write Y themselves
-  const bool fused = a->base != nullptr && !tp && kargs.delta_splits == 1 && !(a->debug & 6);
+  // must match MergeCtx::fused in the kernel: the combiner warp writes Y (no k_finalize launch)
+  const bool fused = a->fused_merge != 0 && a->base != nullptr && !tp && kargs.delta_splits == 1 && !(a->debug & 6);
   // One-time, idempotent kernel attribute setup (the only process-wide state; no per-call state).
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   static int ctas_per_sm = 1;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(k_sbmm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    attr_err = cudaFuncSetAttribute(k_sbmm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (attr_err == cudaSuccess)
-      attr_err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, k_sbmm, NTHREADS, SMEM_BYTES);
+      attr_err = cudaFuncSetAttribute(k_sbmm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, k_sbmm<false>, NTHREADS, SMEM_BYTES);
     if (ctas_per_sm < 1) ctas_per_sm = 1;
   });
   if (attr_err != cudaSuccess) return DZ_E_CUDA;
@@ -1309,14 +1338,14 @@ static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
   const int n_items = ceil_div(a->out, RT) * a->n_jobs * a->delta_splits +
                       ceil_div(a->out, BASE_RT) * a->base_splits * ceil_div(a->T, BASE_N);
   if (grid > n_items) grid = n_items;
-  // Fused merge: the delta items write Y inside k_sbmm, no second launch.
-  st = launch_pdl(1, k_sbmm, grid, NTHREADS, SMEM_BYTES, stream, *a, xmap);
+  st = fused ? launch_pdl(1, k_sbmm<true>, grid, nthreads<true>(), SMEM_BYTES, stream, *a, xmap)
+              : launch_pdl(1, k_sbmm<false>, grid, NTHREADS, SMEM_BYTES, stream, *a, xmap);
   if (st || fused || a->base == nullptr || (a->debug & 4)) return st;
   const float* part = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(a->workspace) + DZ_WS_PART_OFF);
   if (tp)  // row-parallel shard: fused reduction over peer memory
     return dz_tp_finalize_launch(part, a->base_splits + a->delta_splits - 1, a->T, a->out, a->tp, a->Y, a->ldy,
                                  a->y_dtype, a->act, stream);
-  // delta K-splits (an explicit knob): every partial in planes, summed by k_finalize in a fixed order
+  // every partial in planes, summed by k_finalize in a fixed order (base splits, then delta splits)
   const int64_t work = static_cast<int64_t>(a->T - a->t_pf) * a->out / 4;
   int fgrid = static_cast<int>((work + 255) / 256);
   fgrid = fgrid > 4 * 148 ? 4 * 148 : fgrid < 1 ? 1 : fgrid;

@@ -270,16 +270,18 @@ def sbmm_forward(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: De
                  y_dtype: torch.dtype = torch.bfloat16, act: int = L.DZ_ACT_NONE, Y: torch.Tensor | None = None,
                  workspace: Workspace | None = None, grid: int = 0, debug: int = 0,
                  base_splits: int = 0, tp=None, delta_splits: int = 0, next_args: int = 0,
-                 prefill_variant: int = 0) -> torch.Tensor:
+                 prefill_variant: int = 0, fused_merge: bool = False) -> torch.Tensor:
     """Y[T, out] = X W_base^T + ΔW_{slot(t)} x_t for all t, one fused launch (inference.py:126-154).
 
     next_args: device address of the next linear's dz_sbmm_args (see `sbmm_args`), or 0; CTAs that
     run out of work then warm L2 with that launch's first weight stages.
     prefill_variant: K3's delta product for mixed plans (0 = 2:4-sparse tcgen05; 1 / 2 = the
-    dense-dequantised variant with 128- / 256-row items, for A/B runs and equivalence tests)."""
+    dense-dequantised variant with 128- / 256-row items, for A/B runs and equivalence tests).
+    fused_merge: write Y inside the SBMM kernel (combiner warp) instead of a k_finalize launch."""
     a, Y, keep = sbmm_args(X, plan, base, table, y_dtype, act, Y, workspace, grid, debug, base_splits, tp,
                            delta_splits)
     a.prefill_variant = prefill_variant
+    a.fused_merge = 1 if fused_merge else 0
     a.next = next_args or None
     L.check(L.lib().dz_sbmm(C.byref(a), stream_ptr()), "sbmm")
     return Y

@@ -100,3 +100,32 @@ def test_slice_counters_rearm_across_shapes(E):
         R = O.sbmm_matrix(W, dict(enumerate(ods)), ids, X.float().double().cpu().numpy())
         err = (np.linalg.norm(y0.double().cpu().numpy() - R, axis=1) / np.linalg.norm(R, axis=1)).max()
         assert err <= 1e-2
+
+
+@pytest.mark.parametrize("rows,cols,D,T,bits", [(4096, 512, 3, 24, 4), (1000, 256, 4, 70, 4), (33, 128, 2, 5, 2),
+                                                 (640, 384, 5, 200, 4)])
+def test_fused_merge_matches_finalize_launch(E, rows, cols, D, T, bits):
+    """fused_merge=1 (the combiner warp writes Y inside k_sbmm, no k_finalize launch) sums the same
+    planes in the same order as the default k_finalize path: bit-identical, for every base split
+    count, with tanh, bf16 output, a mixed prefill plan and the on-device plan."""
+    rng = np.random.default_rng(rows + T)
+    ods = [O.random_packed_delta(rng, rows, cols, bits) for _ in range(D)]
+    table = E.DeltaTable([E.NativeDelta.from_layer_delta(o) for o in ods], rows, cols)
+    base = E.NativeBase((torch.randn(rows, cols, device="cuda") / np.sqrt(cols)).to(torch.bfloat16))
+    ids = rng.integers(0, D, T).astype(np.int32)
+    X = torch.randn(T, cols, device="cuda").to(torch.bfloat16)
+    plans = [E.Plan(ids, table.kinds, D), E.DevicePlan(T, table.kinds, D).update(torch.from_numpy(ids).cuda())]
+    if T >= 128:
+        plans.append(E.Plan(ids, table.kinds, D, pf_min=32))
+        assert plans[-1].t_pf > 0
+    ws = E.Workspace()
+    for plan in plans:
+        for sp, act, yd in ((1, 0, torch.float32), (3, 1, torch.bfloat16), (2, 0, torch.bfloat16)):
+            y0 = E.sbmm_forward(X, plan, base, table, y_dtype=yd, act=act, base_splits=sp, workspace=ws)
+            for _ in range(2):
+                y1 = E.sbmm_forward(X, plan, base, table, y_dtype=yd, act=act, base_splits=sp, workspace=ws,
+                                    fused_merge=True)
+                assert torch.equal(y0, y1), (type(plan).__name__, sp, act)
+    buf = ws.get(1, 1, X.device)
+    torch.cuda.synchronize()
+    assert int(buf[256: 256 + 4 * 8192].count_nonzero()) == 0  # slice counters re-armed

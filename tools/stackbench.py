@@ -58,6 +58,7 @@ def main():
     ap.add_argument("--sweep", action="store_true", help="cfg5: D in 1..128 x batch in 1..256, Zipf ids")
     ap.add_argument("--base-splits", type=int, default=0, help="K-splits of the decode base GEMM (0 = by shape)")
     ap.add_argument("--max-batch", type=int, default=256, help="sweep: largest batch")
+    ap.add_argument("--points", default="", help="sweep subset: D:B,D:B,...")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -77,8 +78,10 @@ def main():
     if args.sweep:
         Ds = [d for d in (1, 2, 4, 8, 16, 32, 64, 128) if d <= args.deltas]
         Bs = tuple(b for b in (1, 2, 4, 8, 16, 32, 64, 128, 256) if b <= args.max_batch)
-        for D in Ds:
-            for B in Bs:
+        pts = [tuple(map(int, p.split(":"))) for p in args.points.split(",")] if args.points else \
+            [(D, B) for D in Ds for B in Bs]
+        for D, B in pts:
+            if True:
                 sid = zipf_ids(B, D, args.zipf or 1.5, args.seed + 1000 * D + B)
                 print(json.dumps(run(args, st, sid, dev, extra={"sweep_D": D, "batch": B,
                                                                 "base_splits": args.base_splits})), flush=True)
