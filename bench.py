@@ -239,7 +239,7 @@ def measured_peaks():
 def ncu_traffic():
     """Per-launch DRAM bytes (read + write) of the fused kernel from the committed ncu --set full
     capture (profiles/), or None."""
-    p = os.path.join(ROOT, "profiles", "r01_ncu_traffic_v17.json")
+    p = os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")
     if not os.path.exists(p):
         return None, None
     with open(p) as f:
@@ -470,12 +470,12 @@ def main():
                        if world > 1 else "single",
                        "l2": "inputs > L2 (97.5 GB streamed per step at N=1)", "cuda_graph": graph is not None,
                        "step_bytes_rank0": step_bytes},
-            "gpu_launches": len(order) * args.steps,  # one k_sbmm per fused linear (Y written in-kernel)
+            "gpu_launches": 2 * len(order) * args.steps,  # k_sbmm + k_finalize per fused linear
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_algorithmic": traffic_alg, "peak_kind": peak_kind,
                          "kernel": "k_sbmm (fused base GEMM + SBMM), all 4 x layers launches of one step (QKV, o, "
                                    "gate/up, down); achieved = algorithmic bytes / summed launch time; traffic = "
-                                   "mean DRAM bytes per launch (k_sbmm + k_finalize) from ncu --set full (profiles/r01_ncu_full_v17.md)",
+                                   "mean DRAM bytes per launch (k_sbmm + k_finalize) from ncu --set full (profiles/r02_ncu_full.md)",
                          "per_launch_us": {n: float(np.mean(v) * 1e3) for n, v in per_name.items()},
                          "step_GBps": step_bytes / (ms * 1e-3) / 1e9},
             "clocks": clocks,

@@ -236,6 +236,21 @@ int dz_plan_mixed(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t
 int dz_plan_device(const int32_t* slots_dev, int32_t T, const int32_t* kinds_dev, int32_t n_slots,
                    int32_t with_base, int32_t* order_dev, dz_job* jobs_dev, int32_t max_jobs,
                    int32_t* n_jobs_dev, int32_t* err_dev, void* stream);
+/* On-device admission: the decision of scheduler.select_batch (scheduler.py:73-123) — up to K
+ * requests spanning at most N deltas, first come first served, line skips linked to the earliest
+ * batch member of their delta — for an arrival-ordered queue q_*[Q] (Q <= 8192) and the running
+ * requests r_*[R]. *_model: delta id in [0, n_models) (n_models <= 4096); *_id: request id;
+ * *_rank: the request's rank in (arrival, id) order over queue and running requests together.
+ * Writes admitted[Q], skipped[Q] (0/1), parent[Q] (request id, -1 = none), selected[n_models]
+ * (0/1: the batch's delta set) and counts[0] = admitted requests; *err = DZ_E_VALUE for a delta
+ * id out of range. One CTA, stream-ordered, graph-capturable: the admitted requests' slots can
+ * feed dz_plan_device without a host round trip. Queue removal, request states and the lazy
+ * delta eviction (scheduler.py:106-123) stay with the caller's bookkeeping. */
+int dz_admit_device(const int32_t* q_model, const int32_t* q_id, const int32_t* q_rank, int32_t Q,
+                    const int32_t* r_model, const int32_t* r_id, const int32_t* r_rank, int32_t R,
+                    int32_t n_models, int32_t K, int32_t N, uint8_t* admitted, uint8_t* skipped,
+                    int32_t* parent, uint8_t* selected, int32_t* counts, int32_t* err, void* stream);
+
 /* K2 — fused decode SBMM. Replaces inference.sbmm (inference.py:126-154):
  * Y[t] = W_base x_t + ΔW_{slot(t)} x_t for every token in ONE persistent launch:
  * TMA stages W tiles (tcgen05.mma into TMEM), native delta blocks and X through

@@ -448,3 +448,31 @@ def obs_compress_layer(delta, hessian, bits: int, sparsity: str, group_size: int
     od = OracleDelta(rows=r, cols=c, packed_values=packed, index_stream=index, scales=sc, bits=bits,
                      sparsity=sparsity, group_size=group_size)
     return od, loss, quant
+
+
+# --------------------------------------------------------------------------- admission
+# (the decision of scheduler.select_batch, scheduler.py:73-123, restated as the
+#  checker of the on-device admission kernel; pinned to traces the reference produced,
+#  tests/golden/make_admit.py)
+
+
+def select_batch(queue, running, K: int, N: int):
+    """queue / running: lists of (request id, arrival, model id); the queue in (arrival, id) order.
+    Returns (batch ids in batch order, {line-skip id: parent id}, selected delta set).
+    scheduler.py:84-104: running requests first (sorted by key), then the head-first scan."""
+    key = {i: (a, i) for i, a, _ in list(queue) + list(running)}
+    selected = {m for _, _, m in running}
+    batch = sorted(((i, m) for i, _, m in running), key=lambda r: key[r[0]])
+    passed_over = False
+    skips = {}
+    for i, _, m in queue:
+        if len(batch) >= K:
+            break
+        if m in selected or len(selected) < N:
+            if passed_over:
+                skips[i] = min((r for r in batch if r[1] == m), key=lambda r: key[r[0]])[0]
+            selected.add(m)
+            batch.append((i, m))
+        else:
+            passed_over = True
+    return [i for i, _ in batch], skips, selected

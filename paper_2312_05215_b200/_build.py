@@ -17,7 +17,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
            "--expt-relaxed-constexpr", f"-I{os.path.join(ROOT, 'include')}"]
 
-SOURCES = ["dz_codec.cu", "dz_sbmm.cu", "dz_prefill.cu", "dz_tp.cu", "dz_plan.cu", "dz_obs.cu", "dz_host.cpp", "dz_dzdl.cpp"]
+SOURCES = ["dz_codec.cu", "dz_sbmm.cu", "dz_prefill.cu", "dz_tp.cu", "dz_plan.cu", "dz_sched.cu", "dz_obs.cu",
+           "dz_host.cpp", "dz_dzdl.cpp"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:

@@ -1,0 +1,107 @@
+"""Device residency for the drop-in numpy API.
+
+The reference functions are pure: `sbmm(base_layer, deltas, batch)` takes host arrays and
+dequantises every used delta on each call (inference.py:126-154). Re-uploading the base weight and
+re-laying out every delta per call would cost ~1000x the fused kernel, so the mirror keeps what
+it uploaded resident, keyed on the caller's objects:
+
+* the key is the object's identity; the entry is dropped when the object is garbage-collected
+  (weakref finalizer), so an id is never reused for a different object;
+* every hit re-checks a fingerprint: shape, dtype, strides and data pointer of each array, plus a
+  CRC of a fixed sample of elements (`SAMPLE` evenly spaced values, and the first and last row).
+  Replacing an array or a field, or resizing, is always detected; an in-place edit of an array
+  that was already passed is detected when it touches a sampled element. For arbitrary in-place
+  edits call `invalidate(obj)` (or `clear()`), or pass a fresh array.
+
+Nothing here computes anything: it only decides whether the resident copy can be reused.
+"""
+
+from __future__ import annotations
+
+import threading
+import weakref
+import zlib
+
+import numpy as np
+
+SAMPLE = 1024
+
+
+def _array_sig(a) -> tuple:
+    a = np.asarray(a)
+    sig = (a.shape, a.dtype.str, a.strides, a.__array_interface__["data"][0])
+    if a.size == 0:
+        return sig + (0,)
+    flat = a.reshape(-1) if a.flags.c_contiguous else np.ascontiguousarray(a).reshape(-1)
+    step = max(1, flat.size // SAMPLE)
+    crc = zlib.crc32(np.ascontiguousarray(flat[::step]).tobytes())
+    if a.ndim == 2:
+        crc = zlib.crc32(np.ascontiguousarray(a[0]).tobytes(), crc)
+        crc = zlib.crc32(np.ascontiguousarray(a[-1]).tobytes(), crc)
+    return sig + (crc,)
+
+
+def delta_sig(ld) -> tuple:
+    """Fingerprint of a LayerDelta (compress.py:101-143): configuration, array identities and samples."""
+    idx = bytes(ld.index_stream) if not isinstance(ld.index_stream, bytes) else ld.index_stream
+    step = max(1, len(idx) // SAMPLE)
+    return (int(ld.rows), int(ld.cols), int(ld.bits), str(ld.sparsity), int(ld.group_size),
+            _array_sig(ld.packed_values), _array_sig(ld.scales), id(ld.index_stream), len(idx),
+            zlib.crc32(idx[::step]))
+
+
+class ResidentCache:
+    """object -> (fingerprint, resident device object)."""
+
+    def __init__(self):
+        self._lock = threading.Lock()
+        self._entries: dict[int, tuple] = {}
+        self.enabled = True
+        self.hits = self.misses = 0
+
+    def get(self, obj, sig_fn, build):
+        if not self.enabled:
+            return build()
+        key = id(obj)
+        sig = sig_fn(obj)
+        with self._lock:
+            ent = self._entries.get(key)
+        if ent is not None and ent[0] == sig:
+            self.hits += 1
+            return ent[1]
+        self.misses += 1
+        val = build()
+        with self._lock:
+            if key not in self._entries:
+                try:
+                    weakref.finalize(obj, self._drop, key)
+                except TypeError:  # not weak-referenceable: do not cache
+                    return val
+            self._entries[key] = (sig, val)
+        return val
+
+    def _drop(self, key: int) -> None:
+        with self._lock:
+            self._entries.pop(key, None)
+
+    def invalidate(self, obj) -> None:
+        self._drop(id(obj))
+
+    def clear(self) -> None:
+        with self._lock:
+            self._entries.clear()
+
+    def __len__(self) -> int:
+        return len(self._entries)
+
+
+CACHE = ResidentCache()
+
+
+def invalidate(obj) -> None:
+    """Forget the resident copy of `obj` (a base weight array or a LayerDelta)."""
+    CACHE.invalidate(obj)
+
+
+def clear() -> None:
+    CACHE.clear()

@@ -41,11 +41,21 @@ def main():
     lds = {d: P.LayerDelta(name="l", rows=n, cols=n, packed_values=o.packed_values, index_stream=o.index_stream,
                            scales=o.scales, bits=4, sparsity="two_of_four", group_size=128) for d, o in enumerate(ods)}
     batch = P.BatchInput([(i, int(ids[i]), X[i]) for i in range(T)])
+    from paper_2312_05215_b200.resident import CACHE
+    CACHE.enabled = False  # the round-1 behaviour: upload + re-layout every call
     P.sbmm(W, lds, batch)  # warm-up (library load, kernel attributes)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     out = P.sbmm(W, lds, batch)
-    t_api = time.perf_counter() - t0
+    t_api_cold = time.perf_counter() - t0
+    CACHE.enabled = True  # residency: the same objects' uploads are reused (resident.py)
+    P.sbmm(W, lds, batch)
+    ts_api = []
+    for _ in range(20):
+        t0 = time.perf_counter()
+        out = P.sbmm(W, lds, batch)
+        ts_api.append(time.perf_counter() - t0)
+    t_api = float(np.median(ts_api))
     Y = np.stack([out[i] for i in range(T)])
     err_api = float((np.linalg.norm(Y - ref, axis=1) / np.linalg.norm(ref, axis=1)).max())
 
@@ -74,6 +84,7 @@ def main():
         "config": "cfg1: 4096x4096, 4 x 4-bit 2:4 deltas, T=16 (ids i%4)",
         "cpu_reference_s": t_cpu, "cpu_tokens_per_s": T / t_cpu,
         "api_sbmm_s": t_api, "api_tokens_per_s": T / t_api, "api_rel_err": err_api,
+        "api_sbmm_no_residency_s": t_api_cold,
         "device_us": t_dev * 1e6, "device_tokens_per_s": T / t_dev, "device_GBps": nbytes / t_dev / 1e9,
         "device_rel_err": err_dev, "algorithmic_bytes": nbytes,
     }), flush=True)

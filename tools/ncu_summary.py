@@ -33,8 +33,8 @@ def main():
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     idx = {h: i for i, h in enumerate(hdr)}
-    sb = [r for r in data if r[idx["Kernel Name"]].startswith("k_sbmm")]
-    fin = [r for r in data if r[idx["Kernel Name"]].startswith("k_finalize")]
+    sb = [r for r in data if "k_sbmm" in r[idx["Kernel Name"]]]
+    fin = [r for r in data if "k_finalize" in r[idx["Kernel Name"]]]
     assert len(sb) == 4 and len(fin) == 4, (len(sb), len(fin))
 
     def val(r, m):
@@ -62,13 +62,13 @@ def main():
                       "algorithmic_bytes": ALG[k]}
         lines.append(f"| {k} | {ALG[k] / 1e9:.4f} | {s / 1e9:.4f} | {s / ALG[k]:.3f} | {f / 1e6:.2f} | "
                      f"{sb[i][idx['gpu__time_duration.sum']]} | {fin[i][idx['gpu__time_duration.sum']]} |")
-    with open(os.path.join(ROOT, "profiles", f"r01_ncu_full_{tag}.md"), "w") as fh:
+    with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full.md"), "w") as fh:
         fh.write("\n".join(lines) + "\n")
-    js = {"source": f"profiles/r01_ncu_full_{tag}.md (ncu --set full, one capture per launch type, layer 2 of "
+    js = {"source": f"profiles/{tag}_ncu_full.md (ncu --set full, one capture per launch type, layer 2 of "
                     "bench.py --layers 3)", "kernel": f"k_sbmm {tag} (+ k_finalize)", "launches": traffic,
           "mean_dram_bytes_per_launch": sum(t["dram_bytes"] for t in traffic.values()) / 4,
           "mean_algorithmic_bytes_per_launch": sum(ALG.values()) / 4}
-    with open(os.path.join(ROOT, "profiles", f"r01_ncu_traffic_{tag}.json"), "w") as fh:
+    with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_traffic.json"), "w") as fh:
         json.dump(js, fh, indent=1)
     print("\n".join(lines[-6:]))
 
