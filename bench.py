@@ -17,8 +17,9 @@ column-parallel, o,down row-parallel, reduced by the finalize kernel over peer m
 NVLink; DZ_TP_FUSED=0 falls back to an NCCL all-reduce); shared dimensions cut on 128-column
 native-block edges (7B intermediate 11008 = 86 blocks, uneven at TP 4/8).
 
---impl reference: the reference algorithm (oracle port of inference.sbmm, numpy f64) on the
-host cores, one process per core over the active deltas.
+--impl reference: the reference's own sbmm (`deltazip.inference.sbmm` from baseline/_ref, installed
+from /root/reference/pkg; the oracle port when absent) on the host cores, one process per core over
+the active deltas, plus one real cfg1 call as the anchor of the extrapolation.
 """
 
 from __future__ import annotations
@@ -71,17 +72,49 @@ def token_ids():
 # ----------------------------------------------------------------------------- CPU reference arm
 
 
+def _reference_pkg():
+    """The reference package itself (`deltazip`, installed once from /root/reference/pkg into
+    baseline/_ref, git-ignored; it travels to the GPU box with the snapshot), or None — then the
+    CPU arm times the oracle port of the same algorithm instead."""
+    p = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(p, "deltazip")):
+        return None
+    if p not in sys.path:
+        sys.path.insert(0, p)
+    try:
+        import deltazip.compress  # noqa: F401
+        import deltazip.inference  # noqa: F401
+        return sys.modules["deltazip"]
+    except Exception:  # pragma: no cover
+        return None
+
+
+def _ref_delta(dz, o):
+    """A reference LayerDelta (compress.py:101-143) holding the oracle-generated packed fields."""
+    return dz.compress.LayerDelta(name="bench", rows=o.rows, cols=o.cols, packed_values=o.packed_values,
+                                  index_stream=o.index_stream, scales=o.scales, bits=o.bits, sparsity=o.sparsity,
+                                  group_size=o.group_size)
+
+
 def _delta_task(args):
-    """One active delta of the reference sbmm on one linear shape (oracle port, numpy f64):
-    dequantise + the routed tokens' GEMV (inference.py:140-153). Runs in a worker process."""
+    """One active delta of sbmm on one linear shape (dequantise + the routed tokens' products,
+    inference.py:140-153): the reference's own `deltazip.inference.sbmm` when installed, else the
+    oracle port. Runs in a worker process; times only the call."""
     out, inp, seed, tokens = args
     import oracle as O
     rng = np.random.default_rng(seed)
     W = rng.normal(0, 1 / math.sqrt(inp), (out, inp)).astype(np.float32).astype(np.float64)
     ld = O.random_packed_delta(rng, out, inp, BITS)
     X = rng.normal(0, 1, (tokens, inp))
-    t0 = time.perf_counter()
-    O.sbmm_matrix(W, {0: ld}, np.zeros(tokens, np.int64), X)
+    dz = _reference_pkg()
+    if dz is not None:
+        batch = dz.inference.BatchInput([(i, 0, X[i]) for i in range(tokens)])
+        rd = {0: _ref_delta(dz, ld)}
+        t0 = time.perf_counter()
+        dz.inference.sbmm(W, rd, batch)
+    else:
+        t0 = time.perf_counter()
+        O.sbmm_matrix(W, {0: ld}, np.zeros(tokens, np.int64), X)
     return time.perf_counter() - t0
 
 
@@ -105,8 +138,29 @@ def _base_task(args):
     return time.perf_counter() - t0
 
 
+def cfg1_anchor():
+    """One real call of the reference's sbmm at BASELINE configs[0] (4096x4096, 4 deltas 4-bit
+    2:4, 16 tokens ids perm(i%4)), single process: the measured point the extrapolated step rests on."""
+    dz = _reference_pkg()
+    if dz is None:
+        return None
+    import oracle as O
+    rng = np.random.default_rng(11)
+    n = 4096
+    W = rng.normal(0, 1 / math.sqrt(n), (n, n)).astype(np.float32).astype(np.float64)
+    lds = {d: _ref_delta(dz, O.random_packed_delta(rng, n, n, 4)) for d in range(4)}
+    ids = rng.permutation(np.arange(16) % 4)
+    batch = dz.inference.BatchInput([(i, int(ids[i]), rng.normal(0, 1, n)) for i in range(16)])
+    t0 = time.perf_counter()
+    dz.inference.sbmm(W, lds, batch)
+    dt = time.perf_counter() - t0
+    return {"config": "cfg1: 4096x4096, 4 x 4-bit 2:4 deltas, T=16", "seconds_per_call": dt, "tokens_per_s": 16 / dt,
+            "impl": "deltazip.inference.sbmm (baseline/_ref)"}
+
+
 class CpuReference:
-    """The reference algorithm (oracle port of inference.sbmm, numpy f64) on the host cores.
+    """The reference's sbmm on the host cores: `deltazip.inference.sbmm` itself (baseline/_ref)
+    when installed, else the oracle port (numpy f64).
 
     The reference's cost is one dequantise + GEMV per ACTIVE delta per linear (inference.py:
     140-153, single-threaded numpy masked gathers), so the step parallelises over deltas: a pool
@@ -118,6 +172,7 @@ class CpuReference:
         import multiprocessing as mp
         from paper_2312_05215_b200.synth import llama_linears
         self.cores = cores or min(os.cpu_count() or 1, 32)  # ~1.5 GB of numpy temporaries per worker
+        self.kind = "reference" if _reference_pkg() is not None else "port"
         self.pool = mp.get_context("fork").Pool(self.cores, initializer=_worker_init)
         self.shapes = {}
         for name, out, inp in llama_linears(MODEL):
@@ -137,10 +192,11 @@ class CpuReference:
             per_shape[(out, inp)] = (D_DELTAS * per_delta + tb, len(names))
         self.round += 1
         step_s = 32 * sum(t * n for t, n in per_shape.values())
-        desc = (f"oracle port of inference.sbmm (numpy f64): per distinct 7B linear shape, {self.cores} active "
-                f"deltas x {T_TOKENS // D_DELTAS} tokens dequantised concurrently on {self.cores} processes + the "
-                f"64-token base GEMM; extrapolated to {D_DELTAS} active deltas x 32 layers "
-                f"({work:.1f} s wall per sample)")
+        impl = ("deltazip.inference.sbmm (the reference package, baseline/_ref)" if self.kind == "reference"
+                else "oracle port of inference.sbmm (numpy f64)")
+        desc = (f"{impl}: per distinct 7B linear shape, {self.cores} active deltas x {T_TOKENS // D_DELTAS} tokens "
+                f"on {self.cores} processes (one delta each) + the 64-token base GEMM; extrapolated to {D_DELTAS} "
+                f"active deltas x 32 layers ({work:.1f} s wall per sample)")
         return T_TOKENS / step_s, work, desc
 
     def close(self):
@@ -159,6 +215,7 @@ def run_reference(args):
         v, w, desc = ref.sample()
         vals.append(v)
     ref.close()
+    anchor = cfg1_anchor()
     v = float(np.median(vals))
     line = {
         "impl": "reference", "metric": METRIC,
@@ -166,7 +223,8 @@ def run_reference(args):
         "ms_per_step": 1000.0 * T_TOKENS / v, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD.format(layers=32), "global_batch": T_TOKENS, "parallelism": "cpu"},
-        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": ref.cores, "kind": "port", "sample": desc},
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": ref.cores, "kind": ref.kind, "sample": desc,
+                         "cfg1_anchor": anchor},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -455,7 +513,8 @@ def main():
         ref = CpuReference()
         v, wsec, desc = ref.sample()
         ref.close()
-        cpu = {"value": v, "unit": "tokens/s", "cores": ref.cores, "kind": "port", "sample": desc}
+        cpu = {"value": v, "unit": "tokens/s", "cores": ref.cores, "kind": ref.kind, "sample": desc,
+               "cfg1_anchor": cfg1_anchor()}
 
     if rank == 0:
         line = {

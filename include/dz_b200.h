@@ -141,13 +141,17 @@ typedef struct dz_sbmm_args {
 /* Fused tensor-parallel reduction over peer memory (NVLink / NVSwitch), replacing the
  * reference's simulated all-reduce of row-parallel shards (inference.py:216-223) and a separate
  * NCCL all-reduce. Every rank's k_sbmm leaves fp32 partial planes; the finalize kernel sums them
- * into this rank's reduce buffer, publishes a ready flag to every peer, waits for all peers, and
- * sums the peers' buffers in rank order (identical, deterministic Y on every rank). Buffers are
- * double-buffered by a device-resident epoch, so the step stays CUDA-graph capturable. */
+ * into this rank's reduce buffer R, then runs a two-shot reduction over the peers' memory:
+ * reduce-scatter (rank r sums chunk r of every peer's R in rank order, applies the activation,
+ * stores it in its gather buffer G in Y's dtype) and all-gather (every rank copies every owner's
+ * chunk of G into Y). Identical, deterministic Y on every rank; NVLink bytes read per rank
+ * (w-1)/w * T*out * (4 + sizeof(Y)). Buffers are double-buffered by a device-resident epoch, so
+ * the step stays CUDA-graph capturable. */
 typedef struct dz_tp_ctx {
-  float* const* peer_R;     /* device array [world]: rank p's two reduce buffers (fp32,
-                               2 x max_elems), peer-mapped (dz_ipc_open)                  */
-  int* const* peer_flags;   /* device array [world]: rank p's ready flags [world] (int)    */
+  float* const* peer_R;     /* device array [world]: rank p's two reduce buffers R (fp32,
+                               2 x max_elems) followed by its two gather buffers G (2 x
+                               max_elems x 4 bytes), peer-mapped (dz_ipc_open)             */
+  int* const* peer_flags;   /* device array [world]: rank p's ready flags [2 phases][64]  */
   unsigned int* sync;       /* this rank's device words: [0] epoch, [1] barrier count,
                                [2] barrier generation (zeroed once)                        */
   int64_t max_elems;        /* capacity of one reduce buffer: >= T * out                   */

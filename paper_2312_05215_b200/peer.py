@@ -3,7 +3,8 @@ flags per rank in peer-shareable device memory, IPC handles exchanged over torch
 every peer's buffers opened in this process (NVLink / NVSwitch loads and stores).
 
 Replaces the row-parallel all-reduce (the reference's shard-order sum, inference.py:216-223) by
-a finalize kernel that reads the peers' fp32 partial sums directly: no NCCL call on the path.
+a two-shot finalize kernel over peer memory (reduce-scatter of the fp32 partial sums, then an
+all-gather of the reduced chunks in Y's dtype): no NCCL call on the path.
 """
 
 from __future__ import annotations
@@ -15,11 +16,12 @@ import torch
 from . import _lib as L
 from .errors import CudaError
 
-FLAG_BYTES = 256  # ready flags [world] (int32) at the head of every rank's buffer
+FLAG_BYTES = 512  # ready flags [2 phases][64] (int32) at the head of every rank's buffer
 
 
 class PeerGroup:
-    """This rank's view of the world's reduce buffers (capacity `max_elems` fp32 per buffer)."""
+    """This rank's view of the world's reduce buffers: per rank two fp32 reduce buffers R and two
+    gather buffers G (capacity `max_elems` elements each, double-buffered by epoch parity)."""
 
     def __init__(self, rank: int, world: int, max_elems: int, device, group=None):
         import torch.distributed as dist
@@ -27,7 +29,7 @@ class PeerGroup:
             raise ValueError("bad rank / world")
         lib = L.lib()
         self.rank, self.world, self.max_elems, self.device = rank, world, int(max_elems), device
-        nbytes = FLAG_BYTES + 2 * self.max_elems * 4
+        nbytes = FLAG_BYTES + 4 * self.max_elems * 4  # R[2] + G[2]
         ptr = C.c_void_p()
         with torch.cuda.device(device):
             L.check(lib.dz_peer_alloc(nbytes, C.byref(ptr)), "peer alloc")

@@ -1,7 +1,12 @@
 """GPU: the fused tensor-parallel reduction (dz_tp.cu) — row-parallel shards reduced by the
-finalize kernel over peer memory (CUDA IPC), no NCCL on the path. Two ranks run as two processes
-on this one GPU (the IPC / flag protocol is the same as across NVLink peers; the processes
-time-slice the device), each serving its shards of a Llama-shaped layer. Checks:
+two-shot finalize kernel over peer memory (CUDA IPC), no NCCL on the path. Two ranks run as two
+processes, each serving its shards of a Llama-shaped layer:
+  * "shared": both on cuda:0 (the IPC / flag protocol is the same as across NVLink peers; the
+    processes time-slice the device) — runs on any box;
+  * "two_gpus": rank r on cuda:r, real cross-device IPC mapping and system-scope flags over
+    NVLink — runs when >= 2 GPUs are visible, skipped otherwise;
+  * "nccl": two GPUs with the fused reduction off, the NCCL all-reduce fallback of stack.linear.
+Checks:
   * both ranks produce the same Y bit for bit (rank-order sum on every rank);
   * Y matches the unsharded layer within the bf16 tolerance (the reference's tp_forward
     contract, inference.py:180-225);
@@ -36,17 +41,22 @@ def _x():
     return torch.randn(T, 1024, generator=g).to(torch.bfloat16)
 
 
-def _rank_main(rank, world, port, q):
+def _rank_main(rank, world, port, q, placement="shared"):
     try:
         import torch.distributed as dist
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-        dist.init_process_group("gloo", rank=rank, world_size=world)
+        dev = torch.device("cuda", 0 if placement == "shared" else rank)
+        torch.cuda.set_device(dev)
+        if placement == "shared":  # NCCL refuses two ranks on one device
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+        else:
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
         from paper_2312_05215_b200.engine import Plan
         from paper_2312_05215_b200.stack import LlamaStack
-        dev = torch.device("cuda", 0)
-        torch.cuda.set_device(dev)
         st = LlamaStack("tiny", 1, D, 4, dev, rank=rank, world=world)
-        st.enable_fused_tp(T)
+        if placement != "nccl":
+            st.enable_fused_tp(T)
+            assert st.peers is not None, "fused TP reduction unavailable"
         plan = Plan(_ids(), st.kinds, D, device=dev)
         bufs = st.buffers(T)
         bufs["x"].copy_(_x().to(dev))
@@ -68,7 +78,8 @@ def _rank_main(rank, world, port, q):
         # vanish when this process exits before the parent opens it
         q.put((rank, y_eager.float().cpu().numpy(), y_graph.float().cpu().numpy(), None))
         dist.barrier()
-        st.peers.close()
+        if st.peers is not None:
+            st.peers.close()
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover - surfaced by the parent
         import traceback
@@ -76,9 +87,12 @@ def _rank_main(rank, world, port, q):
 
 
 @pytest.mark.timeout(600)
-def test_fused_tp_reduction_two_ranks():
+@pytest.mark.parametrize("placement", ["shared", "two_gpus", "nccl"])
+def test_fused_tp_reduction_two_ranks(placement):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
+    if placement != "shared" and torch.cuda.device_count() < 2:
+        pytest.skip("needs two visible GPUs")
     from paper_2312_05215_b200.engine import Plan
     from paper_2312_05215_b200.stack import LlamaStack
     dev = torch.device("cuda", 0)
@@ -91,7 +105,7 @@ def test_fused_tp_reduction_two_ranks():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q, placement)) for r in range(2)]
     for p in procs:
         p.start()
     res = {}
