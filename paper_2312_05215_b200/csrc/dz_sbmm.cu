@@ -184,7 +184,16 @@ __device__ __forceinline__ void item_coords(int item, int nrt, int nbt, int nspl
 #ifndef DZ_DEFAULT_BASE_SPLITS
 #define DZ_DEFAULT_BASE_SPLITS 1
 #endif
-__host__ __device__ inline int base_splits(int /*out*/, int /*in*/) { return DZ_DEFAULT_BASE_SPLITS; }
+#ifndef DZ_SPLIT_RULE
+#define DZ_SPLIT_RULE 0
+#endif
+__host__ __device__ inline int base_splits(int out, int /*in*/) {
+  if (DZ_SPLIT_RULE) {  // enough base items for every SM of a B200 (148): shape-keyed, never batch-keyed
+    const int nbt = (out + 127) / 128, s = (148 + nbt - 1) / nbt;
+    return s > 4 ? 4 : s;
+  }
+  return DZ_DEFAULT_BASE_SPLITS;
+}
 // Default K-splits of each decode delta job: 1. Splitting the delta items of the out <= 4096 layers
 // in two measured neutral at the BASELINE batch and mixed at low batch (profiles/r01_ab_dsplit.txt),
 // so it stays an explicit knob (dz_sbmm_args.delta_splits). Never derived from the batch.
