@@ -136,6 +136,10 @@ typedef struct dz_sbmm_args {
   const struct dz_sbmm_args* next; /* device copy of the NEXT linear's args in the step, or NULL:
                                CTAs that run out of items warm L2 with the first weight stages
                                their blockIdx gets in that launch (decode plans only)      */
+  const int32_t* pf_counts_dev; /* mixed plan made on the device (dz_plan_mixed_device), or NULL:
+                               device [3] = {prefill jobs, decode jobs, t_pf}; then n_pf_jobs is
+                               the prefill-region capacity (T: decode jobs start at jobs[T]),
+                               n_jobs = n_pf_jobs + decode capacity, and t_pf is ignored     */
 } dz_sbmm_args;
 
 /* Fused tensor-parallel reduction over peer memory (NVLink / NVSwitch), replacing the
@@ -254,6 +258,14 @@ int dz_admit_device(const int32_t* q_model, const int32_t* q_id, const int32_t* 
                     const int32_t* r_model, const int32_t* r_id, const int32_t* r_rank, int32_t R,
                     int32_t n_models, int32_t K, int32_t N, uint8_t* admitted, uint8_t* skipped,
                     int32_t* parent, uint8_t* selected, int32_t* counts, int32_t* err, void* stream);
+
+/* On-device mixed plan: dz_plan_mixed (prefill staging for K3 + the decode plan over the staged
+ * rows) computed by one CTA from device-resident slots. Writes perm[T], order[T], prefill jobs to
+ * jobs[0, T) and decode jobs to jobs[T, T + dz_plan_max_jobs(T)), counts_dev[3] = {prefill jobs,
+ * decode jobs, t_pf}; *err_dev as dz_plan_device. Pass counts_dev as dz_sbmm_args.pf_counts_dev. */
+int dz_plan_mixed_device(const int32_t* slots_dev, int32_t T, const int32_t* kinds_dev, int32_t n_slots,
+                         int32_t with_base, int32_t pf_min, int32_t* perm_dev, int32_t* order_dev,
+                         dz_job* jobs_dev, int32_t* counts_dev, int32_t* err_dev, void* stream);
 
 /* K2 — fused decode SBMM. Replaces inference.sbmm (inference.py:126-154):
  * Y[t] = W_base x_t + ΔW_{slot(t)} x_t for every token in ONE persistent launch:

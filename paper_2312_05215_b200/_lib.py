@@ -67,6 +67,7 @@ class DzSbmmArgs(C.Structure):
         ("keep_planes", C.c_int32), ("prefill_variant", C.c_int32),
         ("fused_merge", C.c_int32), ("_pad5", C.c_int32),
         ("next", C.c_void_p),
+        ("pf_counts_dev", C.c_void_p),
     ]
 
 
@@ -122,6 +123,8 @@ SIGNATURES = {
     "dz_inflate": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]),
     "dz_plan_device": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                  C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "dz_plan_mixed_device": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "dz_admit_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                   C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

@@ -102,3 +102,140 @@ extern "C" int dz_plan_device(const int32_t* slots_dev, int32_t T, const int32_t
                                                                    order_dev, jobs_dev, max_jobs, n_jobs_dev, err_dev);
   return cudaGetLastError() == cudaSuccess ? DZ_OK : DZ_E_CUDA;
 }
+
+// ------------------------------------------------------------------------------------------
+// On-device MIXED plan (dz_plan_mixed_device): the same staging and job cut as the host
+// dz_plan_mixed (dz_host.cpp): groups of >= pf_min tokens of a 2:4 kind send their first
+// J*floor(c/J) tokens (J = DZ_PREFILL_JOB_TOKENS, original order) plus a remainder of >= rmin
+// tokens to prefill jobs (K3), staged first grouped by slot; every other token follows in its
+// original order and is planned for K2 like dz_plan over the staged rows. Prefill jobs go to
+// jobs[0, T) and decode jobs to jobs[T, ...) so the launches can use fixed offsets; the counts
+// are written to counts[0] = prefill jobs, counts[1] = decode jobs, counts[2] = t_pf.
+namespace dz {
+namespace plan {
+
+__global__ void __launch_bounds__(1024) k_plan_mixed(const int32_t* __restrict__ slots, int T,
+                                                     const int32_t* __restrict__ kinds, int n_slots, int with_base,
+                                                     int pf_min, int32_t* __restrict__ perm, int32_t* __restrict__ order,
+                                                     dz_job* __restrict__ jobs, int32_t* __restrict__ counts,
+                                                     int32_t* __restrict__ err) {
+  extern __shared__ int sh[];
+  int* count = sh;               // [n_slots]
+  int* npf = sh + n_slots;       // [n_slots] prefill tokens of the slot
+  int* pstart = npf + n_slots;   // [n_slots] first staged prefill row of the slot
+  int* dstart = pstart + n_slots;  // [n_slots] first decode `order` position of the slot
+  int* rank = dstart + n_slots;  // [n_slots] running occurrence counter (stable pass)
+  __shared__ int bad, t_pf, n_pf, n_dec;
+  const int tid = threadIdx.x;
+  for (int s = tid; s < n_slots; s += blockDim.x) { count[s] = 0; rank[s] = 0; }
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int t = tid; t < T; t += blockDim.x) {
+    const int s = slots[t];
+    if (s < 0 || s >= n_slots) bad = 1;
+    else atomicAdd(&count[s], 1);
+  }
+  __syncthreads();
+  if (bad) {
+    if (tid == 0) { *err = DZ_E_UNKNOWN; counts[0] = counts[1] = counts[2] = 0; }
+    return;
+  }
+  if (tid == 0) {  // per-slot split and exclusive scans (n_slots <= 4096: a serial pass is ~µs)
+    int ps = 0, pj = 0;
+    for (int s = 0; s < n_slots; s++) {
+      const int c = count[s], k = kinds[s];
+      int np = 0;
+      if (pf_min > 0 && c >= pf_min && k != DZ_KIND_DENSE) {
+        const int rem = c % DZ_PREFILL_JOB_TOKENS;
+        const int rmin = c >= DZ_PREFILL_JOB_TOKENS ? (pf_min < DZ_PREFILL_REM_MIN ? pf_min : DZ_PREFILL_REM_MIN) : pf_min;
+        np = c - rem + (rem >= rmin ? rem : 0);
+      }
+      npf[s] = np;
+      pstart[s] = ps;
+      ps += np;
+      pj += (np + DZ_PREFILL_JOB_TOKENS - 1) / DZ_PREFILL_JOB_TOKENS;
+    }
+    t_pf = ps;
+    n_pf = pj;
+    const int n_base = with_base ? (T - ps + DZ_BASE_JOB_TOKENS - 1) / DZ_BASE_JOB_TOKENS : 0;
+    int ds = 0, dj = n_base;
+    for (int s = 0; s < n_slots; s++) {
+      const int c = count[s] - npf[s], chunk = kinds[s] == DZ_KIND_DENSE ? 32 : 8;
+      dstart[s] = ds;
+      ds += c;
+      dj += (c + chunk - 1) / chunk;
+    }
+    n_dec = dj;
+    counts[0] = pj;
+    counts[1] = dj;
+    counts[2] = ps;
+    *err = DZ_OK;
+  }
+  __syncthreads();
+  // prefill jobs [0, n_pf) in slot order, decode jobs from T: base jobs, then delta jobs per slot
+  if (tid == 32) {  // (warp 0 runs the stable pass below)
+    int pj = 0, dj = 0;
+    for (int s = 0; s < n_slots; s++)
+      for (int off = 0; off < npf[s]; off += DZ_PREFILL_JOB_TOKENS)
+        jobs[pj++] = dz_job{s, pstart[s] + off, min(DZ_PREFILL_JOB_TOKENS, npf[s] - off), kinds[s]};
+    const int n_base = with_base ? (T - t_pf + DZ_BASE_JOB_TOKENS - 1) / DZ_BASE_JOB_TOKENS : 0;
+    for (int b = 0; b < n_base; b++) {
+      const int b0 = t_pf + b * DZ_BASE_JOB_TOKENS;
+      jobs[T + dj++] = dz_job{-1, b0, min(DZ_BASE_JOB_TOKENS, T - b0), 0};
+    }
+    for (int s = 0; s < n_slots; s++) {
+      const int c = count[s] - npf[s], chunk = kinds[s] == DZ_KIND_DENSE ? 32 : 8;
+      for (int off = 0; off < c; off += chunk) jobs[T + dj++] = dz_job{s, dstart[s] + off, min(chunk, c - off), kinds[s]};
+    }
+  }
+  // stable pass, one warp, tokens in original order: the occurrence rank of each token inside its
+  // slot decides prefill (rank < npf) or decode; decode tokens keep their original order after t_pf
+  if (tid < 32) {
+    const unsigned lt = (1u << tid) - 1u;
+    int ndec = 0;  // decode tokens seen so far (warp-uniform)
+    for (int b = 0; b < T; b += 32) {
+      const int t = b + tid;
+      const unsigned active = __ballot_sync(0xffffffffu, t < T);
+      int s = 0, r = 0;
+      bool pre = false;
+      if (t < T) {
+        s = slots[t];
+        const unsigned same = __match_any_sync(active, s);
+        r = rank[s] + __popc(same & lt);
+        __syncwarp(active);
+        if ((same & lt) == 0) rank[s] += __popc(same);
+        pre = r < npf[s];
+      }
+      const unsigned dec = __ballot_sync(0xffffffffu, t < T && !pre);
+      if (t < T) {
+        if (pre) {
+          perm[pstart[s] + r] = t;
+        } else {
+          const int row = t_pf + ndec + __popc(dec & lt);  // staged row of this decode token
+          perm[row] = t;
+          order[dstart[s] + (r - npf[s])] = row;
+        }
+      }
+      ndec += __popc(dec);
+      __syncwarp();
+    }
+  }
+}
+
+}  // namespace plan
+}  // namespace dz
+
+extern "C" int dz_plan_mixed_device(const int32_t* slots_dev, int32_t T, const int32_t* kinds_dev, int32_t n_slots,
+                                    int32_t with_base, int32_t pf_min, int32_t* perm_dev, int32_t* order_dev,
+                                    dz_job* jobs_dev, int32_t* counts_dev, int32_t* err_dev, void* stream) {
+  if (T < 0 || n_slots < 1 || n_slots > 4096 || !counts_dev || !err_dev) return DZ_E_VALUE;
+  if (T > 0 && (!slots_dev || !perm_dev || !order_dev || !jobs_dev || !kinds_dev)) return DZ_E_VALUE;
+  const size_t smem = static_cast<size_t>(5) * n_slots * sizeof(int);
+  static std::once_flag once;  // one-time, idempotent kernel attribute setup
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(plan::k_plan_mixed, cudaFuncAttributeMaxDynamicSharedMemorySize, 5 * 4096 * 4);
+  });
+  plan::k_plan_mixed<<<1, 1024, smem, static_cast<cudaStream_t>(stream)>>>(
+      slots_dev, T, kinds_dev, n_slots, with_base, pf_min, perm_dev, order_dev, jobs_dev, counts_dev, err_dev);
+  return cudaGetLastError() == cudaSuccess ? DZ_OK : DZ_E_CUDA;
+}

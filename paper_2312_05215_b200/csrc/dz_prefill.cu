@@ -288,7 +288,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   Smem<MT, SP>* sm = reinterpret_cast<Smem<MT, SP>*>(dslots + NDSLOT * DSLOT);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  const int n_jobs = a.n_pf_jobs;
+  int n_jobs = a.n_pf_jobs;
+  if (a.pf_counts_dev != nullptr) {  // device mixed plan: the count is the planner's output
+    griddep_wait();
+    n_jobs = a.pf_counts_dev[0];
+  }
   const int nrt = ceil_div(a.out, C::ROWS);
   const Sched sc = make_sched(nrt * n_jobs, static_cast<int>(gridDim.x));
   const int n_items = sc.n_items;

@@ -589,9 +589,10 @@ __device__ __forceinline__ void finalize_rows(const float* __restrict__ part, in
 // partial in planes: the default decode launch (k_sbmm<false>), delta K-splits, probes.
 __global__ void __launch_bounds__(256) k_finalize(const float* __restrict__ part, int nsplit, int t0, int T, int out,
                                                   const int32_t* __restrict__ perm, void* __restrict__ Y, int64_t ldy,
-                                                  int y_dtype, int act) {
+                                                  int y_dtype, int act, const int32_t* __restrict__ t0_dev) {
   griddep_wait();
   griddep_launch_dependents();
+  if (t0_dev != nullptr) t0 = *t0_dev;  // device mixed plan: t_pf
   finalize_rows(part, nsplit, t0, T, out, perm, Y, ldy, y_dtype, act,
                 blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x, static_cast<int64_t>(gridDim.x) * blockDim.x);
 }
@@ -818,7 +819,12 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
   const int nkb = ceil_div(a.in, kBlkCols);
   const int nch_base = ceil_div(a.in, BASE_CH * KC_DN);
   const int nbt = ceil_div(a.out, BASE_RT);
-  const int n_base = a.base != nullptr ? ceil_div(a.T - a.t_pf, BASE_N) : 0;  // dz_plan: base jobs first
+  int t_pf = a.t_pf;
+  if (a.pf_counts_dev != nullptr) {  // device mixed plan: the staged prefill rows come from the planner
+    griddep_wait();
+    t_pf = a.pf_counts_dev[2];
+  }
+  const int n_base = a.base != nullptr ? ceil_div(a.T - t_pf, BASE_N) : 0;  // dz_plan: base jobs first
   const int nsplit = a.base_splits;  // resolved by the host (launch_decode)
   const int dsplit = a.delta_splits;  // resolved by the host (launch_decode)
 
@@ -1359,7 +1365,8 @@ static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
   int fgrid = static_cast<int>((work + 255) / 256);
   fgrid = fgrid > 4 * 148 ? 4 * 148 : fgrid < 1 ? 1 : fgrid;
   return launch_pdl(2, k_finalize, fgrid, 256, 0, stream, part, a->base_splits + a->delta_splits - 1, a->t_pf, a->T,
-                    a->out, a->perm, a->Y, a->ldy, a->y_dtype, a->act);
+                    a->out, a->perm, a->Y, a->ldy, a->y_dtype, a->act,
+                    a->pf_counts_dev != nullptr ? a->pf_counts_dev + 2 : static_cast<const int32_t*>(nullptr));
 }
 
 extern "C" int dz_sbmm(const dz_sbmm_args* a, void* stream) {
@@ -1373,10 +1380,11 @@ extern "C" int dz_sbmm(const dz_sbmm_args* a, void* stream) {
   if (a->ldy < a->out) return DZ_E_SHAPE;
   if (a->y_dtype != DZ_F32 && a->y_dtype != DZ_BF16) return DZ_E_VALUE;
   if (a->perm == nullptr) {
-    if (a->n_pf_jobs != 0 || a->t_pf != 0) return DZ_E_VALUE;
+    if (a->n_pf_jobs != 0 || a->t_pf != 0 || a->pf_counts_dev != nullptr) return DZ_E_VALUE;
     return launch_decode(a, stream);
   }
-  // mixed plan: stage X in plan order, prefill jobs on K3, the rest on K2
+  // mixed plan: stage X in plan order, prefill jobs on K3, the rest on K2 (a device mixed plan
+  // passes capacities on the host and the counts in pf_counts_dev)
   if (!a->xs || a->n_pf_jobs < 0 || a->n_pf_jobs > a->n_jobs || a->t_pf < 0 || a->t_pf > a->T) return DZ_E_VALUE;
   const int64_t ldxs = a->ldxs > 0 ? a->ldxs : a->ldx;
   if (ldxs < in_pad || (ldxs % 8) != 0 || (reinterpret_cast<uintptr_t>(a->xs) & 15) != 0) return DZ_E_SHAPE;
@@ -1394,6 +1402,7 @@ extern "C" int dz_sbmm(const dz_sbmm_args* a, void* stream) {
     k.jobs = a->jobs + a->n_pf_jobs;
     k.n_jobs = a->n_jobs - a->n_pf_jobs;
     k.n_pf_jobs = 0;
+    if (a->pf_counts_dev != nullptr) k.n_jobs_dev = a->pf_counts_dev + 1;  // decode job count
     return launch_decode(&k, stream);
   }
   return DZ_OK;

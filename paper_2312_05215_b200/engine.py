@@ -197,28 +197,44 @@ class Plan:
 
 
 class DevicePlan:
-    """On-device decode plan (dz_plan_device): the token -> slot map stays on the
-    GPU and each `update` enqueues one planner CTA that writes order / jobs / the job count, so a
-    decode loop (or a captured CUDA graph of it) needs no host round trip. Same stable
-    group_by_delta and job cut as `Plan` (decode plans: no prefill staging)."""
+    """On-device plan: the token -> slot map stays on the GPU and each `update`
+    enqueues one planner CTA, so a serving loop (or a captured CUDA graph of it) needs no host
+    round trip.
 
-    def __init__(self, T: int, kinds: np.ndarray, n_slots: int, with_base: bool = True, device=None):
+    mixed=False (default): dz_plan_device — the decode plan (same stable group_by_delta and job cut
+    as `Plan` with pf_min=0). mixed=True: dz_plan_mixed_device — `Plan`'s mixed plan: groups of
+    >= pf_min tokens staged for the tensor-core prefill kernel (K3), the rest planned for K2; the
+    counts (prefill jobs, decode jobs, staged prefill rows) stay on the device."""
+
+    def __init__(self, T: int, kinds: np.ndarray, n_slots: int, with_base: bool = True, device=None,
+                 mixed: bool = False, pf_min: int | None = None):
         dev = device or require_cuda()
         lib = L.lib()
-        self.T, self.n_slots, self.with_base = int(T), int(n_slots), with_base
+        self.T, self.n_slots, self.with_base, self.mixed = int(T), int(n_slots), with_base, mixed
+        self.pf_min = (PF_MIN if pf_min is None else int(pf_min)) if mixed else 0
         self.kinds_dev = torch.from_numpy(np.ascontiguousarray(kinds, dtype=np.int32)).to(dev)
         self.max_jobs = int(lib.dz_plan_max_jobs(self.T))
-        self.n_jobs = self.max_jobs  # capacity: the kernel reads the device count
+        pf_cap = self.T if mixed else 0  # prefill region of the job list (decode jobs start at jobs[T])
+        self.n_jobs = pf_cap + self.max_jobs  # capacity: the kernels read the device counts
         self.order = torch.zeros(max(self.T, 1), dtype=torch.int32, device=dev)
-        self.jobs = torch.zeros(max(self.max_jobs, 1) * C.sizeof(L.DzJob), dtype=torch.uint8, device=dev)
+        self.jobs = torch.zeros(max(self.n_jobs, 1) * C.sizeof(L.DzJob), dtype=torch.uint8, device=dev)
         self.n_jobs_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.counts = torch.zeros(3, dtype=torch.int32, device=dev)  # mixed: prefill jobs, decode jobs, t_pf
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.perm, self.t_pf, self.n_pf_jobs = None, 0, 0
+        self.t_pf, self.n_pf_jobs = 0, pf_cap
+        self.perm = torch.zeros(max(self.T, 1), dtype=torch.int32, device=dev) if mixed else None
 
     def update(self, slots_dev: torch.Tensor) -> "DevicePlan":
         if slots_dev.numel() != self.T or slots_dev.dtype != torch.int32 or not slots_dev.is_cuda:
             raise ShapeError("slots must be an int32 CUDA tensor of T entries")
-        L.check(L.lib().dz_plan_device(slots_dev.data_ptr(), self.T, self.kinds_dev.data_ptr(), self.n_slots,
+        lib = L.lib()
+        if self.mixed:
+            L.check(lib.dz_plan_mixed_device(slots_dev.data_ptr(), self.T, self.kinds_dev.data_ptr(), self.n_slots,
+                                             1 if self.with_base else 0, self.pf_min, self.perm.data_ptr(),
+                                             self.order.data_ptr(), self.jobs.data_ptr(), self.counts.data_ptr(),
+                                             self.err.data_ptr(), stream_ptr()), "device mixed plan")
+        else:
+            L.check(lib.dz_plan_device(slots_dev.data_ptr(), self.T, self.kinds_dev.data_ptr(), self.n_slots,
                                        1 if self.with_base else 0, self.order.data_ptr(), self.jobs.data_ptr(),
                                        self.max_jobs, self.n_jobs_dev.data_ptr(), self.err.data_ptr(),
                                        stream_ptr()), "device plan")
@@ -322,7 +338,10 @@ def sbmm_args(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: Delta
     if tp is not None:  # peer.PeerGroup: row-parallel shard, reduced over peer memory by the finalize
         a.tp = C.addressof(tp.ctx)
     if isinstance(plan, DevicePlan):
-        a.n_jobs_dev = plan.n_jobs_dev.data_ptr()
+        if plan.mixed:
+            a.pf_counts_dev = plan.counts.data_ptr()
+        else:
+            a.n_jobs_dev = plan.n_jobs_dev.data_ptr()
     xs = None
     if plan.perm is not None:  # mixed plan: staged (permuted) copy of X, compact padded rows
         ldxs = _ceil(inp, BLK_COLS) * BLK_COLS
