@@ -36,11 +36,9 @@ extern "C" {
 #ifndef DZ_BASE_JOB_TOKENS
 #define DZ_BASE_JOB_TOKENS 128 /* tokens per base-GEMM job of the decode kernel (its UMMA N) */
 #endif
-#ifndef DZ_PREFILL_REM_MIN
-#define DZ_PREFILL_REM_MIN 32      /* smallest remainder of a large group kept on the prefill path */
-#endif
 #ifndef DZ_PREFILL_JOB_TOKENS
-#define DZ_PREFILL_JOB_TOKENS 240 /* tokens per prefill job of K3 (its UMMA N), multiple of 16 */
+#define DZ_PREFILL_JOB_TOKENS 240 /* most tokens per prefill job of K3 (its UMMA N), multiple of 16;
+                                    a group is cut into ceil(c / 240) jobs of equal 16-aligned size */
 #endif
 /* ---- element types --------------------------------------------------------------- */
 #define DZ_F32 0
@@ -132,7 +130,10 @@ typedef struct dz_sbmm_args {
   int32_t fused_merge;      /* 1: Y written inside k_sbmm by a combiner warp per CTA (one launch per
                                linear, no k_finalize); 0 (default): k_finalize sums the partial
                                planes (measured faster, profiles/r02_ab_fused_merge.txt) */
-  int32_t _pad5;
+  int32_t mixed_parts;      /* mixed plans: which parts this call runs, bit 0 = stage X into xs,
+                               bit 1 = prefill jobs (K3), bit 2 = decode jobs (K2 + merge); 0 = all.
+                               Lets a caller run K3 and K2 concurrently on two streams with a
+                               split of the SMs (args.grid per call) after staging once. */
   const struct dz_sbmm_args* next; /* device copy of the NEXT linear's args in the step, or NULL:
                                CTAs that run out of items warm L2 with the first weight stages
                                their blockIdx gets in that launch (decode plans only)      */
@@ -226,8 +227,15 @@ int32_t dz_plan_max_jobs(int32_t T);
 int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t n_slots,
             int32_t with_base, int32_t* order_out, dz_job* jobs_out, int32_t max_jobs,
             int32_t* n_jobs_out);
-/* Mixed plan: delta groups of >= pf_min tokens (2:4 sparse kinds) become prefill jobs of
- * <= 256 tokens for K3, staged first in perm (grouped by slot, stable); the remaining tokens
+/* Tokens per prefill job of a c-token group: ceil(c / ceil(c / DZ_PREFILL_JOB_TOKENS)) rounded up
+ * to 16 (the last job of the group takes the rest). */
+#define DZ_PREFILL_JOB_SIZE(c)                                                                   \
+  ((c) < 1 ? DZ_PREFILL_JOB_TOKENS                                                                \
+           : ((((c) + ((c) + DZ_PREFILL_JOB_TOKENS - 1) / DZ_PREFILL_JOB_TOKENS - 1) /            \
+               (((c) + DZ_PREFILL_JOB_TOKENS - 1) / DZ_PREFILL_JOB_TOKENS) + 15) / 16) * 16)
+/* Mixed plan: delta groups of >= pf_min tokens (2:4 sparse kinds) go to K3 whole, cut into
+ * ceil(c / DZ_PREFILL_JOB_TOKENS) jobs of DZ_PREFILL_JOB_SIZE(c) tokens (a 256-token request: 2 x 128),
+ * staged first in perm (grouped by slot, stable); the remaining tokens
  * keep their original order after them and are planned for K2 exactly as dz_plan does, with
  * order_out indexing staged rows. *t_pf_out = staged prefill rows; when it is 0 the plan is
  * the pure decode plan and perm is the identity (pass perm = NULL to dz_sbmm). */

@@ -65,7 +65,7 @@ class DzSbmmArgs(C.Structure):
         ("tp", C.c_void_p),
         ("n_jobs_dev", C.c_void_p),
         ("keep_planes", C.c_int32), ("prefill_variant", C.c_int32),
-        ("fused_merge", C.c_int32), ("_pad5", C.c_int32),
+        ("fused_merge", C.c_int32), ("mixed_parts", C.c_int32),
         ("next", C.c_void_p),
         ("pf_counts_dev", C.c_void_p),
     ]

@@ -60,11 +60,12 @@ extern "C" int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, in
   return DZ_OK;
 }
 
-// Mixed plan (prefill + decode). A group of c >= pf_min tokens with a 2:4 sparse kind sends its
-// first J*floor(c/J) tokens (in original order) to prefill jobs of J = DZ_PREFILL_JOB_TOKENS, plus the remainder as
-// one more prefill job when it still has >= pf_min tokens; prefill tokens are staged first
-// (grouped by slot in slot order). Every other token follows in its original order and is planned
-// exactly like dz_plan over the staged rows.
+// Mixed plan (prefill + decode). A group of c >= pf_min tokens with a 2:4 sparse kind goes to the
+// prefill kernel whole: ceil(c / J) jobs (J = DZ_PREFILL_JOB_TOKENS) of equal 16-aligned size, the
+// last one shorter (a 256-token request becomes 2 x 128 instead of 240 + a 16-token remainder that
+// would re-stream the delta twice on the decode kernel). Prefill tokens are staged first (grouped
+// by slot in slot order); every other token follows in its original order and is planned exactly
+// like dz_plan over the staged rows.
 extern "C" int dz_plan_mixed(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t n_slots,
                              int32_t with_base, int32_t pf_min, int32_t* perm_out, int32_t* order_out,
                              dz_job* jobs_out, int32_t max_jobs, int32_t* n_jobs_out, int32_t* n_pf_jobs_out,
@@ -80,16 +81,8 @@ extern "C" int dz_plan_mixed(const int32_t* slots, int32_t T, const int32_t* kin
   std::vector<int32_t> count(static_cast<size_t>(n_slots), 0);
   for (int32_t t = 0; t < T; t++) count[slots[t]]++;
   std::vector<int32_t> npf(static_cast<size_t>(n_slots), 0);  // prefill tokens per slot
-  for (int32_t s = 0; s < n_slots; s++) {
-    if (pf_min <= 0 || count[s] < pf_min || kinds[s] == DZ_KIND_DENSE) continue;
-    const int32_t rem = count[s] % DZ_PREFILL_JOB_TOKENS;
-    // the remainder of a group that already has full prefill jobs becomes one more (narrower)
-    // prefill job when it has >= DZ_PREFILL_REM_MIN tokens (cheaper than rem/8 decode jobs each
-    // re-streaming the delta); a group below one full job keeps the pf_min rule
-    const int32_t rmin = count[s] >= DZ_PREFILL_JOB_TOKENS ? (pf_min < DZ_PREFILL_REM_MIN ? pf_min : DZ_PREFILL_REM_MIN)
-                                                           : pf_min;
-    npf[s] = count[s] - rem + (rem >= rmin ? rem : 0);
-  }
+  for (int32_t s = 0; s < n_slots; s++)
+    if (pf_min > 0 && count[s] >= pf_min && kinds[s] != DZ_KIND_DENSE) npf[s] = count[s];
   // staged order: prefill groups by slot, then the decode tokens in original order
   std::vector<int32_t> pstart(static_cast<size_t>(n_slots) + 1, 0);
   for (int32_t s = 0; s < n_slots; s++) pstart[s + 1] = pstart[s] + npf[s];
@@ -113,11 +106,11 @@ extern "C" int dz_plan_mixed(const int32_t* slots, int32_t T, const int32_t* kin
     jobs_out[nj++] = dz_job{slot, b, c, kind};
     return true;
   };
-  for (int32_t s = 0; s < n_slots; s++)
-    for (int32_t off = 0; off < npf[s]; off += DZ_PREFILL_JOB_TOKENS)
-      if (!push(s, pstart[s] + off, (npf[s] - off) < DZ_PREFILL_JOB_TOKENS ? (npf[s] - off) : DZ_PREFILL_JOB_TOKENS,
-                kinds[s]))
-        return DZ_E_VALUE;
+  for (int32_t s = 0; s < n_slots; s++) {
+    const int32_t step = DZ_PREFILL_JOB_SIZE(npf[s]);
+    for (int32_t off = 0; off < npf[s]; off += step)
+      if (!push(s, pstart[s] + off, (npf[s] - off) < step ? (npf[s] - off) : step, kinds[s])) return DZ_E_VALUE;
+  }
   const int32_t n_pf = nj;
   // decode part over staged rows [t_pf, T): base jobs, then delta jobs (dz_plan's rules)
   const int32_t Td = T - t_pf;

@@ -105,10 +105,9 @@ extern "C" int dz_plan_device(const int32_t* slots_dev, int32_t T, const int32_t
 
 // ------------------------------------------------------------------------------------------
 // On-device MIXED plan (dz_plan_mixed_device): the same staging and job cut as the host
-// dz_plan_mixed (dz_host.cpp): groups of >= pf_min tokens of a 2:4 kind send their first
-// J*floor(c/J) tokens (J = DZ_PREFILL_JOB_TOKENS, original order) plus a remainder of >= rmin
-// tokens to prefill jobs (K3), staged first grouped by slot; every other token follows in its
-// original order and is planned for K2 like dz_plan over the staged rows. Prefill jobs go to
+// dz_plan_mixed (dz_host.cpp): groups of >= pf_min tokens of a 2:4 kind go whole to prefill jobs
+// (K3) of DZ_PREFILL_JOB_SIZE tokens, staged first grouped by slot; every other token follows in
+// its original order and is planned for K2 like dz_plan over the staged rows. Prefill jobs go to
 // jobs[0, T) and decode jobs to jobs[T, ...) so the launches can use fixed offsets; the counts
 // are written to counts[0] = prefill jobs, counts[1] = decode jobs, counts[2] = t_pf.
 namespace dz {
@@ -144,16 +143,12 @@ __global__ void __launch_bounds__(1024) k_plan_mixed(const int32_t* __restrict__
     int ps = 0, pj = 0;
     for (int s = 0; s < n_slots; s++) {
       const int c = count[s], k = kinds[s];
-      int np = 0;
-      if (pf_min > 0 && c >= pf_min && k != DZ_KIND_DENSE) {
-        const int rem = c % DZ_PREFILL_JOB_TOKENS;
-        const int rmin = c >= DZ_PREFILL_JOB_TOKENS ? (pf_min < DZ_PREFILL_REM_MIN ? pf_min : DZ_PREFILL_REM_MIN) : pf_min;
-        np = c - rem + (rem >= rmin ? rem : 0);
-      }
+      const int np = (pf_min > 0 && c >= pf_min && k != DZ_KIND_DENSE) ? c : 0;
       npf[s] = np;
       pstart[s] = ps;
       ps += np;
-      pj += (np + DZ_PREFILL_JOB_TOKENS - 1) / DZ_PREFILL_JOB_TOKENS;
+      const int step = DZ_PREFILL_JOB_SIZE(np);
+      pj += (np + step - 1) / step;
     }
     t_pf = ps;
     n_pf = pj;
@@ -175,9 +170,10 @@ __global__ void __launch_bounds__(1024) k_plan_mixed(const int32_t* __restrict__
   // prefill jobs [0, n_pf) in slot order, decode jobs from T: base jobs, then delta jobs per slot
   if (tid == 32) {  // (warp 0 runs the stable pass below)
     int pj = 0, dj = 0;
-    for (int s = 0; s < n_slots; s++)
-      for (int off = 0; off < npf[s]; off += DZ_PREFILL_JOB_TOKENS)
-        jobs[pj++] = dz_job{s, pstart[s] + off, min(DZ_PREFILL_JOB_TOKENS, npf[s] - off), kinds[s]};
+    for (int s = 0; s < n_slots; s++) {
+      const int step = DZ_PREFILL_JOB_SIZE(npf[s]);
+      for (int off = 0; off < npf[s]; off += step) jobs[pj++] = dz_job{s, pstart[s] + off, min(step, npf[s] - off), kinds[s]};
+    }
     const int n_base = with_base ? (T - t_pf + DZ_BASE_JOB_TOKENS - 1) / DZ_BASE_JOB_TOKENS : 0;
     for (int b = 0; b < n_base; b++) {
       const int b0 = t_pf + b * DZ_BASE_JOB_TOKENS;

@@ -1388,16 +1388,21 @@ extern "C" int dz_sbmm(const dz_sbmm_args* a, void* stream) {
   if (!a->xs || a->n_pf_jobs < 0 || a->n_pf_jobs > a->n_jobs || a->t_pf < 0 || a->t_pf > a->T) return DZ_E_VALUE;
   const int64_t ldxs = a->ldxs > 0 ? a->ldxs : a->ldx;
   if (ldxs < in_pad || (ldxs % 8) != 0 || (reinterpret_cast<uintptr_t>(a->xs) & 15) != 0) return DZ_E_SHAPE;
-  int st = dz_gather_rows(a->X, a->ldx, a->perm, a->T, in_pad, static_cast<uint16_t*>(a->xs), ldxs, stream);
-  if (st) return st;
+  const int parts = a->mixed_parts != 0 ? a->mixed_parts : 7;
+  if (parts & ~7) return DZ_E_VALUE;
+  int st = DZ_OK;
+  if (parts & 1) {
+    st = dz_gather_rows(a->X, a->ldx, a->perm, a->T, in_pad, static_cast<uint16_t*>(a->xs), ldxs, stream);
+    if (st) return st;
+  }
   dz_sbmm_args s = *a;  // the staged buffer replaces X for both kernels
   s.X = static_cast<const uint16_t*>(a->xs);
   s.ldx = ldxs;
-  if (a->n_pf_jobs > 0) {
+  if ((parts & 2) && a->n_pf_jobs > 0) {
     st = dz_sbmm_prefill(&s, stream);
     if (st) return st;
   }
-  if (a->n_jobs > a->n_pf_jobs) {
+  if ((parts & 4) && a->n_jobs > a->n_pf_jobs) {
     dz_sbmm_args k = s;
     k.jobs = a->jobs + a->n_pf_jobs;
     k.n_jobs = a->n_jobs - a->n_pf_jobs;

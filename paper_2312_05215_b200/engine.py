@@ -286,21 +286,85 @@ def sbmm_forward(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: De
                  y_dtype: torch.dtype = torch.bfloat16, act: int = L.DZ_ACT_NONE, Y: torch.Tensor | None = None,
                  workspace: Workspace | None = None, grid: int = 0, debug: int = 0,
                  base_splits: int = 0, tp=None, delta_splits: int = 0, next_args: int = 0,
-                 prefill_variant: int = 0, fused_merge: bool = False) -> torch.Tensor:
+                 prefill_variant: int = 0, fused_merge: bool = False, overlap_sms: int | None = None) -> torch.Tensor:
     """Y[T, out] = X W_base^T + ΔW_{slot(t)} x_t for all t, one fused launch (inference.py:126-154).
 
     next_args: device address of the next linear's dz_sbmm_args (see `sbmm_args`), or 0; CTAs that
     run out of work then warm L2 with that launch's first weight stages.
     prefill_variant: K3's delta product for mixed plans (0 = 2:4-sparse tcgen05; 1 / 2 = the
     dense-dequantised variant with 128- / 256-row items, for A/B runs and equivalence tests).
-    fused_merge: write Y inside the SBMM kernel (combiner warp) instead of a k_finalize launch."""
+    fused_merge: write Y inside the SBMM kernel (combiner warp) instead of a k_finalize launch.
+    overlap_sms: mixed plans only — SMs given to the prefill kernel (K3) while the decode kernel
+    (K2) runs on the rest, concurrently on a second stream (None / 0: one after the other, the
+    default: both kernels need every SM — K3 its tensor cores, K2 its decode warps — so a split
+    measured 2-19% slower on cfg3, profiles/r02_ab_cfg3_overlap.txt; -1: the split from
+    `split_sms`)."""
     a, Y, keep = sbmm_args(X, plan, base, table, y_dtype, act, Y, workspace, grid, debug, base_splits, tp,
                            delta_splits)
     a.prefill_variant = prefill_variant
     a.fused_merge = 1 if fused_merge else 0
     a.next = next_args or None
-    L.check(L.lib().dz_sbmm(C.byref(a), stream_ptr()), "sbmm")
+    lib = L.lib()
+    sms = _sm_count(X.device)
+    pf_sms = 0
+    if plan.perm is not None and grid == 0 and plan.n_pf_jobs > 0 and plan.n_jobs > plan.n_pf_jobs:
+        pf_sms = 0 if not overlap_sms else split_sms(plan, table, X.shape[1], sms) if overlap_sms < 0 else overlap_sms
+    if pf_sms <= 0 or pf_sms >= sms:
+        L.check(lib.dz_sbmm(C.byref(a), stream_ptr()), "sbmm")
+        return Y
+    # stage X once, then K3 on an auxiliary stream with pf_sms SMs while K2 runs on the rest: a
+    # tensor-bound and an HBM-bound kernel share the machine (graph-capturable fork / join)
+    main = torch.cuda.current_stream(X.device)
+    aux = _aux_stream(X.device)
+    a.mixed_parts = 1
+    L.check(lib.dz_sbmm(C.byref(a), main.cuda_stream), "sbmm stage")
+    aux.wait_stream(main)
+    a.mixed_parts, a.grid = 2, pf_sms
+    L.check(lib.dz_sbmm(C.byref(a), aux.cuda_stream), "sbmm prefill")
+    a.mixed_parts, a.grid = 4, sms - pf_sms
+    L.check(lib.dz_sbmm(C.byref(a), main.cuda_stream), "sbmm decode")
+    main.wait_stream(aux)
     return Y
+
+
+_AUX: dict = {}
+_SMS: dict = {}
+
+
+def _aux_stream(device) -> torch.cuda.Stream:
+    key = torch.device(device).index
+    if key not in _AUX:
+        _AUX[key] = torch.cuda.Stream(device=device)
+    return _AUX[key]
+
+
+def _sm_count(device) -> int:
+    key = torch.device(device).index
+    if key not in _SMS:
+        _SMS[key] = torch.cuda.get_device_properties(device).multi_processor_count
+    return _SMS[key]
+
+
+def split_sms(plan, table, inp: int, sms: int) -> int:
+    """SMs for K3 when K3 and K2 of a mixed plan run concurrently: balance the prefill part's tensor
+    time (3 flops per staged token per weight: base GEMM + kept 2:4 delta MACs, at ~6.5 TFLOP/s per
+    SM sustained by K3) against the decode part's HBM time (base + the decode groups' deltas at
+    ~45 GB/s per SM, capped by ~6 TB/s)."""
+    out = table.out
+    if isinstance(plan, Plan):
+        t_pf = plan.t_pf
+        dec_slots = {int(s) for s, _, _, k in plan.jobs_host[plan.n_pf_jobs:] if k != 0}
+    else:  # device mixed plan: counts unknown on the host, assume half the tokens prefill
+        t_pf = plan.T // 2
+        dec_slots = set(range(len(table)))
+    flops = 3.0 * t_pf * out * inp
+    nbytes = 2.0 * out * inp + sum(table.deltas[s].nbytes for s in dec_slots)
+    best, best_t = 0, float("inf")
+    for s in range(8, sms - 8, 4):
+        t = max(flops / (s * 6.5e12), nbytes / min((sms - s) * 45e9, 6.0e12))
+        if t < best_t:
+            best, best_t = s, t
+    return best
 
 
 def sbmm_args(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: DeltaTable,

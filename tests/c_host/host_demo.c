@@ -30,14 +30,14 @@ int main(int argc, char** argv) {
   int32_t bad[2] = {0, 7};
   CHECK(dz_plan(bad, 2, kinds, 3, 1, order, jobs, 16, &n_jobs) == DZ_E_UNKNOWN);
   printf("unknown slot -> %s\n", dz_strerror(DZ_E_UNKNOWN));
-  /* mixed plan: 300 tokens on slot 0 -> prefill jobs of DZ_PREFILL_JOB_TOKENS + the remainder */
+  /* mixed plan: 300 tokens on slot 0 -> two prefill jobs of equal 16-aligned size (160 + 140) */
   int32_t T = 300 + 5, *s2 = malloc(sizeof(int32_t) * T), *perm = malloc(sizeof(int32_t) * T);
   int32_t *ord2 = malloc(sizeof(int32_t) * T), n_pf = 0, t_pf = 0;
   dz_job* jobs2 = malloc(sizeof(dz_job) * dz_plan_max_jobs(T));
   for (int i = 0; i < T; i++) s2[i] = i < 300 ? 0 : 1;
   CHECK(dz_plan_mixed(s2, T, kinds, 3, 1, 192, perm, ord2, jobs2, dz_plan_max_jobs(T), &n_jobs, &n_pf, &t_pf) ==
         DZ_OK);
-  CHECK(t_pf == 300 && n_pf == 2 && jobs2[0].tok_count == DZ_PREFILL_JOB_TOKENS);
+  CHECK(t_pf == 300 && n_pf == 2 && jobs2[0].tok_count == 160 && jobs2[1].tok_count == 140);
   printf("mixed plan ok: %d prefill rows, %d jobs\n", t_pf, n_jobs);
   /* DZDL walk */
   if (argc > 1) {

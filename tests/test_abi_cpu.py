@@ -173,13 +173,10 @@ def test_plan_mixed_prefill_decode_host_logic():
         p = Plan(ids, kinds, D, upload=False, pf_min=64)
         T = ids.size
         cnt = np.bincount(ids, minlength=D)
-        J, RM = _header_define("DZ_PREFILL_JOB_TOKENS"), _header_define("DZ_PREFILL_REM_MIN")
+        J = _header_define("DZ_PREFILL_JOB_TOKENS")
 
-        def n_prefill(c):  # dz_plan_mixed's rule (pf_min = 64)
-            if c < 64:
-                return 0
-            rmin = min(64, RM) if c >= J else 64
-            return c - c % J + (c % J if c % J >= rmin else 0)
+        def n_prefill(c):  # dz_plan_mixed's rule (pf_min = 64): the whole group
+            return c if c >= 64 else 0
         npf = np.array([0 if kinds[s] == 3 else n_prefill(cnt[s]) for s in range(D)])
         assert p.t_pf == npf.sum()
         perm = p.perm_host if p.t_pf else np.arange(T)
@@ -190,7 +187,8 @@ def test_plan_mixed_prefill_decode_host_logic():
         covered = []
         for k, (slot, b, c, kind) in enumerate(jobs):
             if k < p.n_pf_jobs:
-                assert 0 < c <= J and kind == kinds[slot] and kind != 3
+                nj = -(-cnt[slot] // J)
+                assert 0 < c <= -(-(-(-cnt[slot] // nj)) // 16) * 16 <= J and kind == kinds[slot] and kind != 3
                 rows = perm[b:b + c]
                 assert np.all(ids[rows] == slot)
                 covered += rows.tolist()

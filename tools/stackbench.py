@@ -59,6 +59,7 @@ def main():
     ap.add_argument("--base-splits", type=int, default=0, help="K-splits of the decode base GEMM (0 = by shape)")
     ap.add_argument("--max-batch", type=int, default=256, help="sweep: largest batch")
     ap.add_argument("--points", default="", help="sweep subset: D:B,D:B,...")
+    ap.add_argument("--overlap-sms", type=int, default=None, help="mixed plans: SMs for K3 (0 = no overlap)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -75,6 +76,7 @@ def main():
     st = LlamaStack(args.model, args.layers, args.deltas, args.bits, dev, rank=args.rank, world=args.world)
     st.world = 1  # one rank's shard timed alone: no collective in this process
     st.base_splits = args.base_splits
+    st.overlap_sms = args.overlap_sms
     if args.sweep:
         Ds = [d for d in (1, 2, 4, 8, 16, 32, 64, 128) if d <= args.deltas]
         Bs = tuple(b for b in (1, 2, 4, 8, 16, 32, 64, 128, 256) if b <= args.max_batch)
