@@ -2,6 +2,7 @@
 # BASELINE configs 3-5 through the layer-stack bench (tools/stackbench.py); one JSON line each.
 set -u
 O=${1:-gpurun_out}
+mkdir -p $O
 timeout 900 python tools/stackbench.py --model 13b --layers 16 --deltas 64 --bits 2 --prefill 8x256 --decode 128 > $O/cfg3.json 2> $O/cfg3.err
 timeout 900 python tools/stackbench.py --model 13b --layers 16 --deltas 64 --bits 2 --prefill 8x256 --decode 128 --pf-min 100000 > $O/cfg3_nopf.json 2> $O/cfg3_nopf.err
 timeout 900 python tools/stackbench.py --model 70b --layers 8 --deltas 16 --decode 64 > $O/cfg4_tp1.json 2> $O/cfg4_tp1.err
