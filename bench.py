@@ -443,7 +443,9 @@ def main():
         # step k+1's tokens and delta ids while step k runs without racing the in-flight copies.
         from paper_2312_05215_b200.engine import DevicePlan
         hid = bufs["x"].shape[1]
-        dplan = DevicePlan(T_TOKENS, kinds, D_DELTAS, device=device)
+        # decode batches of a few tokens per delta: 8-token 2:4 jobs (the narrow kernel instantiation;
+        # a token's result does not depend on the job width)
+        dplan = DevicePlan(T_TOKENS, kinds, D_DELTAS, device=device, sparse_job_tokens=8)
         slots_dev = torch.zeros(T_TOKENS, dtype=torch.int32, device=device)
         if tail_pf:
             st.prepare_chain(dplan, bufs)

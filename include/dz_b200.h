@@ -36,6 +36,9 @@ extern "C" {
 #ifndef DZ_BASE_JOB_TOKENS
 #define DZ_BASE_JOB_TOKENS 128 /* tokens per base-GEMM job of the decode kernel (its UMMA N) */
 #endif
+#define DZ_SPARSE_JOB_TOKENS 16  /* most tokens per 2:4 delta job of the decode kernel (2 mma.sp n-tiles);
+                                    the planners take the job width (8 or 16; 0 = 8) as an argument */
+#define DZ_DENSE_JOB_TOKENS 32   /* tokens per dense-delta job of the decode kernel */
 #ifndef DZ_PREFILL_JOB_TOKENS
 #define DZ_PREFILL_JOB_TOKENS 240 /* most tokens per prefill job of K3 (its UMMA N), multiple of 16;
                                     a group is cut into ceil(c / 240) jobs of equal 16-aligned size */
@@ -83,7 +86,8 @@ typedef struct dz_native_delta {
 typedef struct dz_job {
   int32_t slot;             /* delta-table index; -1 = base GEMM over all tokens     */
   int32_t tok_begin;        /* first position in `order` (delta) or token (base)     */
-  int32_t tok_count;        /* <= DZ_BASE_JOB_TOKENS (base), <= 32 (dense delta), <= 8 (sparse), <= 256 (prefill) */
+  int32_t tok_count;        /* <= DZ_BASE_JOB_TOKENS (base), <= DZ_DENSE_JOB_TOKENS (dense delta),
+                               <= DZ_SPARSE_JOB_TOKENS (2:4 delta), <= DZ_PREFILL_JOB_TOKENS (prefill) */
   int32_t kind;             /* 0 = base, else DZ_KIND_* of the slot                  */
 } dz_job;
 
@@ -141,6 +145,9 @@ typedef struct dz_sbmm_args {
                                device [3] = {prefill jobs, decode jobs, t_pf}; then n_pf_jobs is
                                the prefill-region capacity (T: decode jobs start at jobs[T]),
                                n_jobs = n_pf_jobs + decode capacity, and t_pf is ignored     */
+  int32_t sparse_job_tokens; /* the plan's 2:4 job width (the planners' argument): 8 selects the
+                               kernel instantiation with the smaller X stage; 0 / 16 the wide one */
+  int32_t _pad6;
 } dz_sbmm_args;
 
 /* Fused tensor-parallel reduction over peer memory (NVLink / NVSwitch), replacing the
@@ -222,11 +229,14 @@ int dz_pad_x(const uint16_t* X, int64_t ldx, int32_t T, int32_t in, uint16_t* Xp
 /* Host-side plan. Replaces inference.group_by_delta (inference.py:106-123): stable
  * sort of token rows by slot, then cut into dz_jobs. kinds[n_slots] gives each
  * slot's DZ_KIND_*. Returns DZ_E_UNKNOWN when a slot is out of range
- * (inference.py:135-137). max_jobs >= dz_plan_max_jobs(T). */
+ * (inference.py:135-137). max_jobs >= dz_plan_max_jobs(T). sparse_job_tokens (8 or 16,
+ * 0 = 8; the same argument on every planner) is the width of a 2:4 delta job: a token's result
+ * does not depend on it (the n-tiles of a job are independent MMA columns), 16 decodes each
+ * delta chunk once for twice the tokens (pass dz_sbmm_args.sparse_job_tokens the same value). */
 int32_t dz_plan_max_jobs(int32_t T);
 int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t n_slots,
             int32_t with_base, int32_t* order_out, dz_job* jobs_out, int32_t max_jobs,
-            int32_t* n_jobs_out);
+            int32_t* n_jobs_out, int32_t sparse_job_tokens);
 /* Tokens per prefill job of a c-token group: ceil(c / ceil(c / DZ_PREFILL_JOB_TOKENS)) rounded up
  * to 16 (the last job of the group takes the rest). */
 #define DZ_PREFILL_JOB_SIZE(c)                                                                   \
@@ -242,7 +252,7 @@ int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t n_slo
 int dz_plan_mixed(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t n_slots,
                   int32_t with_base, int32_t pf_min, int32_t* perm_out, int32_t* order_out,
                   dz_job* jobs_out, int32_t max_jobs, int32_t* n_jobs_out, int32_t* n_pf_jobs_out,
-                  int32_t* t_pf_out);
+                  int32_t* t_pf_out, int32_t sparse_job_tokens);
 
 /* On-device plan (decode plans): the same stable group_by_delta and job cut as dz_plan, computed
  * by one CTA from device-resident slots, so a decode loop never round-trips to the host (SURVEY
@@ -251,7 +261,7 @@ int dz_plan_mixed(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t
  * is too small. n_slots <= 4096. Stream-ordered, graph-capturable. */
 int dz_plan_device(const int32_t* slots_dev, int32_t T, const int32_t* kinds_dev, int32_t n_slots,
                    int32_t with_base, int32_t* order_dev, dz_job* jobs_dev, int32_t max_jobs,
-                   int32_t* n_jobs_dev, int32_t* err_dev, void* stream);
+                   int32_t* n_jobs_dev, int32_t* err_dev, int32_t sparse_job_tokens, void* stream);
 /* On-device admission: the decision of scheduler.select_batch (scheduler.py:73-123) — up to K
  * requests spanning at most N deltas, first come first served, line skips linked to the earliest
  * batch member of their delta — for an arrival-ordered queue q_*[Q] (Q <= 8192) and the running
@@ -273,7 +283,8 @@ int dz_admit_device(const int32_t* q_model, const int32_t* q_id, const int32_t* 
  * decode jobs, t_pf}; *err_dev as dz_plan_device. Pass counts_dev as dz_sbmm_args.pf_counts_dev. */
 int dz_plan_mixed_device(const int32_t* slots_dev, int32_t T, const int32_t* kinds_dev, int32_t n_slots,
                          int32_t with_base, int32_t pf_min, int32_t* perm_dev, int32_t* order_dev,
-                         dz_job* jobs_dev, int32_t* counts_dev, int32_t* err_dev, void* stream);
+                         dz_job* jobs_dev, int32_t* counts_dev, int32_t* err_dev,
+                         int32_t sparse_job_tokens, void* stream);
 
 /* K2 — fused decode SBMM. Replaces inference.sbmm (inference.py:126-154):
  * Y[t] = W_base x_t + ΔW_{slot(t)} x_t for every token in ONE persistent launch:

@@ -68,6 +68,7 @@ class DzSbmmArgs(C.Structure):
         ("fused_merge", C.c_int32), ("mixed_parts", C.c_int32),
         ("next", C.c_void_p),
         ("pf_counts_dev", C.c_void_p),
+        ("sparse_job_tokens", C.c_int32), ("_pad6", C.c_int32),
     ]
 
 
@@ -107,10 +108,10 @@ SIGNATURES = {
     "dz_pad_x": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p]),
     "dz_plan_max_jobs": (C.c_int32, [C.c_int32]),
     "dz_plan": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
-                          C.c_int32, C.POINTER(C.c_int32)]),
+                          C.c_int32, C.POINTER(C.c_int32), C.c_int32]),
     "dz_plan_mixed": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                 C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
-                                C.POINTER(C.c_int32)]),
+                                C.POINTER(C.c_int32), C.c_int32]),
     "dz_sbmm_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int32]),
     "dz_sbmm_prefill": (C.c_int, [C.POINTER(DzSbmmArgs), C.c_void_p]),
     "dz_gather_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int64,
@@ -122,9 +123,10 @@ SIGNATURES = {
                                        C.POINTER(C.c_int64)]),
     "dz_inflate": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]),
     "dz_plan_device": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
-                                 C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+                                 C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     "dz_plan_mixed_device": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
-                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                       C.c_void_p]),
     "dz_admit_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                   C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

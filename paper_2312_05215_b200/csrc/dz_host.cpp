@@ -23,12 +23,17 @@ extern "C" const char* dz_strerror(int status) {
 
 extern "C" int32_t dz_plan_max_jobs(int32_t T) { return T < 0 ? 0 : 2 * T + 2; }  // >= base + delta + prefill jobs
 
+static int32_t sparse_chunk(int32_t sparse_job_tokens) {
+  return sparse_job_tokens == 16 ? 16 : sparse_job_tokens == 0 || sparse_job_tokens == 8 ? 8 : -1;
+}
+
 // Stable sort of token rows by slot (inference.py:106-123: `sorted` is stable), then cut into
 // jobs: base token chunks of DZ_BASE_JOB_TOKENS, sparse delta chunks of 8, dense delta chunks of 32.
 extern "C" int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t n_slots,
                        int32_t with_base, int32_t* order_out, dz_job* jobs_out, int32_t max_jobs,
-                       int32_t* n_jobs_out) {
-  if (T < 0 || n_slots < 0 || !n_jobs_out) return DZ_E_VALUE;
+                       int32_t* n_jobs_out, int32_t sparse_job_tokens) {
+  const int32_t sp_chunk = sparse_chunk(sparse_job_tokens);
+  if (T < 0 || n_slots < 0 || !n_jobs_out || sp_chunk < 0) return DZ_E_VALUE;
   *n_jobs_out = 0;
   for (int32_t t = 0; t < T; t++)
     if (slots[t] < 0 || slots[t] >= n_slots) return DZ_E_UNKNOWN;  // inference.py:135-137
@@ -52,7 +57,7 @@ extern "C" int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, in
     const int32_t kind = kinds[s];
     if (kind != DZ_KIND_SPARSE4 && kind != DZ_KIND_SPARSE2 && kind != DZ_KIND_SPARSE3 && kind != DZ_KIND_DENSE)
       return DZ_E_VALUE;
-    const int32_t chunk = kind == DZ_KIND_DENSE ? 32 : 8;
+    const int32_t chunk = kind == DZ_KIND_DENSE ? DZ_DENSE_JOB_TOKENS : sp_chunk;
     for (int32_t off = 0; off < c; off += chunk)
       if (!push(s, start[s] + off, (c - off) < chunk ? (c - off) : chunk, kind)) return DZ_E_VALUE;
   }
@@ -69,8 +74,9 @@ extern "C" int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, in
 extern "C" int dz_plan_mixed(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t n_slots,
                              int32_t with_base, int32_t pf_min, int32_t* perm_out, int32_t* order_out,
                              dz_job* jobs_out, int32_t max_jobs, int32_t* n_jobs_out, int32_t* n_pf_jobs_out,
-                             int32_t* t_pf_out) {
-  if (T < 0 || n_slots < 0 || !n_jobs_out || !n_pf_jobs_out || !t_pf_out) return DZ_E_VALUE;
+                             int32_t* t_pf_out, int32_t sparse_job_tokens) {
+  const int32_t sp_chunk = sparse_chunk(sparse_job_tokens);
+  if (T < 0 || n_slots < 0 || !n_jobs_out || !n_pf_jobs_out || !t_pf_out || sp_chunk < 0) return DZ_E_VALUE;
   *n_jobs_out = *n_pf_jobs_out = *t_pf_out = 0;
   for (int32_t t = 0; t < T; t++)
     if (slots[t] < 0 || slots[t] >= n_slots) return DZ_E_UNKNOWN;  // inference.py:135-137
@@ -125,7 +131,7 @@ extern "C" int dz_plan_mixed(const int32_t* slots, int32_t T, const int32_t* kin
   for (int32_t s = 0; s < n_slots; s++) {
     const int32_t c = dcount[s + 1] - dcount[s];
     if (c == 0) continue;
-    const int32_t chunk = kinds[s] == DZ_KIND_DENSE ? 32 : 8;
+    const int32_t chunk = kinds[s] == DZ_KIND_DENSE ? DZ_DENSE_JOB_TOKENS : sp_chunk;
     for (int32_t off = 0; off < c; off += chunk)
       if (!push(s, dstart[s] + off, (c - off) < chunk ? (c - off) : chunk, kinds[s])) return DZ_E_VALUE;
   }

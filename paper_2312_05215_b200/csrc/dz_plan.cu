@@ -16,7 +16,8 @@ namespace plan {
 __global__ void __launch_bounds__(1024) k_plan(const int32_t* __restrict__ slots, int T,
                                                const int32_t* __restrict__ kinds, int n_slots, int with_base,
                                                int32_t* __restrict__ order, dz_job* __restrict__ jobs, int max_jobs,
-                                               int32_t* __restrict__ n_jobs_out, int32_t* __restrict__ err) {
+                                               int32_t* __restrict__ n_jobs_out, int32_t* __restrict__ err,
+                                               int sp_chunk) {
   extern __shared__ int sh[];
   int* count = sh;              // [n_slots]
   int* fill = sh + n_slots;     // [n_slots] running position (stable scatter)
@@ -40,7 +41,7 @@ __global__ void __launch_bounds__(1024) k_plan(const int32_t* __restrict__ slots
   if (tid == 0) {  // exclusive scans over slots (n_slots <= 4096: a serial pass is ~µs)
     int pos = 0, jb = n_base;
     for (int s = 0; s < n_slots; s++) {
-      const int c = count[s], chunk = kinds[s] == DZ_KIND_DENSE ? 32 : 8;
+      const int c = count[s], chunk = kinds[s] == DZ_KIND_DENSE ? DZ_DENSE_JOB_TOKENS : sp_chunk;
       fill[s] = pos;
       jstart[s] = jb;
       pos += c;
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(1024) k_plan(const int32_t* __restrict__ slots
   if (total_jobs > max_jobs) return;
   // delta jobs (slot order) and base jobs, before fill[] is consumed by the scatter
   for (int s = tid; s < n_slots; s += blockDim.x) {
-    const int c = count[s], chunk = kinds[s] == DZ_KIND_DENSE ? 32 : 8;
+    const int c = count[s], chunk = kinds[s] == DZ_KIND_DENSE ? DZ_DENSE_JOB_TOKENS : sp_chunk;
     for (int k = 0; k * chunk < c; k++) {
       const int n = c - k * chunk < chunk ? c - k * chunk : chunk;
       jobs[jstart[s] + k] = dz_job{s, fill[s] + k * chunk, n, kinds[s]};
@@ -90,8 +91,10 @@ using namespace dz;
 
 extern "C" int dz_plan_device(const int32_t* slots_dev, int32_t T, const int32_t* kinds_dev, int32_t n_slots,
                               int32_t with_base, int32_t* order_dev, dz_job* jobs_dev, int32_t max_jobs,
-                              int32_t* n_jobs_dev, int32_t* err_dev, void* stream) {
+                              int32_t* n_jobs_dev, int32_t* err_dev, int32_t sparse_job_tokens, void* stream) {
+  const int sp_chunk = sparse_job_tokens == 0 ? 8 : sparse_job_tokens;
   if (T < 0 || n_slots < 1 || n_slots > 4096 || !n_jobs_dev || !err_dev || max_jobs < 0) return DZ_E_VALUE;
+  if (sp_chunk != 8 && sp_chunk != 16) return DZ_E_VALUE;
   if (T > 0 && (!slots_dev || !order_dev || !jobs_dev || !kinds_dev)) return DZ_E_VALUE;
   const size_t smem = static_cast<size_t>(3) * n_slots * sizeof(int);
   static std::once_flag once;  // one-time, idempotent kernel attribute setup
@@ -99,7 +102,7 @@ extern "C" int dz_plan_device(const int32_t* slots_dev, int32_t T, const int32_t
     cudaFuncSetAttribute(plan::k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 4096 * 4);
   });
   plan::k_plan<<<1, 1024, smem, static_cast<cudaStream_t>(stream)>>>(slots_dev, T, kinds_dev, n_slots, with_base,
-                                                                   order_dev, jobs_dev, max_jobs, n_jobs_dev, err_dev);
+                                                                   order_dev, jobs_dev, max_jobs, n_jobs_dev, err_dev, sp_chunk);
   return cudaGetLastError() == cudaSuccess ? DZ_OK : DZ_E_CUDA;
 }
 
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(1024) k_plan_mixed(const int32_t* __restrict__
                                                      const int32_t* __restrict__ kinds, int n_slots, int with_base,
                                                      int pf_min, int32_t* __restrict__ perm, int32_t* __restrict__ order,
                                                      dz_job* __restrict__ jobs, int32_t* __restrict__ counts,
-                                                     int32_t* __restrict__ err) {
+                                                     int32_t* __restrict__ err, int sp_chunk) {
   extern __shared__ int sh[];
   int* count = sh;               // [n_slots]
   int* npf = sh + n_slots;       // [n_slots] prefill tokens of the slot
@@ -155,7 +158,7 @@ __global__ void __launch_bounds__(1024) k_plan_mixed(const int32_t* __restrict__
     const int n_base = with_base ? (T - ps + DZ_BASE_JOB_TOKENS - 1) / DZ_BASE_JOB_TOKENS : 0;
     int ds = 0, dj = n_base;
     for (int s = 0; s < n_slots; s++) {
-      const int c = count[s] - npf[s], chunk = kinds[s] == DZ_KIND_DENSE ? 32 : 8;
+      const int c = count[s] - npf[s], chunk = kinds[s] == DZ_KIND_DENSE ? DZ_DENSE_JOB_TOKENS : sp_chunk;
       dstart[s] = ds;
       ds += c;
       dj += (c + chunk - 1) / chunk;
@@ -180,7 +183,7 @@ __global__ void __launch_bounds__(1024) k_plan_mixed(const int32_t* __restrict__
       jobs[T + dj++] = dz_job{-1, b0, min(DZ_BASE_JOB_TOKENS, T - b0), 0};
     }
     for (int s = 0; s < n_slots; s++) {
-      const int c = count[s] - npf[s], chunk = kinds[s] == DZ_KIND_DENSE ? 32 : 8;
+      const int c = count[s] - npf[s], chunk = kinds[s] == DZ_KIND_DENSE ? DZ_DENSE_JOB_TOKENS : sp_chunk;
       for (int off = 0; off < c; off += chunk) jobs[T + dj++] = dz_job{s, dstart[s] + off, min(chunk, c - off), kinds[s]};
     }
   }
@@ -223,8 +226,11 @@ __global__ void __launch_bounds__(1024) k_plan_mixed(const int32_t* __restrict__
 
 extern "C" int dz_plan_mixed_device(const int32_t* slots_dev, int32_t T, const int32_t* kinds_dev, int32_t n_slots,
                                     int32_t with_base, int32_t pf_min, int32_t* perm_dev, int32_t* order_dev,
-                                    dz_job* jobs_dev, int32_t* counts_dev, int32_t* err_dev, void* stream) {
+                                    dz_job* jobs_dev, int32_t* counts_dev, int32_t* err_dev,
+                                    int32_t sparse_job_tokens, void* stream) {
+  const int sp_chunk = sparse_job_tokens == 0 ? 8 : sparse_job_tokens;
   if (T < 0 || n_slots < 1 || n_slots > 4096 || !counts_dev || !err_dev) return DZ_E_VALUE;
+  if (sp_chunk != 8 && sp_chunk != 16) return DZ_E_VALUE;
   if (T > 0 && (!slots_dev || !perm_dev || !order_dev || !jobs_dev || !kinds_dev)) return DZ_E_VALUE;
   const size_t smem = static_cast<size_t>(5) * n_slots * sizeof(int);
   static std::once_flag once;  // one-time, idempotent kernel attribute setup
@@ -232,6 +238,6 @@ extern "C" int dz_plan_mixed_device(const int32_t* slots_dev, int32_t T, const i
     cudaFuncSetAttribute(plan::k_plan_mixed, cudaFuncAttributeMaxDynamicSharedMemorySize, 5 * 4096 * 4);
   });
   plan::k_plan_mixed<<<1, 1024, smem, static_cast<cudaStream_t>(stream)>>>(
-      slots_dev, T, kinds_dev, n_slots, with_base, pf_min, perm_dev, order_dev, jobs_dev, counts_dev, err_dev);
+      slots_dev, T, kinds_dev, n_slots, with_base, pf_min, perm_dev, order_dev, jobs_dev, counts_dev, err_dev, sp_chunk);
   return cudaGetLastError() == cudaSuccess ? DZ_OK : DZ_E_CUDA;
 }

@@ -98,14 +98,16 @@ constexpr int UMMA_M = 128;
 #define DZ_BASE_CH 2
 #endif
 constexpr int NB_SP = DZ_NB_SP;           // sparse chunk = 4 blocks = 512 columns (one 3-D TMA box)
-constexpr int NT_SP = 1;                  // n-tiles per sparse job (8 tokens, dz_plan)
+constexpr int NT_SP = DZ_SPARSE_JOB_TOKENS / 8;  // most n-tiles per 2:4 job (dz_plan): the codes of a
+                                                 // chunk are decoded once for all of the job's tokens
 constexpr int NT_DN = 4;                  // n-tiles per dense-delta job (32 tokens, dz_plan)
 constexpr int KC_DN = 64;                 // dense / base chunk = 64 columns
 constexpr int BASE_N = DZ_BASE_JOB_TOKENS; // tokens per base job == UMMA N (dz_plan)
 constexpr int XS_SP = NB_SP * kBlkCols * 2 + 16;  // smem bytes per staged token row; +16 B so the
 constexpr int XS_DN = KC_DN * 2 + 16;             //   8 rows of an ldmatrix hit distinct banks
 constexpr int A_SP = RG * NB_SP * sparse_block_bytes(4);  // 53248
-constexpr int X_SP = NT_SP * 8 * XS_SP;                   // 8320
+template <int NTS>
+constexpr int x_sp() { return NTS * 8 * XS_SP; }          // 8320 per 8 tokens
 constexpr int DN_HALF = kDenseBlockBytes / 2;             // 2048
 constexpr int A_DN = RG * DN_HALF;                        // 32768 == 256 rows x 128 B (base W tile)
 constexpr int X_DN = 64 * XS_DN;                          // 9216 (>= 64 x 128 B swizzled X tile)
@@ -116,7 +118,12 @@ constexpr int BASE_RT = UMMA_M;           // rows per base item: one UMMA M tile
 constexpr int BASE_CH = DZ_BASE_CH;             // 64-column K-chunks per base stage (32 KB of W in flight per stage)
 constexpr int TMEM_COLS = 2 * BASE_N;     // double-buffered fp32 accumulator, 128 lanes x 128 tokens
 constexpr uint32_t IDESC_BASE = umma_idesc_bf16(UMMA_M, BASE_N);
-constexpr int STAGE_BYTES = (cmax(cmax(A_SP + X_SP, A_DN + X_DN), A_DN + BASE_CH * KC_DN * BASE_N * 2) + 1023) / 1024 * 1024;
+// Stage size of the instantiation for 2:4 jobs of up to NTS n-tiles (X rows staged per stage).
+template <int NTS>
+constexpr int stage_bytes() {
+  return (cmax(cmax(A_SP + x_sp<NTS>(), A_DN + X_DN), A_DN + BASE_CH * KC_DN * BASE_N * 2) + 1023) / 1024 * 1024;
+}
+constexpr int STAGE_BYTES = stage_bytes<1>();
 constexpr int PF_CHUNKS = 4;              // stages of the first item prefetched into L2 before the PDL wait
 // Workspace: [0, 256) scheduler words; [256, +4*MAX_SLICES) per-32-row-slice arrival counters;
 // then the fp32 partial planes [base K-splits + delta K-splits][T][out].
@@ -149,7 +156,9 @@ struct Smem {
   int recs[4][36];                  // MergeRec ring (fused merge)
   int comb_tok[32];                 // the combiner's current token list
 };
-constexpr int SMEM_BYTES = 1024 + STAGE_BYTES * NSTAGE + static_cast<int>(sizeof(Smem));
+template <int NTS>
+constexpr int smem_bytes() { return 1024 + stage_bytes<NTS>() * NSTAGE + static_cast<int>(sizeof(Smem)); }
+constexpr int SMEM_BYTES = smem_bytes<1>();
 
 __device__ __forceinline__ bool kind_dense(int kind) { return kind == 0 || kind == DZ_KIND_DENSE; }
 
@@ -259,10 +268,10 @@ constexpr bool kOnesMma = DZ_ONES_MMA != 0;
 #ifndef DZ_PAIR
 #define DZ_PAIR 2
 #endif
-constexpr int PAIR = DZ_PAIR;
+constexpr int PAIR1 = DZ_PAIR;  // blocks per sparse_pair call at one n-tile
 // FULL: both blocks and all MR row groups valid -> no guards, straight-line code the compiler can
 // interleave (the common case); otherwise guarded (tail chunk / tail row tile).
-template <int FB, int NT, bool FULL>
+template <int FB, int NT, bool FULL, int PAIR>
 __device__ __forceinline__ void sparse_pair(float (&acc)[MR][NT_DN][4], uint32_t sA, uint32_t xl, int b0, int nb,
                                             int nrv, uint32_t off2, int lane) {
   const float offf = __uint_as_float((off2 & 0xFFFFu) << 16);  // 128 + qmax
@@ -352,16 +361,19 @@ __device__ __forceinline__ void sparse_pair(float (&acc)[MR][NT_DN][4], uint32_t
 template <int FB, int NT>
 __device__ __forceinline__ void sparse_chunk(float (&acc)[MR][NT_DN][4], uint32_t sA, uint32_t xl, int nb,
                                              int nrv, uint32_t off2, int lane) {
+  // blocks per call: 2 at one n-tile (8 independent mma.sp chains per warp), 1 at more n-tiles
+  // (the same chain count from the extra n-tiles' accumulators)
+  constexpr int PAIR = NT == 1 ? PAIR1 : 1;
   if (nb == NB_SP && nrv == MR) {
 #if DZ_PAIR_UNROLL
 #pragma unroll
 #else
 #pragma unroll 1
 #endif
-    for (int b0 = 0; b0 < NB_SP; b0 += PAIR) sparse_pair<FB, NT, true>(acc, sA, xl, b0, nb, nrv, off2, lane);
+    for (int b0 = 0; b0 < NB_SP; b0 += PAIR) sparse_pair<FB, NT, true, PAIR>(acc, sA, xl, b0, nb, nrv, off2, lane);
   } else {
 #pragma unroll 1
-    for (int b0 = 0; b0 < nb; b0 += PAIR) sparse_pair<FB, NT, false>(acc, sA, xl, b0, nb, nrv, off2, lane);
+    for (int b0 = 0; b0 < nb; b0 += PAIR) sparse_pair<FB, NT, false, PAIR>(acc, sA, xl, b0, nb, nrv, off2, lane);
   }
 }
 
@@ -805,10 +817,11 @@ __device__ __forceinline__ int job_items(const dz_sbmm_args& a, int n_jobs, int 
 // ------------------------------------------------------------------------------------------
 // The persistent kernel
 // ------------------------------------------------------------------------------------------
-template <bool FUSED>
+template <bool FUSED, int NTS>
 __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
     k_sbmm(const __grid_constant__ dz_sbmm_args a, const __grid_constant__ CUtensorMap xmap) {
   extern __shared__ uint8_t smem_dyn[];
+  constexpr int STAGE_BYTES = stage_bytes<NTS>();
   // 1024-B alignment for the SWIZZLE_128B tiles
   uint8_t* stages = smem_dyn + ((1024 - (smem_u32(smem_dyn) & 1023)) & 1023);
   Smem* sm = reinterpret_cast<Smem*>(stages + STAGE_BYTES * NSTAGE);
@@ -1118,7 +1131,7 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
     griddep_wait();  // Y / merge slots may still be in use by the preceding kernel
     int trace_i = 0;
     (void)trace_i;
-    float acc[MR][NT_DN][4];  // dense deltas use all NT_DN tiles, sparse deltas the first NT_SP
+    float acc[MR][NT_DN][4];  // dense deltas use all NT_DN tiles, sparse deltas the first NTS
     int stage = 0;
     uint32_t phase = 0;
     int nbase = 0;
@@ -1153,19 +1166,28 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
             const uint32_t off2 = off | (off << 16);
             if (h.kind != DZ_KIND_SPARSE2) {
               const uint32_t sA = sbuf + warp * MR * NB_SP * sparse_block_bytes(4);
-              sparse_chunk<4, NT_SP>(acc, sA, xl, h.nb, nrv, off2, lane);
+              if (NTS == 1 || nt <= 1)
+                sparse_chunk<4, 1>(acc, sA, xl, h.nb, nrv, off2, lane);
+              else
+                sparse_chunk<4, NTS>(acc, sA, xl, h.nb, nrv, off2, lane);
             } else {
               const uint32_t sA = sbuf + warp * MR * NB_SP * sparse_block_bytes(2);
-              sparse_chunk<2, NT_SP>(acc, sA, xl, h.nb, nrv, off2, lane);
+              if (NTS == 1 || nt <= 1)
+                sparse_chunk<2, 1>(acc, sA, xl, h.nb, nrv, off2, lane);
+              else
+                sparse_chunk<2, NTS>(acc, sA, xl, h.nb, nrv, off2, lane);
             }
           }
         }
       }
-      int tk0 = 0, tk1 = 0;  // this lane's token ids (sparse/dense-delta epilogue), read before release
+      int tkn[NTS][2] = {};  // this lane's token ids per n-tile (sparse epilogue), read before release
       if ((h.flags & 2) && !is_base) {
         const int t2 = 2 * (lane & 3);
-        if (t2 < h.tok_count) tk0 = sm->tok_ids[stage][t2];
-        if (t2 + 1 < h.tok_count) tk1 = sm->tok_ids[stage][t2 + 1];
+#pragma unroll
+        for (int n = 0; n < NTS; n++) {
+          if (8 * n + t2 < h.tok_count) tkn[n][0] = sm->tok_ids[stage][8 * n + t2];
+          if (8 * n + t2 + 1 < h.tok_count) tkn[n][1] = sm->tok_ids[stage][8 * n + t2 + 1];
+        }
       }
       if ((h.flags & 2) && h.kind == DZ_KIND_DENSE && nrv > 0)  // rare path: needs the stage's token list
         merge_fragments(acc, nt, mctx, nsplit + h.pad, rg0, h.tok_count, sm->tok_ids[stage], lane);
@@ -1189,22 +1211,26 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
           nbase++;
         } else if (nrv > 0 && h.kind != DZ_KIND_DENSE) {
           const int g = lane >> 2, t2 = 2 * (lane & 3);
-          int tk[4 * MR], rw[4 * MR];
-          float x[4 * MR];
-          bool ok[4 * MR];
 #pragma unroll
-          for (int r = 0; r < MR; r++) {
-            const int row = (rg0 + r) * kBlkRows + g;
+          for (int n = 0; n < NTS; n++) {
+            if (8 * n >= h.tok_count) break;
+            int tk[4 * MR], rw[4 * MR];
+            float x[4 * MR];
+            bool ok[4 * MR];
 #pragma unroll
-            for (int v = 0; v < 4; v++) {  // fragment: v&1 -> token t2 / t2+1, v&2 -> row +8
-              const int i = 4 * r + v;
-              tk[i] = (v & 1) ? tk1 : tk0;
-              rw[i] = row + ((v & 2) ? 8 : 0);
-              x[i] = acc[r][0][v];
-              ok[i] = r < nrv && t2 + (v & 1) < h.tok_count && rw[i] < a.out;
+            for (int r = 0; r < MR; r++) {
+              const int row = (rg0 + r) * kBlkRows + g;
+#pragma unroll
+              for (int v = 0; v < 4; v++) {  // fragment: v&1 -> token t2 / t2+1, v&2 -> row +8
+                const int i = 4 * r + v;
+                tk[i] = tkn[n][v & 1];
+                rw[i] = row + ((v & 2) ? 8 : 0);
+                x[i] = acc[r][n][v];
+                ok[i] = r < nrv && 8 * n + t2 + (v & 1) < h.tok_count && rw[i] < a.out;
+              }
             }
+            merge_batch<4 * MR>(mctx, nsplit + h.pad, tk, rw, x, ok);
           }
-          merge_batch<4 * MR>(mctx, nsplit + h.pad, tk, rw, x, ok);
         }
         if (mctx.fused) {  // hand the item to the combiner warp (no wait on any round trip)
           publish_item(recs, sm->mfull, sm->mempty, nmerge, warp, lane, h.rt, is_base ? 1 : 0, is_base ? 0 : h.tok_count,
@@ -1228,10 +1254,11 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
 
 using namespace dz;
 
-static_assert(A_DN + BASE_CH * KC_DN * BASE_N * 2 <= STAGE_BYTES && BASE_CH * BASE_RT * KC_DN * 2 <= A_DN,
+static_assert(A_DN + BASE_CH * KC_DN * BASE_N * 2 <= stage_bytes<1>() && BASE_CH * BASE_RT * KC_DN * 2 <= A_DN,
               "base stage layout");
-static_assert(NB_SP % PAIR == 0, "sparse stages hold whole block pairs");
-static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
+static_assert(NB_SP % PAIR1 == 0, "sparse stages hold whole block pairs");
+static_assert(DZ_SPARSE_JOB_TOKENS % 8 == 0 && NT_SP >= 1 && NT_SP <= NT_DN, "2:4 job = whole n-tiles");
+static_assert(smem_bytes<NT_SP>() <= 232448, "shared memory per CTA");
 static_assert(sizeof(MergeRec) == 36 * sizeof(int) && MREC == 4, "MergeRec ring layout in Smem");
 static_assert(NW == 8 && MR == 2, "8 consumer warps of 32 rows (one 32-row output slice each)");
 static_assert(sizeof(dz_native_delta) == 192, "dz_native_delta must be 192 bytes");
@@ -1291,24 +1318,24 @@ extern "C" size_t dz_sbmm_workspace_bytes(int32_t T, int32_t out) {
 
 extern "C" int dz_sbmm_diag(int* v) {  // numRegs, static smem, dynamic smem, max threads, localBytes
   cudaFuncAttributes fa;
-  if (cudaFuncGetAttributes(&fa, k_sbmm<false>) != cudaSuccess) return -1;
+  if (cudaFuncGetAttributes(&fa, k_sbmm<false, 1>) != cudaSuccess) return -1;
   v[0] = fa.numRegs; v[1] = static_cast<int>(fa.sharedSizeBytes); v[2] = SMEM_BYTES;
   v[3] = fa.maxThreadsPerBlock; v[4] = static_cast<int>(fa.localSizeBytes);
   size_t avail = 0;
-  cudaFuncSetAttribute(k_sbmm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  cudaOccupancyAvailableDynamicSMemPerBlock(&avail, k_sbmm<false>, 2, NTHREADS);
+  cudaFuncSetAttribute(k_sbmm<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaOccupancyAvailableDynamicSMemPerBlock(&avail, k_sbmm<false, 1>, 2, NTHREADS);
   v[5] = static_cast<int>(avail);
-  cudaFuncSetAttribute(k_sbmm<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(k_sbmm<false, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_sbmm<false>, NTHREADS, SMEM_BYTES);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_sbmm<false, 1>, NTHREADS, SMEM_BYTES);
   v[6] = n;
   return 0;
 }
 
 extern "C" int dz_sbmm_ctas_per_sm(void) {
   int n = 0;
-  if (cudaFuncSetAttribute(k_sbmm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess) return -1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_sbmm<false>, NTHREADS, SMEM_BYTES) != cudaSuccess) return -1;
+  if (cudaFuncSetAttribute(k_sbmm<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) != cudaSuccess) return -1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_sbmm<false, 1>, NTHREADS, SMEM_BYTES) != cudaSuccess) return -1;
   return n;
 }
 
@@ -1330,11 +1357,17 @@ static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
   static cudaError_t attr_err = cudaSuccess;
   static int ctas_per_sm = 1;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(k_sbmm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    attr_err = cudaFuncSetAttribute(k_sbmm<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<1>());
     if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(k_sbmm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+      attr_err = cudaFuncSetAttribute(k_sbmm<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<1>());
     if (attr_err == cudaSuccess)
-      attr_err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, k_sbmm<false>, NTHREADS, SMEM_BYTES);
+      attr_err = cudaFuncSetAttribute(k_sbmm<false, NT_SP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      smem_bytes<NT_SP>());
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(k_sbmm<true, NT_SP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      smem_bytes<NT_SP>());
+    if (attr_err == cudaSuccess)
+      attr_err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, k_sbmm<false, 1>, NTHREADS, SMEM_BYTES);
     if (ctas_per_sm < 1) ctas_per_sm = 1;
   });
   if (attr_err != cudaSuccess) return DZ_E_CUDA;
@@ -1353,8 +1386,14 @@ static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
   const int n_items = ceil_div(a->out, RT) * a->n_jobs * a->delta_splits +
                       ceil_div(a->out, BASE_RT) * a->base_splits * ceil_div(a->T, BASE_N);
   if (grid > n_items) grid = n_items;
-  st = fused ? launch_pdl(1, k_sbmm<true>, grid, nthreads<true>(), SMEM_BYTES, stream, *a, xmap)
-              : launch_pdl(1, k_sbmm<false>, grid, NTHREADS, SMEM_BYTES, stream, *a, xmap);
+  // the narrow instantiation when the plan's 2:4 jobs have <= 8 tokens (a smaller X stage)
+  const bool narrow = a->sparse_job_tokens == 8;
+  if (fused)
+    st = narrow ? launch_pdl(1, k_sbmm<true, 1>, grid, nthreads<true>(), smem_bytes<1>(), stream, *a, xmap)
+                : launch_pdl(1, k_sbmm<true, NT_SP>, grid, nthreads<true>(), smem_bytes<NT_SP>(), stream, *a, xmap);
+  else
+    st = narrow ? launch_pdl(1, k_sbmm<false, 1>, grid, NTHREADS, smem_bytes<1>(), stream, *a, xmap)
+                : launch_pdl(1, k_sbmm<false, NT_SP>, grid, NTHREADS, smem_bytes<NT_SP>(), stream, *a, xmap);
   if (st || fused || a->base == nullptr || (a->debug & 4)) return st;
   const float* part = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(a->workspace) + DZ_WS_PART_OFF);
   if (tp)  // row-parallel shard: fused reduction over peer memory

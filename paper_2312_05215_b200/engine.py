@@ -162,10 +162,15 @@ class Plan:
     (permuted) copy of X and the remaining tokens are planned for K2 (dz_plan_mixed)."""
 
     def __init__(self, slots, kinds: np.ndarray, n_slots: int, with_base: bool = True, device=None,
-                 upload: bool = True, pf_min: int | None = None):
+                 upload: bool = True, pf_min: int | None = None, sparse_job_tokens: int | None = None):
         s = np.ascontiguousarray(np.asarray(slots, dtype=np.int32).ravel())
         self.T = int(s.size)
         lib = L.lib()
+        if sparse_job_tokens is None:  # 16-token 2:4 jobs (decode each chunk once per 16 tokens) when
+            # some group is wider than 8 tokens; results do not depend on the width
+            cnt = np.bincount(s, minlength=max(n_slots, 1)) if s.size and s.min() >= 0 else np.zeros(1, int)
+            sparse_job_tokens = 16 if cnt.max(initial=0) > 8 else 8
+        self.sparse_job_tokens = int(sparse_job_tokens)
         maxj = lib.dz_plan_max_jobs(self.T)
         order = np.zeros(max(self.T, 1), dtype=np.int32)
         perm = np.zeros(max(self.T, 1), dtype=np.int32)
@@ -175,7 +180,7 @@ class Plan:
         self.pf_min = PF_MIN if pf_min is None else int(pf_min)
         st = lib.dz_plan_mixed(s.ctypes.data, self.T, kinds.ctypes.data, n_slots, 1 if with_base else 0,
                                self.pf_min, perm.ctypes.data, order.ctypes.data, jobs, maxj, C.byref(nj),
-                               C.byref(npf), C.byref(tpf))
+                               C.byref(npf), C.byref(tpf), self.sparse_job_tokens)
         if st == L.DZ_E_UNKNOWN:
             raise UnknownDeltaError("a token references a slot outside the delta table")
         L.check(st, "plan")
@@ -207,10 +212,11 @@ class DevicePlan:
     counts (prefill jobs, decode jobs, staged prefill rows) stay on the device."""
 
     def __init__(self, T: int, kinds: np.ndarray, n_slots: int, with_base: bool = True, device=None,
-                 mixed: bool = False, pf_min: int | None = None):
+                 mixed: bool = False, pf_min: int | None = None, sparse_job_tokens: int = 16):
         dev = device or require_cuda()
         lib = L.lib()
         self.T, self.n_slots, self.with_base, self.mixed = int(T), int(n_slots), with_base, mixed
+        self.sparse_job_tokens = int(sparse_job_tokens)  # 8: the narrow kernel, for decode-only batches
         self.pf_min = (PF_MIN if pf_min is None else int(pf_min)) if mixed else 0
         self.kinds_dev = torch.from_numpy(np.ascontiguousarray(kinds, dtype=np.int32)).to(dev)
         self.max_jobs = int(lib.dz_plan_max_jobs(self.T))
@@ -232,12 +238,13 @@ class DevicePlan:
             L.check(lib.dz_plan_mixed_device(slots_dev.data_ptr(), self.T, self.kinds_dev.data_ptr(), self.n_slots,
                                              1 if self.with_base else 0, self.pf_min, self.perm.data_ptr(),
                                              self.order.data_ptr(), self.jobs.data_ptr(), self.counts.data_ptr(),
-                                             self.err.data_ptr(), stream_ptr()), "device mixed plan")
+                                             self.err.data_ptr(), self.sparse_job_tokens, stream_ptr()),
+                    "device mixed plan")
         else:
             L.check(lib.dz_plan_device(slots_dev.data_ptr(), self.T, self.kinds_dev.data_ptr(), self.n_slots,
                                        1 if self.with_base else 0, self.order.data_ptr(), self.jobs.data_ptr(),
                                        self.max_jobs, self.n_jobs_dev.data_ptr(), self.err.data_ptr(),
-                                       stream_ptr()), "device plan")
+                                       self.sparse_job_tokens, stream_ptr()), "device plan")
         return self
 
     def check(self) -> None:
@@ -397,6 +404,7 @@ def sbmm_args(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: Delta
     a.workspace = ws.data_ptr()
     a.grid = grid
     a.debug = debug
+    a.sparse_job_tokens = plan.sparse_job_tokens  # selects the kernel instantiation (X stage size)
     a.base_splits = base_splits  # 0 = by shape (batch-independent); 1..4 = explicit K-splits of the base
     a.delta_splits = delta_splits  # 0 = by shape; 1..2 = explicit K-splits of each decode delta job
     if tp is not None:  # peer.PeerGroup: row-parallel shard, reduced over peer memory by the finalize

@@ -23,19 +23,19 @@ int main(int argc, char** argv) {
   int32_t slots[4] = {2, 0, 2, 1}, kinds[3] = {DZ_KIND_SPARSE4, DZ_KIND_SPARSE4, DZ_KIND_SPARSE4};
   int32_t order[4], n_jobs = 0;
   dz_job jobs[16];
-  CHECK(dz_plan(slots, 4, kinds, 3, 1, order, jobs, dz_plan_max_jobs(4), &n_jobs) == DZ_OK);
+  CHECK(dz_plan(slots, 4, kinds, 3, 1, order, jobs, dz_plan_max_jobs(4), &n_jobs, 8) == DZ_OK);
   CHECK(n_jobs == 4 && order[0] == 1 && order[1] == 3 && order[2] == 0 && order[3] == 2);
   CHECK(jobs[0].slot == -1 && jobs[0].tok_count == 4 && jobs[3].slot == 2 && jobs[3].tok_count == 2);
   printf("plan ok: %d jobs\n", n_jobs);
   int32_t bad[2] = {0, 7};
-  CHECK(dz_plan(bad, 2, kinds, 3, 1, order, jobs, 16, &n_jobs) == DZ_E_UNKNOWN);
+  CHECK(dz_plan(bad, 2, kinds, 3, 1, order, jobs, 16, &n_jobs, 8) == DZ_E_UNKNOWN);
   printf("unknown slot -> %s\n", dz_strerror(DZ_E_UNKNOWN));
   /* mixed plan: 300 tokens on slot 0 -> two prefill jobs of equal 16-aligned size (160 + 140) */
   int32_t T = 300 + 5, *s2 = malloc(sizeof(int32_t) * T), *perm = malloc(sizeof(int32_t) * T);
   int32_t *ord2 = malloc(sizeof(int32_t) * T), n_pf = 0, t_pf = 0;
   dz_job* jobs2 = malloc(sizeof(dz_job) * dz_plan_max_jobs(T));
   for (int i = 0; i < T; i++) s2[i] = i < 300 ? 0 : 1;
-  CHECK(dz_plan_mixed(s2, T, kinds, 3, 1, 192, perm, ord2, jobs2, dz_plan_max_jobs(T), &n_jobs, &n_pf, &t_pf) ==
+  CHECK(dz_plan_mixed(s2, T, kinds, 3, 1, 192, perm, ord2, jobs2, dz_plan_max_jobs(T), &n_jobs, &n_pf, &t_pf, 8) ==
         DZ_OK);
   CHECK(t_pf == 300 && n_pf == 2 && jobs2[0].tok_count == 160 && jobs2[1].tok_count == 140);
   printf("mixed plan ok: %d prefill rows, %d jobs\n", t_pf, n_jobs);

@@ -69,7 +69,7 @@ def _plan(lib, slots, kinds, with_base=1):
     order = np.zeros(max(T, 1), np.int32)
     jobs = (_lib.DzJob * max(maxj, 1))()
     nj = C.c_int32(0)
-    st = lib.dz_plan(s.ctypes.data, T, k.ctypes.data, k.size, with_base, order.ctypes.data, jobs, maxj, C.byref(nj))
+    st = lib.dz_plan(s.ctypes.data, T, k.ctypes.data, k.size, with_base, order.ctypes.data, jobs, maxj, C.byref(nj), 8)
     return st, order[:T], [(jobs[i].slot, jobs[i].tok_begin, jobs[i].tok_count, jobs[i].kind) for i in range(nj.value)]
 
 
@@ -194,7 +194,7 @@ def test_plan_mixed_prefill_decode_host_logic():
                 covered += rows.tolist()
             elif slot >= 0:
                 rows = perm[p.order_host[b:b + c]]
-                assert np.all(ids[rows] == slot) and c <= (32 if kind == 3 else 8)
+                assert np.all(ids[rows] == slot) and c <= (32 if kind == 3 else _header_define("DZ_SPARSE_JOB_TOKENS"))
                 covered += rows.tolist()
             else:
                 assert b >= p.t_pf and c <= 128
