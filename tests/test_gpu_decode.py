@@ -129,3 +129,32 @@ def test_fused_merge_matches_finalize_launch(E, rows, cols, D, T, bits):
     buf = ws.get(1, 1, X.device)
     torch.cuda.synchronize()
     assert int(buf[256: 256 + 4 * 8192].count_nonzero()) == 0  # slice counters re-armed
+
+
+@pytest.mark.parametrize("bits", [4, 2, 3])
+def test_sparse_job_width_does_not_change_results(E, bits):
+    """8- and 16-token 2:4 jobs (the narrow and the wide kernel instantiation, host and device plans)
+    give bit-identical results: the n-tiles of a job are independent MMA columns with the same K
+    order, so the plan's automatic width choice (it depends on the batch) keeps batch invariance."""
+    rng = np.random.default_rng(40 + bits)
+    rows, cols, D = 520, 640, 4
+    ods = [O.random_packed_delta(rng, rows, cols, bits) for _ in range(D)]
+    table = E.DeltaTable([E.NativeDelta.from_layer_delta(o) for o in ods], rows, cols)
+    base = E.NativeBase((torch.randn(rows, cols, device="cuda") / np.sqrt(cols)).to(torch.bfloat16))
+    ids = np.concatenate([np.zeros(37, np.int32), rng.integers(1, D, 21).astype(np.int32)])
+    ids = ids[rng.permutation(ids.size)]
+    X = torch.randn(ids.size, cols, device="cuda").to(torch.bfloat16)
+    ys = [E.sbmm_forward(X, E.Plan(ids, table.kinds, D, sparse_job_tokens=w), base, table, y_dtype=torch.float32)
+          for w in (8, 16)]
+    dp = E.DevicePlan(ids.size, table.kinds, D, sparse_job_tokens=16).update(torch.from_numpy(ids).cuda())
+    ys.append(E.sbmm_forward(X, dp, base, table, y_dtype=torch.float32))
+    assert E.Plan(ids, table.kinds, D).sparse_job_tokens == 16  # a 37-token group: wide jobs
+    assert torch.equal(ys[0], ys[1]) and torch.equal(ys[0], ys[2])
+    # a solo row equals its row in the batch
+    i = int(np.nonzero(ids == 0)[0][5])
+    solo = E.sbmm_forward(X[i:i + 1].contiguous(), E.Plan(ids[i:i + 1], table.kinds, D), base, table,
+                          y_dtype=torch.float32)
+    assert torch.equal(solo[0], ys[1][i])
+    R = O.sbmm_matrix(base.W.float().double().cpu().numpy(), dict(enumerate(ods)), ids, X.float().double().cpu().numpy())
+    err = (np.linalg.norm(ys[1].double().cpu().numpy() - R, axis=1) / np.linalg.norm(R, axis=1)).max()
+    assert err <= 1e-2
