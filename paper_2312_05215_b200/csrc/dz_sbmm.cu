@@ -185,22 +185,25 @@ __device__ __forceinline__ void item_coords(int item, int nrt, int nbt, int nspl
   }
 }
 
-// Default base K-splits when the caller passes 0: one (the BASELINE decode step, T=64 with 32 deltas:
-// 3743 tok/s at 1 split, 3714 at 2, 3578 at 4 with the fused merge; profiles/r02_ab_fused_splits.txt).
-// Low-batch serving gains from more base items, which a deployment selects through
-// dz_sbmm_args.base_splits. The split count is never derived from the batch, so a token's result
-// does not depend on the other tokens of the call.
+// Default base K-splits when the caller passes 0 (DZ_SPLIT_RULE 2): two for layers of <= 4096 output
+// rows (o / down at 7B: 32 base tiles of 1 MB each; two K-halves bring a base item near a delta
+// item's size and give a low batch twice the base items), one otherwise. Same box
+// (profiles/r02_ab_split_rule2.txt): cfg5 batch 1-8 +16-19%, the headline step -0.4%. Rule 1 (up
+// to 4 splits for every shape) gave +3..39% at low batch but -2.5% on the headline
+// (profiles/r02_ab_split_rule.txt). A deployment can still pass dz_sbmm_args.base_splits. The split
+// count is never derived from the batch, so a token's result does not depend on the other tokens.
 #ifndef DZ_DEFAULT_BASE_SPLITS
 #define DZ_DEFAULT_BASE_SPLITS 1
 #endif
 #ifndef DZ_SPLIT_RULE
-#define DZ_SPLIT_RULE 0
+#define DZ_SPLIT_RULE 2  // 0: DZ_DEFAULT_BASE_SPLITS everywhere; 1: enough items for 148 SMs; 2: see above
 #endif
 __host__ __device__ inline int base_splits(int out, int /*in*/) {
-  if (DZ_SPLIT_RULE) {  // enough base items for every SM of a B200 (148): shape-keyed, never batch-keyed
+  if (DZ_SPLIT_RULE == 1) {  // enough base items for every SM of a B200 (148): shape-keyed, never batch-keyed
     const int nbt = (out + 127) / 128, s = (148 + nbt - 1) / nbt;
     return s > 4 ? 4 : s;
   }
+  if (DZ_SPLIT_RULE == 2) return out <= 4096 ? 2 : 1;  // base items of the narrow layers ~ delta-item size
   return DZ_DEFAULT_BASE_SPLITS;
 }
 // Default K-splits of each decode delta job: 1. Splitting the delta items of the out <= 4096 layers

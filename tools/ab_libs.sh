@@ -1,7 +1,7 @@
 #!/bin/bash
 # A/B of library variants on the default bench: tools/ab_libs.sh name1 name2 ... ("base" = _dz_b200.so)
 mkdir -p gpurun_out
-for rep in 1 2; do
+for rep in $(seq 1 ${REPS:-2}); do
 for v in "$@"; do
   if [ "$v" = base ]; then unset DZ_B200_LIB; else export DZ_B200_LIB=$PWD/paper_2312_05215_b200/_dz_b200_$v.so; fi
   timeout 600 python bench.py --quick --no-e2e --steps 10 --warmup 3 > gpurun_out/ab_$v.txt 2>&1
