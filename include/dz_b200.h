@@ -40,8 +40,10 @@ extern "C" {
                                     the planners take the job width (8 or 16; 0 = 8) as an argument */
 #define DZ_DENSE_JOB_TOKENS 32   /* tokens per dense-delta job of the decode kernel */
 #ifndef DZ_PREFILL_JOB_TOKENS
-#define DZ_PREFILL_JOB_TOKENS 240 /* most tokens per prefill job of K3 (its UMMA N), multiple of 16;
-                                    a group is cut into ceil(c / 240) jobs of equal 16-aligned size */
+#define DZ_PREFILL_JOB_TOKENS 256 /* most tokens per prefill job of K3 (its UMMA N), multiple of 16;
+                                    a group is cut into ceil(c / 256) jobs of equal 16-aligned size
+                                    (256: one job per 256-token request, single-buffered TMEM
+                                    accumulator; profiles/r02_ab_prefill_jobs.txt) */
 #endif
 /* ---- element types --------------------------------------------------------------- */
 #define DZ_F32 0
@@ -239,10 +241,24 @@ int dz_plan(const int32_t* slots, int32_t T, const int32_t* kinds, int32_t n_slo
             int32_t* n_jobs_out, int32_t sparse_job_tokens);
 /* Tokens per prefill job of a c-token group: ceil(c / ceil(c / DZ_PREFILL_JOB_TOKENS)) rounded up
  * to 16 (the last job of the group takes the rest). */
+/* Prefill tokens of a c-token group (c >= pf_min): all of them, except that a remainder of fewer
+ * than DZ_PREFILL_REM_MIN tokens beyond whole jobs stays on the decode kernel (a few decode tokens
+ * of the request's delta would otherwise double its prefill jobs). 0 disables the rule. */
+#ifndef DZ_PREFILL_REM_MIN
+#define DZ_PREFILL_REM_MIN 32
+#endif
+#define DZ_PREFILL_TOKENS(c)                                                                      \
+  ((c) >= DZ_PREFILL_JOB_TOKENS && (c) % DZ_PREFILL_JOB_TOKENS < DZ_PREFILL_REM_MIN               \
+       ? (c) - (c) % DZ_PREFILL_JOB_TOKENS                                                        \
+       : (c))
+#ifdef DZ_PREFILL_GREEDY_CUT  /* A/B variant: full 240-token jobs, the remainder as one more job */
+#define DZ_PREFILL_JOB_SIZE(c) DZ_PREFILL_JOB_TOKENS
+#else
 #define DZ_PREFILL_JOB_SIZE(c)                                                                   \
   ((c) < 1 ? DZ_PREFILL_JOB_TOKENS                                                                \
            : ((((c) + ((c) + DZ_PREFILL_JOB_TOKENS - 1) / DZ_PREFILL_JOB_TOKENS - 1) /            \
                (((c) + DZ_PREFILL_JOB_TOKENS - 1) / DZ_PREFILL_JOB_TOKENS) + 15) / 16) * 16)
+#endif
 /* Mixed plan: delta groups of >= pf_min tokens (2:4 sparse kinds) go to K3 whole, cut into
  * ceil(c / DZ_PREFILL_JOB_TOKENS) jobs of DZ_PREFILL_JOB_SIZE(c) tokens (a 256-token request: 2 x 128),
  * staged first in perm (grouped by slot, stable); the remaining tokens

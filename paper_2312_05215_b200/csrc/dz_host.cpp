@@ -88,7 +88,7 @@ extern "C" int dz_plan_mixed(const int32_t* slots, int32_t T, const int32_t* kin
   for (int32_t t = 0; t < T; t++) count[slots[t]]++;
   std::vector<int32_t> npf(static_cast<size_t>(n_slots), 0);  // prefill tokens per slot
   for (int32_t s = 0; s < n_slots; s++)
-    if (pf_min > 0 && count[s] >= pf_min && kinds[s] != DZ_KIND_DENSE) npf[s] = count[s];
+    if (pf_min > 0 && count[s] >= pf_min && kinds[s] != DZ_KIND_DENSE) npf[s] = DZ_PREFILL_TOKENS(count[s]);
   // staged order: prefill groups by slot, then the decode tokens in original order
   std::vector<int32_t> pstart(static_cast<size_t>(n_slots) + 1, 0);
   for (int32_t s = 0; s < n_slots; s++) pstart[s + 1] = pstart[s] + npf[s];

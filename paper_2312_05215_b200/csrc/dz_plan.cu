@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(1024) k_plan_mixed(const int32_t* __restrict__
     int ps = 0, pj = 0;
     for (int s = 0; s < n_slots; s++) {
       const int c = count[s], k = kinds[s];
-      const int np = (pf_min > 0 && c >= pf_min && k != DZ_KIND_DENSE) ? c : 0;
+      const int np = (pf_min > 0 && c >= pf_min && k != DZ_KIND_DENSE) ? DZ_PREFILL_TOKENS(c) : 0;
       npf[s] = np;
       pstart[s] = ps;
       ps += np;

@@ -173,10 +173,12 @@ def test_plan_mixed_prefill_decode_host_logic():
         p = Plan(ids, kinds, D, upload=False, pf_min=64)
         T = ids.size
         cnt = np.bincount(ids, minlength=D)
-        J = _header_define("DZ_PREFILL_JOB_TOKENS")
+        J, RM = _header_define("DZ_PREFILL_JOB_TOKENS"), _header_define("DZ_PREFILL_REM_MIN")
 
-        def n_prefill(c):  # dz_plan_mixed's rule (pf_min = 64): the whole group
-            return c if c >= 64 else 0
+        def n_prefill(c):  # dz_plan_mixed's rule (pf_min = 64): the group, a small remainder left to K2
+            if c < 64:
+                return 0
+            return c - c % J if c >= J and c % J < RM else c
         npf = np.array([0 if kinds[s] == 3 else n_prefill(cnt[s]) for s in range(D)])
         assert p.t_pf == npf.sum()
         perm = p.perm_host if p.t_pf else np.arange(T)
@@ -187,8 +189,8 @@ def test_plan_mixed_prefill_decode_host_logic():
         covered = []
         for k, (slot, b, c, kind) in enumerate(jobs):
             if k < p.n_pf_jobs:
-                nj = -(-cnt[slot] // J)
-                assert 0 < c <= -(-(-(-cnt[slot] // nj)) // 16) * 16 <= J and kind == kinds[slot] and kind != 3
+                nj = -(-npf[slot] // J)
+                assert 0 < c <= -(-(-(-npf[slot] // nj)) // 16) * 16 <= J and kind == kinds[slot] and kind != 3
                 rows = perm[b:b + c]
                 assert np.all(ids[rows] == slot)
                 covered += rows.tolist()

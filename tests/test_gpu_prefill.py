@@ -140,7 +140,7 @@ def test_prefill_full_size(E, out_f, in_f, bits):
     ids = _ids(rng, [256, 256, 8, 8])
     X = torch.randn(ids.size, in_f, device="cuda").to(torch.bfloat16)
     plan = E.Plan(ids, table.kinds, D, pf_min=64)
-    assert plan.n_pf_jobs == 4 and plan.t_pf == 512  # each 256-token group: 2 jobs of 128
+    assert plan.n_pf_jobs == 2 and plan.t_pf == 512  # each 256-token group: one job
     Y = E.sbmm_forward(X, plan, base, table, y_dtype=torch.float32)
     R = X.float() @ Wt.float().T
     for d in range(D):

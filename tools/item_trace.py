@@ -35,8 +35,9 @@ e0.record()
 sbmm_forward(X, plan, base, table, workspace=ws)
 e1.record()
 torch.cuda.synchronize()
-n_base = 1  # T <= DZ_BASE_JOB_TOKENS: one base job, default base_splits 1
-n_items = ((out + 127) // 128) * n_base + ((out + 255) // 256) * (plan.n_jobs - n_base)
+n_base = 1  # T <= DZ_BASE_JOB_TOKENS: one base job
+nsplit = 2 if out <= 4096 else 1  # the default split rule (dz_sbmm.cu base_splits, DZ_SPLIT_RULE 2)
+n_items = ((out + 127) // 128) * n_base * nsplit + ((out + 255) // 256) * (plan.n_jobs - n_base)
 lib = L.lib()
 lib.dz_item_trace_read.argtypes = [C.c_void_p, C.c_int]
 buf = np.zeros((n_items, 3), dtype=np.uint64)
