@@ -490,6 +490,9 @@ def main():
         for k in range(2):  # warm: first-call host overheads outside the timed region
             e2e_step(k)
         torch.cuda.synchronize()
+        # the same starting point as the `value` block: the GPU idles briefly after the warm-up steps
+        # (a block that starts right after another runs a few percent lower under the power cap)
+        time.sleep(float(os.environ.get("DZ_BENCH_E2E_GAP", "1.0")))
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for k in range(args.steps):
