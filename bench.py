@@ -56,6 +56,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--quick", action="store_true", help="skip clocks sampler / cpu baseline (profiling runs)")
+    p.add_argument("--fused-merge", action="store_true", help="Y written inside k_sbmm (no k_finalize launch)")
     return p.parse_args()
 
 
@@ -335,6 +336,7 @@ def main():
 
     t_build = time.time()
     st = LlamaStack(MODEL, args.layers, D_DELTAS, BITS, device, rank=rank, world=world)
+    st.fused_merge = args.fused_merge
     fused_tp = world > 1 and os.environ.get("DZ_TP_FUSED", "1") == "1"
     if fused_tp:  # row-parallel outputs reduced over peer memory by the finalize kernel (no NCCL)
         st.enable_fused_tp(T_TOKENS)
@@ -534,7 +536,7 @@ def main():
                        if world > 1 else "single",
                        "l2": "inputs > L2 (97.5 GB streamed per step at N=1)", "cuda_graph": graph is not None,
                        "step_bytes_rank0": step_bytes},
-            "gpu_launches": 2 * len(order) * args.steps,  # k_sbmm + k_finalize per fused linear
+            "gpu_launches": (1 if args.fused_merge else 2) * len(order) * args.steps,  # k_sbmm (+ k_finalize) per fused linear
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_algorithmic": traffic_alg, "peak_kind": peak_kind,
                          "kernel": "k_sbmm (fused base GEMM + SBMM), all 4 x layers launches of one step (QKV, o, "

@@ -149,11 +149,11 @@ struct Smem {
   uint64_t tmem_full[2];
   uint64_t tmem_empty[2];
   StageHdr hdr[NSTAGE];
-  uint64_t mfull[4];       // consumer warps -> combiner: the item's partial planes are stored
-  uint64_t mempty[4];      // combiner -> consumers: the record slot may be reused
+  uint64_t mfull[8];       // consumer warps -> combiner: the item's partial planes are stored (MREC <= 8)
+  uint64_t mempty[8];      // combiner -> consumers: the record slot may be reused
   uint32_t tmem_base;
   int tok_ids[NSTAGE][JOB_DN_TOK];  // token ids of the item, staged with its last chunk
-  int recs[4][36];                  // MergeRec ring (fused merge)
+  int recs[8][36];                  // MergeRec ring (fused merge), MREC <= 8
   int comb_tok[32];                 // the combiner's current token list
 };
 template <int NTS>
@@ -660,7 +660,13 @@ __device__ __forceinline__ void tail_prefetch(const dz_sbmm_args& nx) {
 // summation order (deterministic, batch-invariant). A combiner only ever waits on base items,
 // which are first in the item order and never wait, so the persistent grid cannot deadlock; the
 // consumers never wait on a round trip.
-constexpr int MREC = 4;                   // records in flight (consumer warps -> combiner)
+#ifndef DZ_MREC
+#define DZ_MREC 4
+#endif
+#ifndef DZ_COMB_SLEEP
+#define DZ_COMB_SLEEP 32  // ns between polls of the record ring (the combiner shares an SMSP with consumers)
+#endif
+constexpr int MREC = DZ_MREC;             // records in flight (consumer warps -> combiner)
 struct MergeRec {
   int rt;        // row tile (base: 128-row tile, delta: 256-row tile); -1 = end of work
   int is_base;
@@ -1125,7 +1131,7 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
     if (mctx.fused) {
       mctx.readers = (a.n_jobs_dev != nullptr ? *a.n_jobs_dev : a.n_jobs) - n_base;  // delta jobs
       for (int k = 0;; k++) {
-        while (!mbar_test(&sm->mfull[k % MREC], (k / MREC) & 1)) __nanosleep(32);
+        while (!mbar_test(&sm->mfull[k % MREC], (k / MREC) & 1)) __nanosleep(DZ_COMB_SLEEP);
         if (!service_record(sm, mctx, k, lane)) break;
       }
     }
@@ -1262,7 +1268,7 @@ static_assert(A_DN + BASE_CH * KC_DN * BASE_N * 2 <= stage_bytes<1>() && BASE_CH
 static_assert(NB_SP % PAIR1 == 0, "sparse stages hold whole block pairs");
 static_assert(DZ_SPARSE_JOB_TOKENS % 8 == 0 && NT_SP >= 1 && NT_SP <= NT_DN, "2:4 job = whole n-tiles");
 static_assert(smem_bytes<NT_SP>() <= 232448, "shared memory per CTA");
-static_assert(sizeof(MergeRec) == 36 * sizeof(int) && MREC == 4, "MergeRec ring layout in Smem");
+static_assert(sizeof(MergeRec) == 36 * sizeof(int) && MREC <= 8, "MergeRec ring layout in Smem");
 static_assert(NW == 8 && MR == 2, "8 consumer warps of 32 rows (one 32-row output slice each)");
 static_assert(sizeof(dz_native_delta) == 192, "dz_native_delta must be 192 bytes");
 static_assert(offsetof(dz_native_delta, tmap) == 64, "tensor map must be 64-byte aligned in the entry");
