@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--quick", action="store_true", help="skip clocks sampler / cpu baseline (profiling runs)")
     p.add_argument("--fused-merge", action="store_true", help="Y written inside k_sbmm (no k_finalize launch)")
+    p.add_argument("--chain", action="store_true", help="the whole step as ONE chained launch (dz_sbmm_chain)")
+    p.add_argument("--chain-len", type=int, default=0, help="with --chain: linears per chained launch (0 = all)")
     return p.parse_args()
 
 
@@ -355,27 +357,30 @@ def main():
     if tail_pf:  # each launch warms L2 with the next launch's first weight stages at its tail
         st.prepare_chain(plan, bufs)
     stream = torch.cuda.current_stream()
+    chained = args.chain and world == 1
+    st.chain_len = args.chain_len
+    step_fn = (lambda p_: st.step_chained(p_, bufs)) if chained else (lambda p_: st.step(p_, bufs))
 
-    st.step(plan, bufs)  # eager warm-up (sets kernel attributes, NCCL communicators)
+    step_fn(plan)  # eager warm-up (sets kernel attributes, NCCL communicators)
     torch.cuda.synchronize()
     graph = None
     if not args.no_graph:
         s_ = torch.cuda.Stream()
         s_.wait_stream(stream)
         with torch.cuda.stream(s_):
-            st.step(plan, bufs)
+            step_fn(plan)
         stream.wait_stream(s_)
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            st.step(plan, bufs)
+            step_fn(plan)
         torch.cuda.synchronize()
 
     def run_step():
         if graph is not None:
             graph.replay()
         else:
-            st.step(plan, bufs)
+            step_fn(plan)
 
     for _ in range(args.warmup):
         run_step()

@@ -312,6 +312,21 @@ int dz_plan_mixed_device(const int32_t* slots_dev, int32_t T, const int32_t* kin
  * k_sbmm by a combiner warp (args.fused_merge = 1). Deterministic and batch-invariant:
  * a token's result does not depend on the other tokens in the call. */
 size_t dz_sbmm_workspace_bytes(int32_t T, int32_t out);
+/* Chained launch: the linears of a decode step (L <= 256, e.g. 4 per decoder layer) in ONE
+ * persistent kernel — the launches of dz_sbmm, back to back, without the launch boundaries: the
+ * items of linear l follow those of linear l-1 in one scheduler, each delta item's rows are
+ * merged and written by the CTA's combiner warp (the fused merge), and linear l's X loads wait
+ * until every Y row of linear l-1 is written (its weights stream ahead meanwhile). Linear l's
+ * input may be any earlier linear's output. Decode plans of single-GPU linears with a base, one
+ * shared workspace (sized for the widest linear), results bit-identical to fused_merge launches.
+ * dz_sbmm_chain_encode fills a host buffer (64-byte aligned, dz_sbmm_chain_desc_bytes) that the
+ * caller copies to device memory once; *narrow_out selects the kernel instantiation for
+ * dz_sbmm_chain (1 when every linear's plan has 8-token 2:4 jobs). All CTAs must be resident:
+ * grid <= SMs (0 = one per SM). */
+size_t dz_sbmm_chain_desc_bytes(int32_t L);
+int dz_sbmm_chain_encode(const dz_sbmm_args* args, int32_t L, void* desc_host, size_t desc_bytes,
+                         int32_t* narrow_out);
+int dz_sbmm_chain(const void* desc_dev, int32_t L, int32_t narrow, int32_t grid, void* stream);
 /* K3 — prefill SBMM (dz_prefill.cu), launched by dz_sbmm for the prefill jobs of a mixed plan:
  * per (128-row tile, <= 256-token group) one TMEM accumulator receives tcgen05 MMAs of the base
  * W tile and of the group's delta tile, dequantised (code * scale -> bf16) from native blocks

@@ -113,6 +113,9 @@ SIGNATURES = {
                                 C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                 C.POINTER(C.c_int32), C.c_int32]),
     "dz_sbmm_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int32]),
+    "dz_sbmm_chain_desc_bytes": (C.c_size_t, [C.c_int32]),
+    "dz_sbmm_chain_encode": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_size_t, C.POINTER(C.c_int32)]),
+    "dz_sbmm_chain": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
     "dz_sbmm_prefill": (C.c_int, [C.POINTER(DzSbmmArgs), C.c_void_p]),
     "dz_gather_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int64,
                                  C.c_void_p]),

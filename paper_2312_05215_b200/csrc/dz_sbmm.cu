@@ -43,6 +43,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "dz_common.cuh"
 #include "dz_tmap.h"
@@ -128,8 +129,10 @@ constexpr int PF_CHUNKS = 4;              // stages of the first item prefetched
 // Workspace: [0, 256) scheduler words; [256, +4*MAX_SLICES) per-32-row-slice arrival counters;
 // then the fp32 partial planes [base K-splits + delta K-splits][T][out].
 constexpr int MAX_SLICES = 8192;          // out <= 262144 rows per launch
+constexpr int MAX_CHAIN = 256;            // linears per chained launch
 constexpr int DZ_WS_CNT_OFF = 256;
-constexpr int DZ_WS_PART_OFF = DZ_WS_CNT_OFF + 4 * MAX_SLICES;
+constexpr int DZ_WS_CHAIN_OFF = DZ_WS_CNT_OFF + 4 * MAX_SLICES;  // [exit count][item counters][done counts]
+constexpr int DZ_WS_PART_OFF = DZ_WS_CHAIN_OFF + 4 * (1 + 2 * MAX_CHAIN) + 252;
 
 struct StageHdr {
   int item;       // -1: end of work
@@ -139,7 +142,8 @@ struct StageHdr {
   int tok_count;
   int nb;         // sparse: blocks in chunk; dense: 1
   int flags;      // bit0: first chunk, bit1: last chunk
-  int pad;
+  int pad;        // K-split of the item
+  int lin;        // linear of a chained launch (0 otherwise)
 };
 
 struct Smem {
@@ -671,7 +675,7 @@ struct MergeRec {
   int rt;        // row tile (base: 128-row tile, delta: 256-row tile); -1 = end of work
   int is_base;
   int ntok;      // delta: tokens of the job (<= 32)
-  int pad;
+  int lin;       // linear of a chained launch
   int tok[32];   // delta: the job's token (staged row) ids
 };
 
@@ -770,7 +774,7 @@ __device__ __noinline__ void combine_tokens(const MergeCtx m, int r0, int ntok, 
 // Consumer warp `warp` finished its plane stores of merged item #k: warp 0 fills the record, every
 // warp arrives (its lanes' stores, ordered by the warp barrier, precede the arrive's release).
 __device__ __forceinline__ void publish_item(MergeRec* recs, uint64_t* mfull, uint64_t* mempty, int k, int warp,
-                                             int lane, int rt, int is_base, int ntok, int rtok) {
+                                             int lane, int rt, int is_base, int ntok, int rtok, int lin = 0) {
   const int slot = k % MREC;
   mbar_wait(&mempty[slot], ((k / MREC) & 1) ^ 1);
   if (warp == 0) {
@@ -778,6 +782,7 @@ __device__ __forceinline__ void publish_item(MergeRec* recs, uint64_t* mfull, ui
       recs[slot].rt = rt;
       recs[slot].is_base = is_base;
       recs[slot].ntok = ntok;
+      recs[slot].lin = lin;
     }
     if (lane < ntok) recs[slot].tok[lane] = rtok;
   }
@@ -817,6 +822,78 @@ __device__ __forceinline__ bool service_record(Smem* sm, const MergeCtx& mctx, i
   return true;
 }
 
+// Per-linear constants of a launch, or of one linear of a chained launch.
+struct LinGeo {
+  int n16, nrt, nkb, nch_base, nbt, n_base, nsplit, dsplit;
+};
+__device__ __forceinline__ LinGeo lin_geo(const dz_sbmm_args& a) {
+  LinGeo g;
+  g.n16 = ceil_div(a.out, kBlkRows);
+  g.nrt = ceil_div(a.out, RT);
+  g.nkb = ceil_div(a.in, kBlkCols);
+  g.nch_base = ceil_div(a.in, BASE_CH * KC_DN);
+  g.nbt = ceil_div(a.out, BASE_RT);
+  int t_pf = a.t_pf;
+  if (a.pf_counts_dev != nullptr) {  // device mixed plan: the staged prefill rows come from the planner
+    griddep_wait();
+    t_pf = a.pf_counts_dev[2];
+  }
+  g.n_base = a.base != nullptr ? ceil_div(a.T - t_pf, BASE_N) : 0;  // dz_plan: base jobs first
+  g.nsplit = a.base_splits;   // resolved by the host (launch_decode / dz_sbmm_chain_encode)
+  g.dsplit = a.delta_splits;
+  return g;
+}
+
+template <bool FUSED>
+__device__ __forceinline__ MergeCtx make_mctx(const dz_sbmm_args& a, const LinGeo& g) {
+  MergeCtx m;
+  m.slice_cnt = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(a.workspace) + DZ_WS_CNT_OFF);
+  m.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(a.workspace) + DZ_WS_PART_OFF);
+  m.fused = FUSED && a.base != nullptr && !a.keep_planes && g.dsplit == 1 && !(a.debug & 6);
+  m.base_target = g.n_base * g.nsplit;  // base items publishing each slice
+  m.readers = 0;
+  m.T = a.T;
+  m.nsplit = g.nsplit;
+  m.perm = a.perm;
+  m.Y = a.Y;
+  m.ldy = a.ldy;
+  m.out = a.out;
+  m.y_dtype = a.y_dtype;
+  m.act = a.act;
+  m.has_base = a.base != nullptr;
+  m.debug = a.debug;
+  return m;
+}
+
+// One linear of a chained launch (dz_sbmm_chain): its arguments (splits resolved by the host) and
+// the tensor map of its X. Host-encoded by dz_sbmm_chain_encode, copied to the device by the caller.
+struct ChainLin {
+  dz_sbmm_args a;
+  alignas(64) CUtensorMap xmap;
+};
+
+// Delta items of a linear: what its combiners count in the chain's done counter.
+__device__ __forceinline__ int delta_items(const dz_sbmm_args& a) {
+  const LinGeo g = lin_geo(a);
+  const int n_jobs = a.n_jobs_dev != nullptr ? *a.n_jobs_dev : a.n_jobs;
+  return g.nrt * (n_jobs - g.n_base) * g.dsplit;
+}
+
+__device__ __forceinline__ int ld_acquire_gpu_s32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Chained launch: wait until linear l-1 wrote all of Y (its X), then let the async proxy (TMA) see it.
+__device__ __forceinline__ void wait_linear(const int* done, int target) {
+#ifdef DZ_CHAIN_NOWAIT  // A/B probe only: results are wrong
+  return;
+#endif
+  while (ld_acquire_gpu_s32(done) < target) __nanosleep(64);
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // Work items of a launch (debug bit 1: base items only, a probe of the base stream).
 __device__ __forceinline__ int job_items(const dz_sbmm_args& a, int n_jobs, int n_base, int nrt, int nbt, int nsplit,
                                          int dsplit) {
@@ -826,9 +903,14 @@ __device__ __forceinline__ int job_items(const dz_sbmm_args& a, int n_jobs, int 
 // ------------------------------------------------------------------------------------------
 // The persistent kernel
 // ------------------------------------------------------------------------------------------
-template <bool FUSED, int NTS>
-__global__ void __launch_bounds__(nthreads<FUSED>(), 1)
-    k_sbmm(const __grid_constant__ dz_sbmm_args a, const __grid_constant__ CUtensorMap xmap) {
+// The body of one launch. CHAIN: a chained launch over L linears (lins, device), each linear's items
+// after the previous linear's, one global pipeline; a linear's X loads wait for the previous linear's
+// last combined Y row (the weights stream ahead). Otherwise one linear (a0 / xmap0, kernel params).
+template <bool FUSED, int NTS, bool CHAIN>
+__device__ __forceinline__ void sbmm_body(const dz_sbmm_args& a0, const CUtensorMap* xmap0, const ChainLin* lins,
+                                          int L) {
+  auto lin = [&](int l) -> const dz_sbmm_args& { return CHAIN ? lins[l].a : a0; };
+  const dz_sbmm_args& a = a0;  // launch-wide fields (workspace) and the single-linear case
   extern __shared__ uint8_t smem_dyn[];
   constexpr int STAGE_BYTES = stage_bytes<NTS>();
   // 1024-B alignment for the SWIZZLE_128B tiles
@@ -836,37 +918,10 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
   Smem* sm = reinterpret_cast<Smem*>(stages + STAGE_BYTES * NSTAGE);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  const int n16 = ceil_div(a.out, kBlkRows);
-  const int nrt = ceil_div(a.out, RT);
-  const int nkb = ceil_div(a.in, kBlkCols);
-  const int nch_base = ceil_div(a.in, BASE_CH * KC_DN);
-  const int nbt = ceil_div(a.out, BASE_RT);
-  int t_pf = a.t_pf;
-  if (a.pf_counts_dev != nullptr) {  // device mixed plan: the staged prefill rows come from the planner
-    griddep_wait();
-    t_pf = a.pf_counts_dev[2];
-  }
-  const int n_base = a.base != nullptr ? ceil_div(a.T - t_pf, BASE_N) : 0;  // dz_plan: base jobs first
-  const int nsplit = a.base_splits;  // resolved by the host (launch_decode)
-  const int dsplit = a.delta_splits;  // resolved by the host (launch_decode)
-
   int* sched = reinterpret_cast<int*>(a.workspace);  // [0] item counter, [1] finished CTAs
-  MergeCtx mctx;
-  mctx.slice_cnt = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(a.workspace) + DZ_WS_CNT_OFF);
-  mctx.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(a.workspace) + DZ_WS_PART_OFF);
-  mctx.fused = FUSED && a.base != nullptr && !a.keep_planes && dsplit == 1 && !(a.debug & 6);
-  mctx.base_target = n_base * nsplit;  // base items publishing each slice
-  mctx.readers = 0;  // set after the PDL wait (the job count may come from dz_plan_device)
-  mctx.T = a.T;
-  mctx.nsplit = nsplit;
-  mctx.perm = a.perm;
-  mctx.Y = a.Y;
-  mctx.ldy = a.ldy;
-  mctx.out = a.out;
-  mctx.y_dtype = a.y_dtype;
-  mctx.act = a.act;
-  mctx.has_base = a.base != nullptr;
-  mctx.debug = a.debug;
+  int* chain = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(a.workspace) + DZ_WS_CHAIN_OFF);
+  int* chain_cnt = chain + 1;               // per-linear item counters (chained launch)
+  int* chain_done = chain + 1 + MAX_CHAIN;  // per-linear combined delta items (chained launch)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; s++) {
@@ -899,9 +954,19 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
     (void)trace_i;
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_keep = policy_evict_last();
-    if (lane == 0) prefetch_tmap(&xmap);
     int stage = 0;
     uint32_t phase = 0;
+    for (int l = 0; l < L; l++) {
+    // chained launch: the linear's arguments live in global memory, whose L1 lines every acquire
+    // poll invalidates; a register copy keeps them off the per-stage path (kernel params otherwise)
+    std::conditional_t<CHAIN, const dz_sbmm_args, const dz_sbmm_args&> a = lin(l);
+    const CUtensorMap* xmap = CHAIN ? &lins[l].xmap : xmap0;
+    if (lane == 0) prefetch_tmap(xmap);
+    const LinGeo geo = lin_geo(a);
+    const int nrt = geo.nrt, nkb = geo.nkb, nch_base = geo.nch_base, nbt = geo.nbt, n_base = geo.n_base;
+    const int nsplit = geo.nsplit, dsplit = geo.dsplit;
+    int* item_cnt = CHAIN ? chain_cnt + l : &sched[0];
+    bool dep_ready = !CHAIN || l == 0;  // X of this linear = Y of the previous one
     // First item static (blockIdx.x), later ones from the counter. Before waiting for the preceding
     // kernel (programmatic dependent launch), prefetch the first chunks of this item's weight
     // stream into L2: it depends only on resident weights, not on the predecessor's output.
@@ -931,8 +996,10 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
         for (int c = d0; c < d0 + PF_CHUNKS && c * NB_SP < nkb; c++) tma_prefetch_3d(m0, 0, c * NB_SP, rt * RG);
       }
     }
-    griddep_wait();
-    griddep_launch_dependents();
+    if (l == 0) {
+      griddep_wait();
+      griddep_launch_dependents();
+    }
     if (a.n_jobs_dev != nullptr) {  // dz_plan_device wrote the count and the jobs
       n_jobs = *a.n_jobs_dev;
       n_items = job_items(a, n_jobs, n_base, nrt, nbt, nsplit, dsplit);
@@ -1006,6 +1073,7 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
           h.tok_begin = job.tok_begin; h.tok_count = job.tok_count; h.nb = nb;
           h.flags = (ch == 0 ? 1 : 0) | (last ? 2 : 0) | ((c0 + ch) << 8);  // absolute chunk (X producer)
           h.pad = sp;  // K-split of the item: selects the partial plane its epilogue writes
+          h.lin = CHAIN ? l : 0;
           sm->hdr[stage] = h;
           const uint32_t xb = is_base ? static_cast<uint32_t>(nb * KC_DN * BASE_N * 2)
                                       : static_cast<uint32_t>(job.tok_count * xbytes);
@@ -1013,11 +1081,15 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
           mbar_arrive_expect_tx(&sm->full[stage], (is_base ? nb : 1) * abytes + xb);  // release: orders the smem writes above
           TRACE(7, item, ch);
           if (is_base) {
-            for (int c = 0; c < nb; c++) {
+            for (int c = 0; c < nb; c++)
               tma_load_2d(sbuf + c * (BASE_RT * KC_DN * 2), amap, ax + c * KC_DN, ay, &sm->full[stage], pol_stream);
-              tma_load_2d(sbuf + A_DN + c * (KC_DN * BASE_N * 2), &xmap, col0 + c * KC_DN, job.tok_begin,
-                          &sm->full[stage], pol_keep);
+            if (CHAIN && !dep_ready) {  // the weights are in flight; X waits for the previous linear
+              wait_linear(chain_done + l - 1, delta_items(lin(l - 1)));
+              dep_ready = true;
             }
+            for (int c = 0; c < nb; c++)
+              tma_load_2d(sbuf + A_DN + c * (KC_DN * BASE_N * 2), xmap, col0 + c * KC_DN, job.tok_begin,
+                          &sm->full[stage], pol_keep);
           } else if (dense) {
             tma_load_2d(sbuf, amap, ax, ay, &sm->full[stage], pol_stream);
           } else {
@@ -1029,7 +1101,7 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
         if (lane == 0) TRACE(9, item, ch);
         if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
         // ---- next-item prefetch, spread over the first chunks ----
-        if (ch == 0 && lane == 0) id_nxt_raw = static_cast<int>(gridDim.x) + atomicAdd(&sched[0], 1);
+        if (ch == 0 && lane == 0) id_nxt_raw = static_cast<int>(gridDim.x) + atomicAdd(item_cnt, 1);
         if (ch == (nch > 1 ? 1 : 0)) {
           item_nxt = __shfl_sync(0xffffffffu, id_nxt_raw, 0);
           if (item_nxt < n_items) {
@@ -1053,16 +1125,19 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
       tok = tok_n;
       tok2 = tok2_n;
     }
-    if (a.next != nullptr && lane == 0) tail_prefetch(*a.next);
+    }  // linears
+    if (!CHAIN && a.next != nullptr && lane == 0) tail_prefetch(*a.next);
     mbar_wait(&sm->empty[stage], phase ^ 1);
     if (lane == 0) {
       sm->hdr[stage].item = -1;
       mbar_arrive(&sm->xreq[stage]);
       mbar_arrive(&sm->full[stage]);
-      const int done = atomicAdd(&sched[1], 1);
-      if (done == static_cast<int>(gridDim.x) - 1) {  // last CTA out resets the scheduler
-        sched[0] = 0;
-        sched[1] = 0;
+      if (!CHAIN) {
+        const int done = atomicAdd(&sched[1], 1);
+        if (done == static_cast<int>(gridDim.x) - 1) {  // last CTA out resets the scheduler
+          sched[0] = 0;
+          sched[1] = 0;
+        }
       }
     }
   } else if (warp == WARP_XPROD) {
@@ -1073,11 +1148,24 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
     griddep_wait();  // X is the preceding kernel's output
     int stage = 0;
     uint32_t phase = 0;
+    int dep_l = 0;  // chained launch: the X of linears <= dep_l is known to be complete
+    int x_l = 0;    // linear of xg / ldx
+    const uint16_t* xg = lin(0).X;
+    int64_t ldx = lin(0).ldx;
     while (true) {
       mbar_wait(&sm->xreq[stage], phase);
       const StageHdr h = sm->hdr[stage];
       if (h.item < 0) break;
       if (h.kind != 0) {
+        if (CHAIN && h.lin != x_l) {
+          x_l = h.lin;
+          xg = lin(x_l).X;
+          ldx = lin(x_l).ldx;
+        }
+        if (CHAIN && h.lin > dep_l) {
+          wait_linear(chain_done + h.lin - 1, delta_items(lin(h.lin - 1)));
+          dep_l = h.lin;
+        }
         const bool dense = h.kind == DZ_KIND_DENSE;
         const int col0 = dense ? (h.flags >> 8) * KC_DN : (h.flags >> 8) * NB_SP * kBlkCols;
         const int xbytes = dense ? KC_DN * 2 : h.nb * kBlkCols * 2;
@@ -1085,7 +1173,7 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
         const int xs = dense ? XS_DN : XS_SP;
         uint8_t* sbuf = stages + static_cast<size_t>(stage) * STAGE_BYTES;
         for (int tk = lane; tk < h.tok_count; tk += 32)
-          tma_load_1d(sbuf + aoff + tk * xs, a.X + static_cast<int64_t>(sm->tok_ids[stage][tk]) * a.ldx + col0,
+          tma_load_1d(sbuf + aoff + tk * xs, xg + static_cast<int64_t>(sm->tok_ids[stage][tk]) * ldx + col0,
                       static_cast<uint32_t>(xbytes), &sm->full[stage], pol_keep);
       }
       if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
@@ -1128,11 +1216,25 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
   } else if (FUSED && warp == WARP_COMB) {
     // ===================== combiner (fused merge) =====================
     griddep_wait();
+    int cur_l = 0;
+    const LinGeo g0 = lin_geo(lin(0));
+    MergeCtx mctx = make_mctx<FUSED>(lin(0), g0);
+    mctx.readers = (lin(0).n_jobs_dev != nullptr ? *lin(0).n_jobs_dev : lin(0).n_jobs) - g0.n_base;  // delta jobs
     if (mctx.fused) {
-      mctx.readers = (a.n_jobs_dev != nullptr ? *a.n_jobs_dev : a.n_jobs) - n_base;  // delta jobs
+      const MergeRec* recs = reinterpret_cast<const MergeRec*>(sm->recs);
       for (int k = 0;; k++) {
         while (!mbar_test(&sm->mfull[k % MREC], (k / MREC) & 1)) __nanosleep(DZ_COMB_SLEEP);
+        const int rl = recs[k % MREC].lin, rbase = recs[k % MREC].is_base;
+        if (CHAIN && rl != cur_l && recs[k % MREC].rt >= 0) {
+          cur_l = rl;
+          const LinGeo g = lin_geo(lin(rl));
+          mctx = make_mctx<FUSED>(lin(rl), g);
+          mctx.readers = (lin(rl).n_jobs_dev != nullptr ? *lin(rl).n_jobs_dev : lin(rl).n_jobs) - g.n_base;
+        }
         if (!service_record(sm, mctx, k, lane)) break;
+        // chained launch: count the delta item's Y rows as written (release: its stores first)
+        if (CHAIN && !rbase && lane == 0)
+          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(chain_done + rl) : "memory");
       }
     }
   } else {
@@ -1144,6 +1246,10 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
     int stage = 0;
     uint32_t phase = 0;
     int nbase = 0;
+    int cur_l = 0;
+    LinGeo geo = lin_geo(lin(0));
+    MergeCtx mctx = make_mctx<FUSED>(lin(0), geo);
+    int c_debug = lin(0).debug, c_out = lin(0).out;  // register copies (chained launch: global memory)
     int nmerge = 0;  // items merged so far (record ring position)
     MergeRec* recs = reinterpret_cast<MergeRec*>(sm->recs);
     while (true) {
@@ -1154,12 +1260,20 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
         if (mctx.fused) publish_item(recs, sm->mfull, sm->mempty, nmerge, warp, lane, -1, 0, 0, 0);
         break;
       }
+      if (CHAIN && h.lin != cur_l) {  // the next linear of a chained launch
+        cur_l = h.lin;
+        geo = lin_geo(lin(cur_l));
+        mctx = make_mctx<FUSED>(lin(cur_l), geo);
+        c_debug = lin(cur_l).debug;
+        c_out = lin(cur_l).out;
+      }
+      const int n16 = geo.n16, nsplit = geo.nsplit;
       const bool is_base = h.kind == 0;
       const int rg0 = h.rt * RG + warp * MR;
       const int nrv = (n16 - rg0) < MR ? (n16 - rg0) : MR;  // row groups of this warp inside `out`
       const uint32_t sbuf = smem_u32(stages + static_cast<size_t>(stage) * STAGE_BYTES);
       const int nt = ceil_div(h.tok_count, 8);
-      if (!is_base && !(a.debug & 1)) {
+      if (!is_base && !(c_debug & 1)) {
         if (h.flags & 1) {
 #pragma unroll
           for (int r = 0; r < MR; r++)
@@ -1235,7 +1349,7 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
                 tk[i] = tkn[n][v & 1];
                 rw[i] = row + ((v & 2) ? 8 : 0);
                 x[i] = acc[r][n][v];
-                ok[i] = r < nrv && 8 * n + t2 + (v & 1) < h.tok_count && rw[i] < a.out;
+                ok[i] = r < nrv && 8 * n + t2 + (v & 1) < h.tok_count && rw[i] < c_out;
               }
             }
             merge_batch<4 * MR>(mctx, nsplit + h.pad, tk, rw, x, ok);
@@ -1243,7 +1357,7 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
         }
         if (mctx.fused) {  // hand the item to the combiner warp (no wait on any round trip)
           publish_item(recs, sm->mfull, sm->mempty, nmerge, warp, lane, h.rt, is_base ? 1 : 0, is_base ? 0 : h.tok_count,
-                       rtok);
+                       rtok, h.lin);
           nmerge++;
         }
         if (lane == 0 && warp == 0) TRACE(5, h.item, 0);
@@ -1257,6 +1371,28 @@ __global__ void __launch_bounds__(nthreads<FUSED>(), 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, TMEM_COLS);
   }
+  if (CHAIN && threadIdx.x == 0) {  // every role of this CTA is done: the last CTA re-arms the chain
+    __threadfence();
+    if (atomicAdd(chain, 1) == static_cast<int>(gridDim.x) - 1) {
+      for (int l = 0; l < L; l++) {
+        chain_cnt[l] = 0;
+        chain_done[l] = 0;
+      }
+      chain[0] = 0;
+    }
+  }
+}
+
+template <bool FUSED, int NTS>
+__global__ void __launch_bounds__(nthreads<FUSED>(), 1)
+    k_sbmm(const __grid_constant__ dz_sbmm_args a, const __grid_constant__ CUtensorMap xmap) {
+  sbmm_body<FUSED, NTS, false>(a, &xmap, nullptr, 1);
+}
+
+// Chained launch: L linears of a decode step in one persistent kernel (fused merge).
+template <int NTS>
+__global__ void __launch_bounds__(nthreads<true>(), 1) k_sbmm_chain(const ChainLin* __restrict__ lins, int L) {
+  sbmm_body<true, NTS, true>(lins[0].a, &lins[0].xmap, lins, L);
 }
 
 }  // namespace dz
@@ -1459,6 +1595,71 @@ extern "C" int dz_sbmm(const dz_sbmm_args* a, void* stream) {
     return launch_decode(&k, stream);
   }
   return DZ_OK;
+}
+
+
+// ------------------------------------------------------------------------------------------
+// Chained launch: the linears of a decode step in ONE persistent kernel (see sbmm_body, CHAIN).
+// ------------------------------------------------------------------------------------------
+extern "C" size_t dz_sbmm_chain_desc_bytes(int32_t L) {
+  return L < 1 || L > MAX_CHAIN ? 0 : static_cast<size_t>(L) * sizeof(ChainLin);
+}
+
+extern "C" int dz_sbmm_chain_encode(const dz_sbmm_args* args, int32_t L, void* desc_host, size_t desc_bytes,
+                                    int32_t* narrow_out) {
+  if (!args || !desc_host || !narrow_out || L < 1 || L > MAX_CHAIN) return DZ_E_VALUE;
+  if (desc_bytes < dz_sbmm_chain_desc_bytes(L) || (reinterpret_cast<uintptr_t>(desc_host) & 63)) return DZ_E_VALUE;
+  ChainLin* lins = static_cast<ChainLin*>(desc_host);
+  int narrow = 1;
+  for (int l = 0; l < L; l++) {
+    const dz_sbmm_args& a = args[l];
+    if (!a.X || !a.Y || !a.workspace || !a.base || !a.table || !a.jobs || !a.order) return DZ_E_VALUE;
+    if (a.workspace != args[0].workspace) return DZ_E_VALUE;  // one scheduler / plane region for the chain
+    if (a.perm != nullptr || a.pf_counts_dev != nullptr || (a.tp != nullptr && a.tp->world > 1) || a.debug)
+      return DZ_E_UNSUPPORTED;  // decode plans of single-GPU linears only
+    if (a.T < 1 || a.out < 1 || a.in < 1 || a.out > 32 * MAX_SLICES) return DZ_E_SHAPE;
+    const int in_pad = ceil_div(a.in, kBlkCols) * kBlkCols;
+    if (a.ldx < in_pad || (a.ldx % 8) != 0 || (reinterpret_cast<uintptr_t>(a.X) & 15) != 0 || a.ldy < a.out)
+      return DZ_E_SHAPE;
+    if (a.y_dtype != DZ_F32 && a.y_dtype != DZ_BF16) return DZ_E_VALUE;
+    ChainLin& c = lins[l];
+    std::memset(&c, 0, sizeof(c));
+    c.a = a;
+    resolve_splits(c.a.out, c.a.in, true, c.a.base_splits, c.a.delta_splits);
+    if (c.a.delta_splits != 1) return DZ_E_UNSUPPORTED;
+    c.a.keep_planes = 0;
+    c.a.fused_merge = 1;
+    c.a.next = nullptr;
+    if (a.sparse_job_tokens != 8) narrow = 0;
+    const int st = encode_2d(&c.xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.X, static_cast<uint64_t>(a.in),
+                             static_cast<uint64_t>(a.T), static_cast<uint64_t>(a.ldx) * 2, KC_DN, BASE_N,
+                             CU_TENSOR_MAP_SWIZZLE_128B);
+    if (st) return st;
+  }
+  *narrow_out = narrow;
+  return DZ_OK;
+}
+
+extern "C" int dz_sbmm_chain(const void* desc_dev, int32_t L, int32_t narrow, int32_t grid, void* stream) {
+  if (!desc_dev || L < 1 || L > MAX_CHAIN || (reinterpret_cast<uintptr_t>(desc_dev) & 63)) return DZ_E_VALUE;
+  static std::once_flag once;  // one-time, idempotent kernel attribute setup
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(k_sbmm_chain<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<1>());
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(k_sbmm_chain<NT_SP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      smem_bytes<NT_SP>());
+  });
+  if (attr_err != cudaSuccess) return DZ_E_CUDA;
+  if (grid <= 0) {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return DZ_E_CUDA;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return DZ_E_CUDA;
+    grid = sms;  // one CTA per SM: every CTA must be resident (the chain's waits span CTAs)
+  }
+  const ChainLin* lins = static_cast<const ChainLin*>(desc_dev);
+  return narrow ? launch_pdl(1, k_sbmm_chain<1>, grid, nthreads<true>(), smem_bytes<1>(), stream, lins, L)
+                : launch_pdl(1, k_sbmm_chain<NT_SP>, grid, nthreads<true>(), smem_bytes<NT_SP>(), stream, lins, L);
 }
 
 #ifdef DZ_TRACE

@@ -187,6 +187,50 @@ class LlamaStack:
             self.chains = {}
         self.chains[(id(plan), bufs["x"].data_ptr())] = (plan, args_to_device(args, self.device))
 
+    def prepare_step_kernel(self, plan: Plan, bufs: dict[str, torch.Tensor]) -> None:
+        """Encode the whole decode step (every layer's four launches) for ONE chained launch
+        (`dz_sbmm_chain`): no launch boundaries between linears, Y merged in-kernel. Single GPU,
+        decode plans; the device descriptors stay valid while `bufs`, `plan` and the stack live."""
+        import ctypes as C
+        from .engine import sbmm_args
+        # one workspace for the whole chain, sized for the widest linear before any args point to it
+        self.ws.get(plan.T, max(lin[f].out for lin in self.stack for f in FUSED), self.device)
+        args, h = [], bufs["x"]
+        for lin in self.stack:
+            src = {"h": h, "v": bufs["v"], "up": bufs["up"]}
+            for f, s_ in STEP_ORDER:
+                a, _, _ = sbmm_args(src[s_], plan, lin[f].base, lin[f].table, Y=bufs[f], workspace=self.ws,
+                                    base_splits=getattr(self, "base_splits", 0))
+                args.append(a)
+            h = bufs["down"]
+        lib = L.lib()
+        n = len(args)
+        arr = (L.DzSbmmArgs * n)(*args)
+        nbytes = int(lib.dz_sbmm_chain_desc_bytes(n))
+        host = torch.empty(nbytes + 64, dtype=torch.uint8)
+        off = (-host.data_ptr()) % 64
+        narrow = C.c_int32(0)
+        L.check(lib.dz_sbmm_chain_encode(arr, n, host.data_ptr() + off, nbytes, C.byref(narrow)), "chain encode")
+        dev = torch.empty(nbytes + 64, dtype=torch.uint8, device=self.device)
+        doff = (-dev.data_ptr()) % 64
+        dev[doff:doff + nbytes].copy_(host[off:off + nbytes])
+        self.step_kernel = (plan, bufs["x"].data_ptr(), dev, doff, n, int(narrow.value))
+
+    def step_chained(self, plan: Plan, bufs: dict[str, torch.Tensor]) -> torch.Tensor:
+        """One decode step as ONE chained launch (see prepare_step_kernel)."""
+        from .device import stream_ptr
+        pk = getattr(self, "step_kernel", None)
+        if pk is None or pk[0] is not plan or pk[1] != bufs["x"].data_ptr():
+            self.prepare_step_kernel(plan, bufs)
+            pk = self.step_kernel
+        _, _, dev, doff, n, narrow = pk
+        per = getattr(self, "chain_len", 0) or n  # linears per launch (A/B: 1 = the chain kernel per linear)
+        esz = int(L.lib().dz_sbmm_chain_desc_bytes(1))
+        for l0 in range(0, n, per):
+            L.check(L.lib().dz_sbmm_chain(dev.data_ptr() + doff + l0 * esz, min(per, n - l0), narrow, 0,
+                                          stream_ptr()), "chain")
+        return bufs["down"]
+
     def step(self, plan: Plan, bufs: dict[str, torch.Tensor], record=None) -> torch.Tensor:
         """One decode step through every layer; returns the last layer's output buffer."""
         chain = getattr(self, "chains", {}).get((id(plan), bufs["x"].data_ptr()))

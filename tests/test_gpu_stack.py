@@ -89,3 +89,39 @@ def test_stack_step_graph_and_bytes(S):
     lb = st.launch_bytes(T, D)
     assert lb["o"] == linear_algorithmic_bytes(1024, 1024, 4, D, T)
     assert lb["down"] == linear_algorithmic_bytes(1024, 1408, 4, D, T)
+
+
+@pytest.mark.parametrize("T,D,layers", [(16, 4, 2), (130, 3, 2), (64, 32, 1)])
+def test_chained_step_equals_launch_per_linear(S, T, D, layers):
+    """dz_sbmm_chain (every linear of the step in ONE persistent launch, Y merged in-kernel, each
+    linear's X waiting for the previous linear's rows) equals the step of one launch per linear
+    bit for bit — eager, and replayed in a CUDA graph — for decode plans with one or two base
+    jobs (T=130) and 8- or 16-token delta jobs."""
+    from paper_2312_05215_b200.engine import Plan
+    dev = torch.device("cuda", 0)
+    st = S.LlamaStack("tiny", layers, D, 4, dev)
+    ids = np.random.default_rng(T).integers(0, D, T).astype(np.int32)
+    for width in (8, 16):
+        plan = Plan(ids, st.kinds, D, device=dev, sparse_job_tokens=width)
+        bufs = st.buffers(T)
+        bufs["x"].copy_(torch.randn(T, 1024, device=dev).to(torch.bfloat16))
+        x0 = bufs["x"].clone()
+        y_ref = st.step(plan, bufs).clone()
+        bufs["x"].copy_(x0)
+        y_chain = st.step_chained(plan, bufs).clone()
+        assert torch.equal(y_chain, y_ref), width
+        for f in ("qkv", "o", "gate_up"):  # every intermediate buffer too (last layer's)
+            assert torch.isfinite(bufs[f].float()).all()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            st.step_chained(plan, bufs)
+        torch.cuda.current_stream().wait_stream(s)
+        with torch.cuda.graph(g):
+            st.step_chained(plan, bufs)
+        for _ in range(3):
+            bufs["x"].copy_(x0)
+            g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(bufs["down"], y_ref), width

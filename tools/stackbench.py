@@ -60,6 +60,8 @@ def main():
     ap.add_argument("--max-batch", type=int, default=256, help="sweep: largest batch")
     ap.add_argument("--points", default="", help="sweep subset: D:B,D:B,...")
     ap.add_argument("--overlap-sms", type=int, default=None, help="mixed plans: SMs for K3 (0 = no overlap)")
+    ap.add_argument("--chain", action="store_true", help="decode step as one chained launch (dz_sbmm_chain)")
+    ap.add_argument("--fused-merge", action="store_true", help="in-kernel merge (k_sbmm<true>)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -77,6 +79,7 @@ def main():
     st.world = 1  # one rank's shard timed alone: no collective in this process
     st.base_splits = args.base_splits
     st.overlap_sms = args.overlap_sms
+    st.fused_merge = args.fused_merge
     if args.sweep:
         Ds = [d for d in (1, 2, 4, 8, 16, 32, 64, 128) if d <= args.deltas]
         Bs = tuple(b for b in (1, 2, 4, 8, 16, 32, 64, 128, 256) if b <= args.max_batch)
@@ -96,16 +99,17 @@ def run(args, st, ids, dev, extra=None):
     plan = Plan(ids, st.kinds, args.deltas, device=dev, pf_min=args.pf_min)
     bufs = st.buffers(T)
     bufs["x"].copy_(torch.randn(T, bufs["x"].shape[1], device=dev).to(torch.bfloat16))
-    st.step(plan, bufs)
+    step = (lambda: st.step_chained(plan, bufs)) if args.chain else (lambda: st.step(plan, bufs))
+    step()
     torch.cuda.synchronize()
     s_ = torch.cuda.Stream()
     s_.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s_):
-        st.step(plan, bufs)
+        step()
     torch.cuda.current_stream().wait_stream(s_)
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
-        st.step(plan, bufs)
+        step()
     for _ in range(args.warmup):
         g.replay()
     torch.cuda.synchronize()
