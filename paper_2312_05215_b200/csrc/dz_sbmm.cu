@@ -95,15 +95,12 @@ constexpr int UMMA_M = 128;
 #ifndef DZ_NSTAGE
 #define DZ_NSTAGE 3
 #endif
-#ifndef DZ_BASE_CH
-#define DZ_BASE_CH 2
-#endif
 constexpr int NB_SP = DZ_NB_SP;           // sparse chunk = 4 blocks = 512 columns (one 3-D TMA box)
 constexpr int NT_SP = DZ_SPARSE_JOB_TOKENS / 8;  // most n-tiles per 2:4 job (dz_plan): the codes of a
                                                  // chunk are decoded once for all of the job's tokens
 constexpr int NT_DN = 4;                  // n-tiles per dense-delta job (32 tokens, dz_plan)
 constexpr int KC_DN = 64;                 // dense / base chunk = 64 columns
-constexpr int BASE_N = DZ_BASE_JOB_TOKENS; // tokens per base job == UMMA N (dz_plan)
+constexpr int BASE_N = DZ_BASE_JOB_TOKENS; // most tokens per base job (dz_plan's cut) = TMEM buffer stride
 constexpr int XS_SP = NB_SP * kBlkCols * 2 + 16;  // smem bytes per staged token row; +16 B so the
 constexpr int XS_DN = KC_DN * 2 + 16;             //   8 rows of an ldmatrix hit distinct banks
 constexpr int A_SP = RG * NB_SP * sparse_block_bytes(4);  // 53248
@@ -112,19 +109,35 @@ constexpr int x_sp() { return NTS * 8 * XS_SP; }          // 8320 per 8 tokens
 constexpr int DN_HALF = kDenseBlockBytes / 2;             // 2048
 constexpr int A_DN = RG * DN_HALF;                        // 32768 == 256 rows x 128 B (base W tile)
 constexpr int X_DN = 64 * XS_DN;                          // 9216 (>= 64 x 128 B swizzled X tile)
-constexpr int cmax(int x, int y) { return x > y ? x : y; }
+__host__ __device__ constexpr int cmax(int x, int y) { return x > y ? x : y; }
+__host__ __device__ constexpr int cmin(int x, int y) { return x < y ? x : y; }
 constexpr int NSTAGE = DZ_NSTAGE;
 constexpr int JOB_DN_TOK = BASE_N;        // largest token count of a job
 constexpr int BASE_RT = UMMA_M;           // rows per base item: one UMMA M tile (half a delta row tile)
-constexpr int BASE_CH = DZ_BASE_CH;             // 64-column K-chunks per base stage (32 KB of W in flight per stage)
+constexpr int SPLIT_CH = 2;               // base K-splits fall on 2-chunk (128-column) boundaries
 constexpr int TMEM_COLS = 2 * BASE_N;     // double-buffered fp32 accumulator, 128 lanes x 128 tokens
-constexpr uint32_t IDESC_BASE = umma_idesc_bf16(UMMA_M, BASE_N);
+// Base stage shape of a launch, from its token count T only (so never from the batch's composition):
+// UMMA N = bn (the X tile holds bn token rows) and bch 64-column K-chunks per stage. A narrow X tile
+// (T <= 32) leaves room for 3 W chunks, 48 KB of W in flight per stage instead of 32 KB. The
+// accumulation order of a token is the same for every (bn, bch): K-chunks in order, splits on
+// SPLIT_CH-chunk boundaries (profiles/r02_ab_base_n.txt).
+#ifndef DZ_BASE_BN64
+#define DZ_BASE_BN64 0  // bn = 64 for 32 < T <= 64: measured -1% on the 7B step (T = 64), off
+#endif
+__host__ __device__ constexpr int base_bn(int T) {
+  return T <= 32 ? cmin(32, BASE_N) : (DZ_BASE_BN64 && T <= 64) ? cmin(64, BASE_N) : BASE_N;
+}
+__host__ __device__ constexpr int base_bch(int bn) { return bn <= 32 ? 3 : 2; }
+__host__ __device__ constexpr int base_xoff(int bch) { return cmax(A_DN, bch * UMMA_M * KC_DN * 2); }
+__host__ __device__ constexpr int base_stage_bytes(int bn) {
+  return base_xoff(base_bch(bn)) + base_bch(bn) * KC_DN * bn * 2;
+}
 // Stage size of the instantiation for 2:4 jobs of up to NTS n-tiles (X rows staged per stage).
 template <int NTS>
 constexpr int stage_bytes() {
-  return (cmax(cmax(A_SP + x_sp<NTS>(), A_DN + X_DN), A_DN + BASE_CH * KC_DN * BASE_N * 2) + 1023) / 1024 * 1024;
+  return (cmax(cmax(cmax(A_SP + x_sp<NTS>(), A_DN + X_DN), base_stage_bytes(BASE_N)),
+               cmax(base_stage_bytes(32), base_stage_bytes(64))) + 1023) / 1024 * 1024;
 }
-constexpr int STAGE_BYTES = stage_bytes<1>();
 constexpr int PF_CHUNKS = 4;              // stages of the first item prefetched into L2 before the PDL wait
 // Workspace: [0, 256) scheduler words; [256, +4*MAX_SLICES) per-32-row-slice arrival counters;
 // then the fp32 partial planes [base K-splits + delta K-splits][T][out].
@@ -219,12 +232,20 @@ __host__ __device__ inline int delta_splits(int /*out*/, int /*in*/) { return 1;
 __host__ __device__ inline void resolve_splits(int out, int in, bool has_base, int& bs, int& ds) {
   if (bs <= 0) bs = base_splits(out, in);
   if (ds <= 0) ds = delta_splits(out, in);
-  const int nch_base = ceil_div(in, BASE_CH * KC_DN), nch_sp = ceil_div(ceil_div(in, kBlkCols), NB_SP);
+  const int nch_base = ceil_div(in, SPLIT_CH * KC_DN), nch_sp = ceil_div(ceil_div(in, kBlkCols), NB_SP);
   bs = bs > 4 ? 4 : bs;
   bs = bs > nch_base ? nch_base : bs;
   ds = ds > 2 ? 2 : ds;
   ds = ds > nch_sp ? nch_sp : ds;
   if (!has_base) ds = 1;  // single contributor: the delta writes Y directly
+}
+
+// K-chunk range [k0, k1) of base split sp of ns: splits cut whole SPLIT_CH-chunk units, whatever the
+// stage size, so a token's partial sums the same chunks in the same order for every bn / bch.
+__host__ __device__ inline void base_chunks(int in, int sp, int ns, int& k0, int& k1) {
+  const int nck = ceil_div(in, KC_DN), nsu = ceil_div(nck, SPLIT_CH);
+  k0 = SPLIT_CH * (sp * nsu / ns);
+  k1 = cmin(nck, SPLIT_CH * ((sp + 1) * nsu / ns));
 }
 
 __device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
@@ -478,11 +499,12 @@ __device__ __forceinline__ void merge_contribution(const MergeCtx& m, int slot, 
 
 // Base accumulators (TMEM, lane = output row, column = token) -> merge. Warp w drains half w/4
 // (rows 128*(w/4)..) of the tile, TMEM lanes 32*(w%4)..+31 (the lanes warp w may access).
+template <int BN>
 __device__ __forceinline__ void drain_base_accumulator(uint32_t tmem_acc, int warp, int lane, const MergeCtx& m,
                                                        int split, int row0, int tok_begin, int tcount) {
   // TMEM lane quarter q = warp % 4 (the hardware's warp -> lane restriction); the NW/4 warps of a
-  // quarter split the 64 token columns.
-  constexpr int PER = BASE_N / 16 / (NW / 4);  // 16-column chunks per warp
+  // quarter split the BN token columns.
+  constexpr int PER = BN / 16 / (NW / 4);  // 16-column chunks per warp
   const int q = warp & 3, part = warp >> 2;
   const int row = row0 + 32 * q + lane;
   const uint32_t taddr = tmem_acc + (static_cast<uint32_t>(32 * q) << 16);
@@ -493,12 +515,12 @@ __device__ __forceinline__ void drain_base_accumulator(uint32_t tmem_acc, int wa
     if (c0 * 16 >= tcount) break;
     uint32_t vv[2][16];
     tmem_ld16(taddr + c0 * 16, vv[0]);
-    if ((c0 + 1) * 16 < tcount) tmem_ld16(taddr + (c0 + 1) * 16, vv[1]);
+    if (c0 + 1 < (part + 1) * PER && (c0 + 1) * 16 < tcount) tmem_ld16(taddr + (c0 + 1) * 16, vv[1]);
     tmem_ld_wait();
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       const int c = c0 + h;
-      if (c * 16 >= tcount) break;
+      if (c >= (part + 1) * PER || c * 16 >= tcount) break;
       int tk[16], rw[16];
       float x[16];
       bool ok[16];
@@ -532,6 +554,13 @@ __device__ __forceinline__ void drain_base_accumulator(uint32_t tmem_acc, int wa
     merge_batch<16>(m, split, tk, rw, x, ok);
   }
 #endif
+}
+
+// The narrow-tile drain (T <= 32). Inline: out of line (__noinline__) measured ~1% slower on the
+// 7B step and at cfg5 points (the MergeCtx goes through the stack).
+__device__ __forceinline__ void drain_narrow(uint32_t tmem_acc, int warp, int lane, const MergeCtx& m, int split,
+                                          int row0, int tok_begin, int tcount) {
+  drain_base_accumulator<DZ_BASE_BN64 ? 64 : 32>(tmem_acc, warp, lane, m, split, row0, tok_begin, tcount);
 }
 
 // Dense-delta job partial (mma.sync fragments) -> merge.
@@ -626,7 +655,6 @@ constexpr int TAIL_PF_CHUNKS = DZ_TAIL_PF;
 __device__ __forceinline__ void tail_prefetch(const dz_sbmm_args& nx) {
   if (nx.perm != nullptr || nx.T <= 0) return;  // decode plans only
   const int nrt = ceil_div(nx.out, RT), nbt = ceil_div(nx.out, BASE_RT), nkb = ceil_div(nx.in, kBlkCols);
-  const int nch_base = ceil_div(nx.in, BASE_CH * KC_DN);
   const int n_base = nx.base != nullptr ? ceil_div(nx.T, BASE_N) : 0;
   const int n_jobs = nx.n_jobs_dev != nullptr ? *nx.n_jobs_dev : nx.n_jobs;
   int nsplit = nx.base_splits, dsplit = nx.delta_splits;
@@ -640,9 +668,10 @@ __device__ __forceinline__ void tail_prefetch(const dz_sbmm_args& nx) {
   const dz_native_delta* e = job.kind == 0 ? nx.base : nx.table + job.slot;
   const void* m = e->tmap;
   if (job.kind == 0) {
-    const int k0 = (sp * nch_base / nsplit) * BASE_CH * KC_DN;
-    for (int c = 0; c < TAIL_PF_CHUNKS * BASE_CH && k0 + c * KC_DN < nx.in; c++)
-      tma_prefetch_2d(m, k0 + c * KC_DN, rt * BASE_RT);
+    int k0, k1;
+    base_chunks(nx.in, sp, nsplit, k0, k1);
+    for (int c = k0; c < k0 + TAIL_PF_CHUNKS * base_bch(base_bn(nx.T)) && c < k1; c++)
+      tma_prefetch_2d(m, c * KC_DN, rt * BASE_RT);
   } else if (kind_dense(job.kind)) {
     const int d0 = sp * (2 * nkb) / dsplit;
     for (int c = d0; c < d0 + TAIL_PF_CHUNKS && c < 2 * nkb; c++) tma_prefetch_2d(m, c * (DN_HALF / 8), rt * RG);
@@ -824,14 +853,15 @@ __device__ __forceinline__ bool service_record(Smem* sm, const MergeCtx& mctx, i
 
 // Per-linear constants of a launch, or of one linear of a chained launch.
 struct LinGeo {
-  int n16, nrt, nkb, nch_base, nbt, n_base, nsplit, dsplit;
+  int n16, nrt, nkb, nbt, n_base, nsplit, dsplit, bn, bch;
 };
 __device__ __forceinline__ LinGeo lin_geo(const dz_sbmm_args& a) {
   LinGeo g;
   g.n16 = ceil_div(a.out, kBlkRows);
   g.nrt = ceil_div(a.out, RT);
   g.nkb = ceil_div(a.in, kBlkCols);
-  g.nch_base = ceil_div(a.in, BASE_CH * KC_DN);
+  g.bn = base_bn(a.T);
+  g.bch = base_bch(g.bn);
   g.nbt = ceil_div(a.out, BASE_RT);
   int t_pf = a.t_pf;
   if (a.pf_counts_dev != nullptr) {  // device mixed plan: the staged prefill rows come from the planner
@@ -963,7 +993,7 @@ __device__ __forceinline__ void sbmm_body(const dz_sbmm_args& a0, const CUtensor
     const CUtensorMap* xmap = CHAIN ? &lins[l].xmap : xmap0;
     if (lane == 0) prefetch_tmap(xmap);
     const LinGeo geo = lin_geo(a);
-    const int nrt = geo.nrt, nkb = geo.nkb, nch_base = geo.nch_base, nbt = geo.nbt, n_base = geo.n_base;
+    const int nrt = geo.nrt, nkb = geo.nkb, nbt = geo.nbt, n_base = geo.n_base, bn = geo.bn, bch = geo.bch;
     const int nsplit = geo.nsplit, dsplit = geo.dsplit;
     int* item_cnt = CHAIN ? chain_cnt + l : &sched[0];
     bool dep_ready = !CHAIN || l == 0;  // X of this linear = Y of the previous one
@@ -985,9 +1015,9 @@ __device__ __forceinline__ void sbmm_body(const dz_sbmm_args& a0, const CUtensor
       const dz_native_delta* e0 = job.kind == 0 ? a.base : a.table + job.slot;
       const void* m0 = e0->tmap;
       if (job.kind == 0) {
-        const int k0 = (sp * nch_base / nsplit) * BASE_CH * KC_DN;
-        for (int c = 0; c < PF_CHUNKS * BASE_CH && k0 + c * KC_DN < a.in; c++)
-          tma_prefetch_2d(m0, k0 + c * KC_DN, rt * BASE_RT);
+        int k0, k1;
+        base_chunks(a.in, sp, nsplit, k0, k1);
+        for (int c = k0; c < k0 + PF_CHUNKS * bch && c < k1; c++) tma_prefetch_2d(m0, c * KC_DN, rt * BASE_RT);
       } else if (dn) {
         const int d0 = sp * (2 * nkb) / dsplit;
         for (int c = d0; c < d0 + PF_CHUNKS && c < 2 * nkb; c++) tma_prefetch_2d(m0, c * (DN_HALF / 8), rt * RG);
@@ -1020,11 +1050,13 @@ __device__ __forceinline__ void sbmm_body(const dz_sbmm_args& a0, const CUtensor
       const dz_native_delta* ent = is_base ? a.base : a.table + job.slot;
       const void* amap = ent->tmap;  // address only: the descriptor stays in global memory
       const int bb = dense ? kDenseBlockBytes : sparse_block_bytes(kind_fbits(job.kind));
-      // base items stream K-chunks [c0, c0 + nch) of split sp; delta items all of K
-      const int nch_all = is_base ? nch_base : dense ? 2 * nkb : ceil_div(nkb, NB_SP);
-      const int ns = is_base ? nsplit : dsplit;
-      const int c0 = sp * nch_all / ns;
-      const int nch = (sp + 1) * nch_all / ns - c0;
+      // base items stream the K-chunks [kb0, kb1) of split sp, bch per stage; delta items stages
+      // [c0, c0 + nch) of split sp
+      int kb0 = 0, kb1 = 0;
+      if (is_base) base_chunks(a.in, sp, nsplit, kb0, kb1);
+      const int nch_all = dense ? 2 * nkb : ceil_div(nkb, NB_SP);
+      const int c0 = is_base ? 0 : sp * nch_all / dsplit;
+      const int nch = is_base ? ceil_div(kb1 - kb0, bch) : (sp + 1) * nch_all / dsplit - c0;
       const uint32_t abytes = is_base ? static_cast<uint32_t>(BASE_RT * KC_DN * 2)
                               : dense ? static_cast<uint32_t>(A_DN) : static_cast<uint32_t>(RG * NB_SP * bb);
       // Next item: its id is fetched after chunk 0 goes out (one item of lookahead per CTA keeps
@@ -1042,8 +1074,8 @@ __device__ __forceinline__ void sbmm_body(const dz_sbmm_args& a0, const CUtensor
         uint8_t* sbuf = stages + static_cast<size_t>(stage) * STAGE_BYTES;
         int nb, col0, xbytes, ax, ay;
         if (is_base) {
-          col0 = (c0 + ch) * BASE_CH * KC_DN;
-          nb = (a.in - col0) < KC_DN ? 1 : BASE_CH;  // K-chunks in this stage (no fully-OOB boxes)
+          col0 = (kb0 + ch * bch) * KC_DN;
+          nb = cmin(bch, kb1 - (kb0 + ch * bch));  // K-chunks in this stage (none fully out of bounds)
           xbytes = 0;
           ax = col0;
           ay = rt * BASE_RT;
@@ -1071,11 +1103,12 @@ __device__ __forceinline__ void sbmm_body(const dz_sbmm_args& a0, const CUtensor
           StageHdr h;
           h.item = item; h.rt = rt; h.kind = job.kind;
           h.tok_begin = job.tok_begin; h.tok_count = job.tok_count; h.nb = nb;
-          h.flags = (ch == 0 ? 1 : 0) | (last ? 2 : 0) | ((c0 + ch) << 8);  // absolute chunk (X producer)
+          // bits 2-4: bn / 32 of a base stage (the MMA's N and X layout); bits 8+: absolute chunk (X producer)
+          h.flags = (ch == 0 ? 1 : 0) | (last ? 2 : 0) | (is_base ? (bn >> 5) << 2 : 0) | ((c0 + ch) << 8);
           h.pad = sp;  // K-split of the item: selects the partial plane its epilogue writes
           h.lin = CHAIN ? l : 0;
           sm->hdr[stage] = h;
-          const uint32_t xb = is_base ? static_cast<uint32_t>(nb * KC_DN * BASE_N * 2)
+          const uint32_t xb = is_base ? static_cast<uint32_t>(nb * KC_DN * bn * 2)
                                       : static_cast<uint32_t>(job.tok_count * xbytes);
           TRACE(6, item, ch);
           mbar_arrive_expect_tx(&sm->full[stage], (is_base ? nb : 1) * abytes + xb);  // release: orders the smem writes above
@@ -1088,7 +1121,7 @@ __device__ __forceinline__ void sbmm_body(const dz_sbmm_args& a0, const CUtensor
               dep_ready = true;
             }
             for (int c = 0; c < nb; c++)
-              tma_load_2d(sbuf + A_DN + c * (KC_DN * BASE_N * 2), xmap, col0 + c * KC_DN, job.tok_begin,
+              tma_load_2d(sbuf + base_xoff(bch) + c * (KC_DN * bn * 2), xmap, col0 + c * KC_DN, job.tok_begin,
                           &sm->full[stage], pol_keep);
           } else if (dense) {
             tma_load_2d(sbuf, amap, ax, ay, &sm->full[stage], pol_stream);
@@ -1195,12 +1228,15 @@ __device__ __forceinline__ void sbmm_body(const dz_sbmm_args& a0, const CUtensor
         if (lane == 0) {
           const uint32_t sbuf = smem_u32(stages + static_cast<size_t>(stage) * STAGE_BYTES);
           const uint32_t tmem_d = tmem_base + buf * BASE_N;
+          const int bn = ((h.flags >> 2) & 7) << 5;
+          const int xoff = base_xoff(base_bch(bn));
+          const uint32_t idesc = umma_idesc_bf16(UMMA_M, bn);
           for (int c = 0; c < h.nb; c++) {
             const uint64_t adesc = umma_desc_sw128(sbuf + c * (BASE_RT * KC_DN * 2));
-            const uint64_t bdesc = umma_desc_sw128(sbuf + A_DN + c * (KC_DN * BASE_N * 2));
+            const uint64_t bdesc = umma_desc_sw128(sbuf + xoff + c * (KC_DN * bn * 2));
 #pragma unroll
             for (int k = 0; k < KC_DN / 16; k++)  // K=16 per MMA: +32 B inside the 128-B swizzle atom
-              umma_bf16(tmem_d, adesc + 2 * k, bdesc + 2 * k, IDESC_BASE, (h.flags & 1) && c == 0 && k == 0 ? 0u : 1u);
+              umma_bf16(tmem_d, adesc + 2 * k, bdesc + 2 * k, idesc, (h.flags & 1) && c == 0 && k == 0 ? 0u : 1u);
           }
           umma_commit(&sm->empty[stage]);
           if (h.flags & 2) umma_commit(&sm->tmem_full[buf]);
@@ -1326,8 +1362,11 @@ __device__ __forceinline__ void sbmm_body(const dz_sbmm_args& a0, const CUtensor
           const int buf = nbase & 1;
           mbar_wait(&sm->tmem_full[buf], (nbase >> 1) & 1);
           tc_fence_after();
-          drain_base_accumulator(tmem_base + buf * BASE_N, warp, lane, mctx, h.pad, h.rt * BASE_RT, h.tok_begin,
-                                 h.tok_count);
+          if (geo.bn == BASE_N)
+            drain_base_accumulator<BASE_N>(tmem_base + buf * BASE_N, warp, lane, mctx, h.pad, h.rt * BASE_RT,
+                                           h.tok_begin, h.tok_count);
+          else  // bn = 32 (or 64 with DZ_BASE_BN64; columns at or past tcount are skipped)
+            drain_narrow(tmem_base + buf * BASE_N, warp, lane, mctx, h.pad, h.rt * BASE_RT, h.tok_begin, h.tok_count);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm->tmem_empty[buf]);
@@ -1399,7 +1438,8 @@ __global__ void __launch_bounds__(nthreads<true>(), 1) k_sbmm_chain(const ChainL
 
 using namespace dz;
 
-static_assert(A_DN + BASE_CH * KC_DN * BASE_N * 2 <= stage_bytes<1>() && BASE_CH * BASE_RT * KC_DN * 2 <= A_DN,
+static_assert(base_stage_bytes(32) <= stage_bytes<1>() && base_stage_bytes(64) <= stage_bytes<1>() &&
+                  base_stage_bytes(BASE_N) <= stage_bytes<1>() && BASE_N % 32 == 0,
               "base stage layout");
 static_assert(NB_SP % PAIR1 == 0, "sparse stages hold whole block pairs");
 static_assert(DZ_SPARSE_JOB_TOKENS % 8 == 0 && NT_SP >= 1 && NT_SP <= NT_DN, "2:4 job = whole n-tiles");
@@ -1518,7 +1558,7 @@ static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
   if (attr_err != cudaSuccess) return DZ_E_CUDA;
   CUtensorMap xmap;  // X [T][in] bf16, 64-column x 128-token SWIZZLE_128B tiles (base UMMA B operand)
   int st = encode_2d(&xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a->X, static_cast<uint64_t>(a->in),
-                     static_cast<uint64_t>(a->T), static_cast<uint64_t>(a->ldx) * 2, KC_DN, BASE_N,
+                     static_cast<uint64_t>(a->T), static_cast<uint64_t>(a->ldx) * 2, KC_DN, base_bn(a->T),
                      CU_TENSOR_MAP_SWIZZLE_128B);
   if (st) return st;
   int grid = a->grid;
@@ -1632,7 +1672,7 @@ extern "C" int dz_sbmm_chain_encode(const dz_sbmm_args* args, int32_t L, void* d
     c.a.next = nullptr;
     if (a.sparse_job_tokens != 8) narrow = 0;
     const int st = encode_2d(&c.xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.X, static_cast<uint64_t>(a.in),
-                             static_cast<uint64_t>(a.T), static_cast<uint64_t>(a.ldx) * 2, KC_DN, BASE_N,
+                             static_cast<uint64_t>(a.T), static_cast<uint64_t>(a.ldx) * 2, KC_DN, base_bn(a.T),
                              CU_TENSOR_MAP_SWIZZLE_128B);
     if (st) return st;
   }

@@ -9,11 +9,17 @@ from . import _lib as L
 from .errors import CudaError
 
 
+_CUDA_OK = False  # set once the library loaded and a device was seen (checked on every call until then)
+
+
 def require_cuda() -> torch.device:
     """The product path has no CPU fallback: fail loudly without a GPU or the extension."""
-    L.lib()
-    if not torch.cuda.is_available():
-        raise CudaError("no CUDA device: the DeltaZip B200 path has no CPU fallback")
+    global _CUDA_OK
+    if not _CUDA_OK:
+        L.lib()
+        if not torch.cuda.is_available():
+            raise CudaError("no CUDA device: the DeltaZip B200 path has no CPU fallback")
+        _CUDA_OK = True
     return torch.device("cuda", torch.cuda.current_device())
 
 

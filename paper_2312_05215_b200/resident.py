@@ -9,7 +9,7 @@ it uploaded resident, keyed on the caller's objects:
   (weakref finalizer), so an id is never reused for a different object;
 * every hit re-checks a fingerprint: shape, dtype, strides and data pointer of each array, plus a
   CRC of a fixed sample of elements (`SAMPLE` evenly spaced values, plus `SAMPLE` evenly spaced
-  values of the first and of the last row).
+  values of the first and of the last row), gathered with one precomputed index array.
   Replacing an array or a field, or resizing, is always detected; an in-place edit of an array
   that was already passed is detected when it touches a sampled element. For arbitrary in-place
   edits call `invalidate(obj)` (or `clear()`), or pass a fresh array.
@@ -28,28 +28,40 @@ import numpy as np
 SAMPLE = 256
 
 
+_IDX: dict = {}  # (shape) -> flat indices of the sampled elements (one gather per fingerprint)
+
+
+def _sample_index(shape: tuple) -> np.ndarray:
+    idx = _IDX.get(shape)
+    if idx is None:
+        size = int(np.prod(shape))
+        parts = [np.arange(0, size, max(1, size // SAMPLE))]
+        if len(shape) == 2:  # the first and the last row
+            rs = max(1, shape[1] // SAMPLE)
+            parts += [np.arange(0, shape[1], rs), (shape[0] - 1) * shape[1] + np.arange(0, shape[1], rs)]
+        idx = np.concatenate(parts).astype(np.intp)
+        if len(_IDX) < 256:
+            _IDX[shape] = idx
+    return idx
+
+
 def _array_sig(a) -> tuple:
     a = np.asarray(a)
     sig = (a.shape, a.dtype.str, a.strides, a.__array_interface__["data"][0])
     if a.size == 0:
         return sig + (0,)
-    flat = a.reshape(-1) if a.flags.c_contiguous else np.ascontiguousarray(a).reshape(-1)
-    step = max(1, flat.size // SAMPLE)
-    crc = zlib.crc32(np.ascontiguousarray(flat[::step]).tobytes())
-    if a.ndim == 2:
-        rs = max(1, a.shape[1] // SAMPLE)
-        crc = zlib.crc32(np.ascontiguousarray(a[0, ::rs]).tobytes(), crc)
-        crc = zlib.crc32(np.ascontiguousarray(a[-1, ::rs]).tobytes(), crc)
-    return sig + (crc,)
+    flat = a.reshape(-1)  # a view for C-contiguous arrays, a copy otherwise
+    return sig + (zlib.crc32(flat.take(_sample_index(a.shape)).tobytes()),)
 
 
 def delta_sig(ld) -> tuple:
     """Fingerprint of a LayerDelta (compress.py:101-143): configuration, array identities and samples."""
-    idx = bytes(ld.index_stream) if not isinstance(ld.index_stream, bytes) else ld.index_stream
-    step = max(1, len(idx) // SAMPLE)
-    return (int(ld.rows), int(ld.cols), int(ld.bits), str(ld.sparsity), int(ld.group_size),
-            _array_sig(ld.packed_values), _array_sig(ld.scales), id(ld.index_stream), len(idx),
-            zlib.crc32(idx[::step]))
+    idx = ld.index_stream
+    n = len(idx)
+    step = max(1, n // SAMPLE)
+    samp = idx[::step] if isinstance(idx, (bytes, bytearray)) else bytes(memoryview(idx).cast("B")[::step])
+    return (ld.rows, ld.cols, ld.bits, ld.sparsity, ld.group_size,
+            _array_sig(ld.packed_values), _array_sig(ld.scales), id(idx), n, zlib.crc32(samp))
 
 
 class ResidentCache:
