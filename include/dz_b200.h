@@ -34,7 +34,8 @@ extern "C" {
 
 /* ---- plan granularity ---------------------------------------------------------------- */
 #ifndef DZ_BASE_JOB_TOKENS
-#define DZ_BASE_JOB_TOKENS 128 /* tokens per base-GEMM job of the decode kernel (its UMMA N) */
+#define DZ_BASE_JOB_TOKENS 128 /* tokens per base-GEMM job of the decode kernel (its largest UMMA N; a
+                                   launch of <= 32 tokens runs its base stages at N = 32) */
 #endif
 #define DZ_SPARSE_JOB_TOKENS 16  /* most tokens per 2:4 delta job of the decode kernel (2 mma.sp n-tiles);
                                     the planners take the job width (8 or 16; 0 = 8) as an argument */

@@ -1,8 +1,9 @@
 """GPU: decode-path (K2) merge and base K-split properties. Every output element is the fixed-order
-sum of the base K-split partials and the token's delta partial, done inside k_sbmm by the warp
-that completes each 32-row output slice (arrival counters in the workspace), so results are
-deterministic, independent of the batch for a given split count, and within fp32 rounding of
-each other across split counts."""
+sum of the base K-split partials and the token's delta partial (k_finalize by default, or the
+fused combiner warp), so results are deterministic, independent of the batch for a given split
+count, and within fp32 rounding of each other across split counts. The base stage shape depends
+on the launch's token count (narrow 32-row X tile and 3 W chunks per stage at T <= 32), never on
+which tokens share the batch, so a token's row is bit-identical across batch sizes."""
 
 import numpy as np
 import pytest
@@ -47,6 +48,31 @@ def test_base_splits_agree_and_batch_invariant(E, rows, cols):
         assert rel < 1e-5, rel
     R = O.sbmm_matrix(W.float().double().cpu().numpy(), dict(enumerate(ods)), ids, X.float().double().cpu().numpy())
     err = np.linalg.norm(ys[4].double().cpu().numpy() - R, axis=1) / np.linalg.norm(R, axis=1)
+    assert err.max() <= 1e-2
+
+
+@pytest.mark.parametrize("rows,cols", [(256, 11008), (130, 2944)])
+def test_narrow_base_stage_batch_invariant(E, rows, cols):
+    """T <= 32 launches use the narrow base stage (UMMA N 32, 3 K-chunks per stage), larger ones the
+    wide one (N 128, 2 chunks): same K-split boundaries and chunk order, so every row agrees bit
+    for bit across T = 1, 32, 33, 64 at each split count, and with the reference algorithm."""
+    rng = np.random.default_rng(rows * 7 + cols)
+    D, T = 3, 64
+    ods = [O.random_packed_delta(rng, rows, cols, 4) for _ in range(D)]
+    table = E.DeltaTable([E.NativeDelta.from_layer_delta(o) for o in ods], rows, cols)
+    W = (torch.randn(rows, cols, device="cuda") / np.sqrt(cols)).to(torch.bfloat16)
+    base = E.NativeBase(W)
+    ids = rng.integers(0, D, T).astype(np.int32)
+    X = torch.randn(T, cols, device="cuda").to(torch.bfloat16)
+    for sp in (1, 2, 3):
+        y = E.sbmm_forward(X, E.Plan(ids, table.kinds, D), base, table, y_dtype=torch.float32, base_splits=sp)
+        for n in (1, 32, 33):
+            sel = np.arange(T - n, T)
+            ysub = E.sbmm_forward(X[T - n:].contiguous(), E.Plan(ids[sel], table.kinds, D), base, table,
+                                  y_dtype=torch.float32, base_splits=sp)
+            assert torch.equal(ysub, y[T - n:]), (sp, n)
+    R = O.sbmm_matrix(W.float().double().cpu().numpy(), dict(enumerate(ods)), ids, X.float().double().cpu().numpy())
+    err = np.linalg.norm(y.double().cpu().numpy() - R, axis=1) / np.linalg.norm(R, axis=1)
     assert err.max() <= 1e-2
 
 

@@ -1,6 +1,7 @@
 """Per-item timeline of one fused launch across ALL CTAs (DZ_TRACE build).
 
-  DZ_B200_LIB=paper_2312_05215_b200/_dz_b200_trace.so python tools/item_trace.py [out in]
+  DZ_B200_LIB=paper_2312_05215_b200/_dz_b200_trace.so python tools/item_trace.py [out in [T D]]
+  (FLUSH=1: the traced launch reads cold, L2 flushed before it)
 Prints item-duration stats by kind, the CTA busy fraction and the tail.
 """
 import ctypes as C
@@ -16,7 +17,7 @@ from paper_2312_05215_b200.engine import DeltaTable, NativeBase, Plan, Workspace
 from paper_2312_05215_b200.synth import random_base, random_native_delta  # noqa: E402
 
 out, inp = (int(sys.argv[1]), int(sys.argv[2])) if len(sys.argv) > 2 else (4096, 4096)
-T, D = 64, 32
+T, D = (int(sys.argv[3]), int(sys.argv[4])) if len(sys.argv) > 4 else (64, 32)
 dev = torch.device("cuda")
 gen = torch.Generator(device=dev)
 gen.manual_seed(1)
@@ -30,6 +31,8 @@ ws = Workspace()
 for _ in range(3):
     sbmm_forward(X, plan, base, table, workspace=ws)
 torch.cuda.synchronize()
+if os.environ.get("FLUSH") == "1":
+    torch.empty(256 << 20, dtype=torch.uint8, device=dev).zero_()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 sbmm_forward(X, plan, base, table, workspace=ws)
