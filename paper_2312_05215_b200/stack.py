@@ -166,7 +166,8 @@ class LlamaStack:
         sbmm_forward(X, plan, lin.base, lin.table, Y=Y, workspace=self.ws, tp=self.peers if fused else None,
                      base_splits=getattr(self, "base_splits", 0), next_args=next_args,
                      overlap_sms=getattr(self, "overlap_sms", None),
-                     fused_merge=getattr(self, "fused_merge", False))
+                     fused_merge=getattr(self, "fused_merge", False),
+                     prefill_variant=getattr(self, "prefill_variant", 0))
         if lin.row_parallel and self.world > 1 and not fused:
             import torch.distributed as dist
             dist.all_reduce(Y, op=dist.ReduceOp.SUM, group=self.group)

@@ -62,6 +62,7 @@ def main():
     ap.add_argument("--overlap-sms", type=int, default=None, help="mixed plans: SMs for K3 (0 = no overlap)")
     ap.add_argument("--chain", action="store_true", help="decode step as one chained launch (dz_sbmm_chain)")
     ap.add_argument("--fused-merge", action="store_true", help="in-kernel merge (k_sbmm<true>)")
+    ap.add_argument("--prefill-variant", type=int, default=0, help="K3 delta product (0 sparse, 1/2 dense MT=1/2)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -80,6 +81,7 @@ def main():
     st.base_splits = args.base_splits
     st.overlap_sms = args.overlap_sms
     st.fused_merge = args.fused_merge
+    st.prefill_variant = args.prefill_variant
     if args.sweep:
         Ds = [d for d in (1, 2, 4, 8, 16, 32, 64, 128) if d <= args.deltas]
         Bs = tuple(b for b in (1, 2, 4, 8, 16, 32, 64, 128, 256) if b <= args.max_batch)
