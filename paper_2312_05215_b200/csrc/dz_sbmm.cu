@@ -917,9 +917,6 @@ __device__ __forceinline__ int ld_acquire_gpu_s32(const int* p) {
 
 // Chained launch: wait until linear l-1 wrote all of Y (its X), then let the async proxy (TMA) see it.
 __device__ __forceinline__ void wait_linear(const int* done, int target) {
-#ifdef DZ_CHAIN_NOWAIT  // A/B probe only: results are wrong
-  return;
-#endif
   while (ld_acquire_gpu_s32(done) < target) __nanosleep(64);
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
