@@ -41,6 +41,7 @@ from .inference import (
     tp_partition,
 )
 
+from .device import set_nvtx
 from .resident import clear as clear_resident_cache, invalidate as invalidate_resident
 from .formats import CompressConfig, CompressedDelta, inspect_delta, read_delta, write_delta
 from .solver import CalibrationSet, compress_model, compute_hessian, obs_compress_layer

@@ -23,6 +23,25 @@ def require_cuda() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_NVTX = [False]  # NVTX ranges around launches / layers / API calls (nsys, ncu --nvtx); off by default
+
+
+def set_nvtx(on: bool = True) -> None:
+    """Annotate launches (`dz_sbmm <out>x<in> T=<T>`), stack layers and drop-in API calls with NVTX
+    ranges, for nsys timelines and `ncu --nvtx --nvtx-include`. Off: one list lookup per call."""
+    _NVTX[0] = bool(on)
+
+
+def nvtx_push(name: str) -> None:
+    if _NVTX[0]:
+        torch.cuda.nvtx.range_push(name)
+
+
+def nvtx_pop() -> None:
+    if _NVTX[0]:
+        torch.cuda.nvtx.range_pop()
+
+
 def stream_ptr() -> int:
     """cudaStream_t of the current stream (the raw handle; torch.cuda.current_stream() builds a
     Python Stream object per call, a measurable share of a small drop-in call)."""

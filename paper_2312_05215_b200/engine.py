@@ -22,7 +22,7 @@ import torch
 
 from . import _lib as L
 from .compress import SPARSITY_2_4, dequantize_layer_device
-from .device import ErrFlag, RefDeltaDevice, require_cuda, stream_ptr
+from .device import _NVTX, ErrFlag, RefDeltaDevice, nvtx_pop, nvtx_push, require_cuda, stream_ptr
 from .errors import ShapeError, UnknownDeltaError
 
 BLK_ROWS, BLK_COLS = 16, 128
@@ -306,6 +306,19 @@ def sbmm_forward(X: torch.Tensor, plan: Plan, base: NativeBase | None, table: De
     default: both kernels need every SM — K3 its tensor cores, K2 its decode warps — so a split
     measured 2-19% slower on cfg3, profiles/r02_ab_cfg3_overlap.txt; -1: the split from
     `split_sms`)."""
+    if _NVTX[0]:
+        nvtx_push(f"dz_sbmm {table.out}x{table.inp} T={X.shape[0]}")
+        try:
+            return _sbmm_forward(X, plan, base, table, y_dtype, act, Y, workspace, grid, debug, base_splits, tp,
+                                 delta_splits, next_args, prefill_variant, fused_merge, overlap_sms)
+        finally:
+            nvtx_pop()
+    return _sbmm_forward(X, plan, base, table, y_dtype, act, Y, workspace, grid, debug, base_splits, tp,
+                         delta_splits, next_args, prefill_variant, fused_merge, overlap_sms)
+
+
+def _sbmm_forward(X, plan, base, table, y_dtype, act, Y, workspace, grid, debug, base_splits, tp, delta_splits,
+                  next_args, prefill_variant, fused_merge, overlap_sms) -> torch.Tensor:
     a, Y, keep = sbmm_args(X, plan, base, table, y_dtype, act, Y, workspace, grid, debug, base_splits, tp,
                            delta_splits)
     a.prefill_variant = prefill_variant

@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from .device import ErrFlag
+from .device import ErrFlag, nvtx_pop, nvtx_push
 from .engine import DeltaTable, NativeBase, NativeDelta, Plan, Workspace, concat_rows, sbmm_forward
 from .synth import delta_algorithmic_bytes, llama_linears, random_base, random_native_delta
 
@@ -238,7 +238,8 @@ class LlamaStack:
         use_chain = chain is not None and chain[0] is plan and self.world == 1
         n_lin = len(self.stack) * len(STEP_ORDER)
         h, k = bufs["x"], 0
-        for lin in self.stack:
+        for li, lin in enumerate(self.stack):
+            nvtx_push(f"layer {li}")
             src = {"h": h, "v": bufs["v"], "up": bufs["up"]}
             for f, s_ in STEP_ORDER:
                 if record is not None:
@@ -249,6 +250,7 @@ class LlamaStack:
                     record(f, "end")
                 k += 1
             h = bufs["down"]
+            nvtx_pop()
         return h
 
     # ------------------------------------------------------------------ bytes

@@ -86,6 +86,13 @@ def test_stack_step_graph_and_bytes(S):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(bufs["down"], y_eager)
+    # NVTX-annotated step (set_nvtx): same launches, same bits
+    from paper_2312_05215_b200 import set_nvtx
+    set_nvtx(True)
+    try:
+        assert torch.equal(st.step(plan, bufs), y_eager)
+    finally:
+        set_nvtx(False)
     lb = st.launch_bytes(T, D)
     assert lb["o"] == linear_algorithmic_bytes(1024, 1024, 4, D, T)
     assert lb["down"] == linear_algorithmic_bytes(1024, 1408, 4, D, T)

@@ -53,3 +53,17 @@ def test_disabled_cache_always_builds():
     for _ in range(3):
         c.get(a, R._array_sig, lambda: calls.append(1))
     assert len(calls) == 3 and len(c) == 0
+
+
+def test_nvtx_ranges_toggle():
+    """NVTX annotation is opt-in (set_nvtx) and balanced push/pop works without a GPU."""
+    import paper_2312_05215_b200 as P
+    from paper_2312_05215_b200 import device
+    assert device._NVTX[0] is False
+    P.set_nvtx(True)
+    try:
+        device.nvtx_push("dz test")
+        device.nvtx_pop()
+    finally:
+        P.set_nvtx(False)
+    assert device._NVTX[0] is False
