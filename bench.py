@@ -353,6 +353,12 @@ def main():
     plan = Plan(ids, kinds, D_DELTAS, device=device)
     assert plan.t_pf == 0  # 2 tokens per delta: pure decode plan
     bufs = st.buffers(T_TOKENS)
+    # random token activations (N(0, 1), bf16): the stack's buffers start at zero, and an all-zero
+    # step draws less power and clocks ~3% higher under the power cap than real data
+    # (profiles/r02_e2e_zero_inputs.txt)
+    gen_x = torch.Generator(device=device)
+    gen_x.manual_seed(1234 + rank)
+    bufs["x"].copy_(torch.randn(T_TOKENS, bufs["x"].shape[1], generator=gen_x, device=device).to(torch.bfloat16))
     tail_pf = world == 1 and os.environ.get("DZ_TAIL_PREFETCH", "1") != "0"
     if tail_pf:  # each launch warms L2 with the next launch's first weight stages at its tail
         st.prepare_chain(plan, bufs)
@@ -534,13 +540,16 @@ def main():
             "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (random bf16 base, random reference-layout 4-bit 2:4 deltas uploaded via dz_repack_sparse)",
+            "data": "synthetic (random bf16 base, random reference-layout 4-bit 2:4 deltas uploaded via dz_repack_sparse, "
+                    "random N(0,1) bf16 token activations)",
             "config": {"workload": WORKLOAD.format(layers=args.layers),
                        "global_batch": T_TOKENS,
                        "parallelism": (f"tp{world}" + ("+peer-memory reduce" if fused_tp else "+nccl all-reduce"))
                        if world > 1 else "single",
                        "l2": "inputs > L2 (97.5 GB streamed per step at N=1)", "cuda_graph": graph is not None,
-                       "step_bytes_rank0": step_bytes},
+                       "step_bytes_rank0": step_bytes,
+                       "output_rms": float(bufs["down"].float().pow(2).mean().sqrt()),
+                       "output_finite": bool(torch.isfinite(bufs["down"]).all())},
             "gpu_launches": (1 if args.fused_merge else 2) * len(order) * args.steps,  # k_sbmm (+ k_finalize) per fused linear
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_algorithmic": traffic_alg, "peak_kind": peak_kind,
