@@ -3,20 +3,21 @@
 // Replaces inference.sbmm (inference.py:126-154): y_t = W_base x_t + ΔW_{slot(t)} x_t.
 //
 // Work decomposition. An item is (row tile, job); a job is either the base GEMM for up to 128
-// tokens (row tile = 128 rows, one UMMA M tile) or one delta group for up to 8 (2:4 sparse) / 32
-// (dense) of its tokens (row tile = 256 rows; dz_plan = group_by_delta, inference.py:106-123).
+// tokens (row tile = 128 rows, one UMMA M tile) or one delta group for up to 8 or 16 (2:4 sparse:
+// the plan's job width, one kernel instantiation each) / 32 (dense) of its tokens (row tile = 256
+// rows; dz_plan = group_by_delta, inference.py:106-123).
 // Base items come first, then delta items row-tile-major; one persistent CTA per SM pulls items
 // from a self-resetting atomic counter with one item of lookahead.
 //
 // Warp roles per CTA (11 warps):
-//  * TMA producer (1 warp): per stage ONE tensor copy of the A operand — two 64-col x 128-row
-//    SWIZZLE_128B tiles of the base W in its natural layout, or a 3-D box of 4 native blocks x 16
-//    row groups of a delta (53 KB) — plus, for base stages, the swizzled X tile (contiguous tokens,
-//    OOB rows zero-filled). 3-deep ring with full/empty mbarriers; the next item's id, descriptor
+//  * TMA producer (1 warp): per stage ONE tensor copy of the A operand — two (three when the
+//    launch has <= 32 tokens) 64-col x 128-row SWIZZLE_128B tiles of the base W in its natural
+//    layout, or a 3-D box of 4 native blocks x 16 row groups of a delta (53 KB) — plus, for base
+//    stages, the swizzled X tile (bn = 128 or 32 contiguous token rows, OOB rows zero-filled). 3-deep ring with full/empty mbarriers; the next item's id, descriptor
 //    and token ids are prefetched while the current item streams.
 //  * X producer (1 warp): one 1-D bulk copy per routed token row of a delta stage.
 //  * MMA issuer (1 warp, one elected thread): base stages become tcgen05.mma kind::f16 (M=128,
-//    N=128 tokens, K=16 x 8 per stage) into a double-buffered TMEM accumulator; tcgen05.commit
+//    N=bn tokens, K=16 per MMA) into a double-buffered TMEM accumulator; tcgen05.commit
 //    frees the stage and, on the last chunk, signals the accumulator full.
 //  * consumers (8 warps, two 16-row groups each): 2:4 delta stages — decode codes in registers
 //    (LOP3 magic-number bf16 conversion; deferred per-(row,128-col) scaling) and mma.sp m16n8k32
@@ -29,8 +30,9 @@
 //  * default: k_finalize (one short launch) sums the planes in a fixed order and writes Y;
 //  * fused (k_sbmm<true>): a 12th "combiner" warp per CTA writes Y for each delta item's tokens
 //    once the base partials of its rows are published (per-32-row-slice counters), so no second
-//    launch. Measured ~1% slower on the 7B step and 5-10% slower at cfg5 points than the
-//    k_finalize path on the same box (profiles/r02_ab_fused_merge.txt), hence opt-in.
+//    launch. Measured 1-3% slower on the 7B step and 5-20% slower at cfg5 points than the
+//    k_finalize path on the same box (profiles/r02_ab_fused_merge.txt, r02_ab_chain.txt), hence
+//    opt-in. The same body also runs a whole decode step as one chained launch (k_sbmm_chain).
 // Both are deterministic and batch-invariant: the summation order is fixed per element.
 //
 // Mixed batches: groups large enough for the tensor-core prefill kernel (K3, dz_prefill.cu) are
