@@ -1593,11 +1593,12 @@ static int launch_decode(const dz_sbmm_args* a_in, void* stream) {
 }
 
 extern "C" int dz_sbmm(const dz_sbmm_args* a, void* stream) {
-  if (!a || !a->X || !a->Y || !a->workspace) return DZ_E_VALUE;
+  if (!a) return DZ_E_VALUE;
+  if (a->T < 0 || a->out < 1 || a->in < 1 || a->out > 32 * MAX_SLICES) return DZ_E_SHAPE;
+  if (a->T == 0 || a->n_jobs == 0) return DZ_OK;  // nothing to compute (empty X / Y may be null)
+  if (!a->X || !a->Y || !a->workspace) return DZ_E_VALUE;
   if (a->tp != nullptr && a->tp->world > 1 && (a->perm != nullptr || a->base == nullptr))
     return DZ_E_UNSUPPORTED;  // the fused reduction takes decode plans with a base
-  if (a->T < 0 || a->out < 1 || a->in < 1 || a->out > 32 * MAX_SLICES) return DZ_E_SHAPE;
-  if (a->T == 0 || a->n_jobs == 0) return DZ_OK;
   const int in_pad = ceil_div(a->in, kBlkCols) * kBlkCols;
   if (a->ldx < in_pad || (a->ldx % 8) != 0 || (reinterpret_cast<uintptr_t>(a->X) & 15) != 0) return DZ_E_SHAPE;
   if (a->ldy < a->out) return DZ_E_SHAPE;
