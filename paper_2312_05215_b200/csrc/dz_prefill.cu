@@ -596,9 +596,10 @@ static int launch_prefill(const dz_sbmm_args& k, const CUtensorMap& xmap, int gr
 // Items of 128 or 256 rows: the one with fewer item rounds per SM, weighted by the measured
 // per-item efficiency (MT=2 shares each X tile between two M tiles). Results are identical.
 extern "C" int dz_sbmm_prefill(const dz_sbmm_args* a, void* stream) {
-  if (!a || !a->Y || !a->table || !a->jobs) return DZ_E_VALUE;
+  if (!a) return DZ_E_VALUE;
   if (a->T < 0 || a->out < 1 || a->in < 1) return DZ_E_SHAPE;
-  if (a->n_pf_jobs <= 0 || a->T == 0) return DZ_OK;
+  if (a->n_pf_jobs <= 0 || a->T == 0) return DZ_OK;  // nothing to compute
+  if (!a->Y || !a->table || !a->jobs) return DZ_E_VALUE;
   const uint16_t* X = a->X;  // the staged buffer (dz_sbmm passes it as X with its row stride)
   if (!X) return DZ_E_VALUE;
   if ((a->ldx % 8) != 0 || (reinterpret_cast<uintptr_t>(X) & 15) != 0 || a->ldx < a->in) return DZ_E_SHAPE;
